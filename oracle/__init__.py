@@ -1,0 +1,201 @@
+"""CPU oracle for the derived-convolution hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baseline``
+leg and ``--impl reference``) may import this package.  The product package
+``paper_2208_02025_b200`` never imports it and shares no code with it; the two
+meet only in the seeded input generators of ``ollie_synth.py``.
+
+Everything is fp64.  Conv / ConvT / GEMM / OffsetAdd / selective-add / weight DLT
+are nested C loops in ``conv_oracle.c`` (built with gcc, OpenMP); the eOperator
+interpreter is pure Python in ``eop_oracle.py`` (small cases only).
+
+Pins (all in ``tests/test_oracle_*.py``, marked ``not gpu``): brute force by
+explicit im2col, torch CPU fp64 ``F.conv2d`` / ``F.conv_transpose2d`` as an
+independent library, the all-ones worked example, closed forms,
+adjointness, the derivation identity, the row-wrap sentinel (Q5),
+the ConvT tap table, identity / permutation / round-trip checks for eOps.
+No function here is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+from .eop_oracle import eop_eval, eop_is_identity, eop_bounds_ok  # noqa: F401
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "conv_oracle.c")
+_LIB_DIR = os.path.join(_HERE, "_build")
+_LIB = os.path.join(_LIB_DIR, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+_i64 = ctypes.c_int64
+_dp = ctypes.POINTER(ctypes.c_double)
+
+
+def build_oracle(force: bool = False) -> str:
+    """Compile conv_oracle.c with gcc (-O2 -fopenmp).  Building the checker is not using it."""
+    os.makedirs(_LIB_DIR, exist_ok=True)
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11",
+                               "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            lib = ctypes.CDLL(build_oracle())
+            I = _i64
+            lib.oracle_conv_out_size.restype = I
+            lib.oracle_conv_out_size.argtypes = [I] * 5
+            lib.oracle_convt_out_size.restype = I
+            lib.oracle_convt_out_size.argtypes = [I] * 6
+            lib.oracle_conv2d.argtypes = [I] * 10 + [_dp] * 3
+            lib.oracle_convtranspose2d.argtypes = [I] * 11 + [_dp] * 3
+            lib.oracle_gemm_nt.argtypes = [I] * 3 + [_dp] * 3
+            lib.oracle_weight_dlt_conv2d.argtypes = [I] * 4 + [_dp] * 2
+            lib.oracle_weight_dlt_convt.argtypes = [I] * 4 + [_dp] * 2
+            lib.oracle_offset_add.argtypes = [I] * 9 + [_dp] * 2
+            lib.oracle_selective_add.argtypes = [I] * 10 + [_dp] * 2
+            lib.oracle_num_threads.restype = ctypes.c_int
+            _lib = lib
+    return _lib
+
+
+def _f64(a) -> np.ndarray:
+    """Upcast the (already rounded) generated values to contiguous fp64."""
+    if hasattr(a, "detach"):  # torch tensor
+        a = a.detach().to("cpu").double().numpy()
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+def num_threads() -> int:
+    return int(_load().oracle_num_threads())
+
+
+def conv_out_size(n, k, pad, stride, dil) -> int:
+    return int(_load().oracle_conv_out_size(n, k, pad, stride, dil))
+
+
+def convt_out_size(n, k, pad, stride, dil, opad=0) -> int:
+    return int(_load().oracle_convt_out_size(n, k, pad, stride, dil, opad))
+
+
+def conv2d(x_nhwc, w_fcrs, pad=0, stride=1, dilation=1) -> np.ndarray:
+    """O1: direct Conv2d (cross-correlation, zero padding).  x [n,h,w,c], w [f,c,r,s] -> y [n,OH,OW,f]."""
+    x = _f64(x_nhwc)
+    w = _f64(w_fcrs)
+    n, h, wd, c = x.shape
+    f, c2, r, s = w.shape
+    assert c == c2
+    oh = conv_out_size(h, r, pad, stride, dilation)
+    ow = conv_out_size(wd, s, pad, stride, dilation)
+    y = np.zeros((n, oh, ow, f), np.float64)
+    _load().oracle_conv2d(n, c, h, wd, f, r, s, pad, stride, dilation, _p(x), _p(w), _p(y))
+    return y
+
+
+def conv_transpose2d(x_nhwc, w_cfrs, pad=0, stride=1, dilation=1, output_padding=0) -> np.ndarray:
+    """O2: ConvTranspose2d in scatter form.  x [n,h,w,c], w [c,f,r,s] -> y [n,OH,OW,f]."""
+    x = _f64(x_nhwc)
+    w = _f64(w_cfrs)
+    n, h, wd, c = x.shape
+    c2, f, r, s = w.shape
+    assert c == c2
+    oh = convt_out_size(h, r, pad, stride, dilation, output_padding)
+    ow = convt_out_size(wd, s, pad, stride, dilation, output_padding)
+    y = np.zeros((n, oh, ow, f), np.float64)
+    _load().oracle_convtranspose2d(n, c, h, wd, f, r, s, pad, stride, dilation, output_padding,
+                                   _p(x), _p(w), _p(y))
+    return y
+
+
+def gemm_nt(a_mk, b_nk) -> np.ndarray:
+    """O5: C[m,n] = sum_k A[m,k] B[n,k]."""
+    a = _f64(a_mk)
+    b = _f64(b_nk)
+    m, k = a.shape
+    n, k2 = b.shape
+    assert k == k2
+    cm = np.zeros((m, n), np.float64)
+    _load().oracle_gemm_nt(m, n, k, _p(a), _p(b), _p(cm))
+    return cm
+
+
+def weight_dlt_conv2d(w_fcrs) -> np.ndarray:
+    """a0 for Conv2d: wp[(i*S+j)*F+f, c] = W[f,c,i,j]  (Eq. layout-K transposed)."""
+    w = _f64(w_fcrs)
+    f, c, r, s = w.shape
+    wp = np.zeros((r * s * f, c), np.float64)
+    _load().oracle_weight_dlt_conv2d(f, c, r, s, _p(w), _p(wp))
+    return wp
+
+
+def weight_dlt_convt(w_cfrs) -> np.ndarray:
+    """a0 for ConvTranspose2d: wp[(i*S+j)*F+f, c] = W[c,f,i,j]."""
+    w = _f64(w_cfrs)
+    c, f, r, s = w.shape
+    wp = np.zeros((r * s * f, c), np.float64)
+    _load().oracle_weight_dlt_convt(c, f, r, s, _p(w), _p(wp))
+    return wp
+
+
+def merged_gemm(x_nhwc, wp) -> np.ndarray:
+    """a1+a2: T[n*h*w, r*s*f] = A'[m, c] . K'[c, n]; A' = A is the identity on NHWC."""
+    x = _f64(x_nhwc)
+    n, h, w, c = x.shape
+    return gemm_nt(x.reshape(n * h * w, c), wp)
+
+
+def offset_add(T, n, h, w, f, r, s, pad=0, stride=1, dilation=1) -> np.ndarray:
+    """a3: OffsetAdd eOperator (E7), per-dimension bounds on the 5-D view of T."""
+    t = _f64(T)
+    assert t.shape == (n * h * w, r * s * f), t.shape
+    oh = conv_out_size(h, r, pad, stride, dilation)
+    ow = conv_out_size(w, s, pad, stride, dilation)
+    y = np.zeros((n, oh, ow, f), np.float64)
+    _load().oracle_offset_add(n, h, w, f, r, s, pad, stride, dilation, _p(t), _p(y))
+    return y
+
+
+def selective_add(T, n, h, w, f, r, s, pad=0, stride=1, dilation=1, output_padding=0) -> np.ndarray:
+    """a4: ConvTranspose selective addition over the Matmul outputs."""
+    t = _f64(T)
+    assert t.shape == (n * h * w, r * s * f), t.shape
+    oh = convt_out_size(h, r, pad, stride, dilation, output_padding)
+    ow = convt_out_size(w, s, pad, stride, dilation, output_padding)
+    y = np.zeros((n, oh, ow, f), np.float64)
+    _load().oracle_selective_add(n, h, w, f, r, s, pad, stride, dilation, output_padding,
+                                 _p(t), _p(y))
+    return y
+
+
+def conv2d_derived(x_nhwc, w_fcrs, pad=0, stride=1, dilation=1) -> np.ndarray:
+    """O3 for Conv2d: OffsetAdd(Matmul(A', DLT(K))) -- the paper's derived program, step by step."""
+    x = _f64(x_nhwc)
+    n, h, w, c = x.shape
+    f, _, r, s = np.shape(w_fcrs)
+    T = merged_gemm(x, weight_dlt_conv2d(w_fcrs))
+    return offset_add(T, n, h, w, f, r, s, pad, stride, dilation)
+
+
+def conv_transpose2d_derived(x_nhwc, w_cfrs, pad=0, stride=1, dilation=1, output_padding=0):
+    """O3 for ConvTranspose2d: SelectiveAdd(Matmul(A', DLT(K))) on the unpadded input."""
+    x = _f64(x_nhwc)
+    n, h, w, c = x.shape
+    _, f, r, s = np.shape(w_cfrs)
+    T = merged_gemm(x, weight_dlt_convt(w_cfrs))
+    return selective_add(T, n, h, w, f, r, s, pad, stride, dilation, output_padding)
