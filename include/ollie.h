@@ -1,0 +1,212 @@
+/*
+ * ollie.h -- C ABI of libollie, the B200 (sm_100a) runtime of the programs Ollie's
+ * expression derivation produces for Conv2d / ConvTranspose2d (arXiv 2208.02025).
+ *
+ * Citation keys: "P:n" = /root/reference/PAPER.md line n (assembled copy P:670-1704),
+ * "S:n" = SPEC.md line n, "SURVEY" = /root/repo/SURVEY.md.
+ *
+ * The hot path:
+ *   a0  weight DLT, evaluated once at "compile time"  (Eq. layout-K)
+ *   a1  input layout-A  A'[t1*W+t2, c] = A[t1,t2,c]   (Eq. layout-A) -- the identity
+ *       on NHWC memory, eliminated without a launch
+ *   a2  merged Matmul T[m, (i,j,f)] = sum_c X[m,c] * W'[(i,j,f), c]
+ *   a3  OffsetAdd eOperator (E7)
+ *   a4  ConvTranspose selective addition
+ *   a5  fused eOperator pair (chain rule)
+ *   a7  generic scoped eOperator L_x Sum_y f(T[tau(x,y)])
+ *   a8  OffsetAdd / selective add fused into the GEMM epilogue (instance of P:955-965)
+ *
+ * Conventions (apply to every entry point):
+ *  - Ownership: every data pointer is a CALLER-OWNED CUDA DEVICE pointer.  The library
+ *    never allocates or frees device memory, never retains a pointer after the call
+ *    returns, and never synchronises the device.  Descriptor structs are read during
+ *    the call only (host memory, caller-owned).
+ *  - Streams: `stream` is a cudaStream_t (NULL = legacy default stream).  All device
+ *    work of a call is enqueued on it, asynchronously.
+ *  - Errors: status codes only; no C++ exception crosses the ABI.  All validation
+ *    happens BEFORE any launch, so a call that fails validation has no side effect.
+ *    ollie_last_error() returns a thread-local, human-readable detail string.
+ *  - Threading: calls are stateless and reentrant; ordering is by `stream` only.
+ *  - Layouts: activations are NHWC (the paper's HWC "A[t1,t2,c]");
+ *    Conv2d weights are PyTorch [f][c][r][s], ConvTranspose2d weights [c][f][r][s];
+ *    the prepared (merged) weight is W'[(i*S+j)*F+f][c] (K-major: the transpose of the
+ *    paper's K'[c, r*S*F+s*F+f]); the intermediate T is [n*h*w][r*s*f] with columns in
+ *    (i, j, f) order.
+ *  - dtypes: OLLIE_BF16 -- x, w, w_prep, y are bf16, accumulation fp32, T fp32;
+ *            OLLIE_TF32 -- x, w, w_prep, y are fp32 in memory, TF32 tensor-core MMA,
+ *                          fp32 accumulation (the paper's fp32, reading Q1/Q14).
+ *  - Alignment: x rows (c * sizeof(elem)) must be a multiple of 16 bytes and every
+ *    base pointer 16-byte aligned (TMA rule), else OLLIE_E_ALIGN; channel-pad the
+ *    activation first with an eOperator.
+ */
+#ifndef OLLIE_H_
+#define OLLIE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OLLIE_ABI_VERSION 1
+
+typedef void *ollie_stream_t; /* a cudaStream_t */
+
+typedef enum {
+    OLLIE_OK = 0,
+    OLLIE_E_INVALID = -1,     /* bad shape / range / arity / undeclared iterator       */
+    OLLIE_E_UNSUPPORTED = -2, /* valid but not implemented (dtype combination, plan)         */
+    OLLIE_E_WORKSPACE = -3,   /* ws too small or NULL when the unfused plan needs T           */
+    OLLIE_E_OOB = -4,         /* an index map reads outside the pad band              */
+    OLLIE_E_ALIGN = -5,       /* base pointer / row stride violates the 16-byte TMA rule      */
+    OLLIE_E_CUDA = -6         /* CUDA launch / runtime error; detail in ollie_last_error()    */
+} ollie_status;
+
+typedef enum {
+    OLLIE_BF16 = 0, /* bfloat16 storage                                   */
+    OLLIE_TF32 = 1, /* fp32 storage, TF32 tensor-core operands             */
+    OLLIE_FP32 = 2  /* fp32 storage, fp32 arithmetic (eOperators, T, y)    */
+} ollie_dtype;
+
+/* The problem statement of a layer (SPEC OpNode attrs "strides, dilation,
+ * pads").  Offsets follow PyTorch: kernel tap i reads input row oh*stride - pad
+ * + i*dilation (reading Q2 of DESIGN.md: the paper's centred r in [-1,1] is i - pad). */
+typedef struct {
+    int64_t n, c, h, w;     /* input: batch, channels, height, width                 */
+    int64_t f, r, s;        /* output channels, kernel height (R), kernel width (S)  */
+    int32_t pad, stride, dilation;
+    int32_t output_padding; /* ConvTranspose2d only (PyTorch semantics, reading Q9)  */
+} ollie_conv_shape;
+
+enum { OLLIE_PLAN_AUTO = 0, OLLIE_PLAN_FUSED = 1, OLLIE_PLAN_UNFUSED = 2 };
+
+/* ---------------------------------------------------------------------------------
+ * Versioning and errors
+ * --------------------------------------------------------------------------------- */
+int         ollie_abi_version(void);
+const char *ollie_status_string(ollie_status st);
+const char *ollie_last_error(void); /* thread-local detail of the last failing call ("" if none) */
+
+/* Output spatial size of the layer (Conv2d if transposed == 0, else ConvTranspose2d).
+ * Returns OLLIE_E_INVALID for a non-positive size. */
+ollie_status ollie_output_hw(const ollie_conv_shape *shape, int transposed, int64_t *oh, int64_t *ow);
+
+/* ---------------------------------------------------------------------------------
+ * a0 -- compile-time weight DLT (Eq. layout-K; compile-time expression
+ * evaluation):   w_prep[(i*S+j)*F+f][c] = W[f][c][i][j]   (Conv2d)
+ *                             w_prep[(i*S+j)*F+f][c] = W[c][f][i][j]   (ConvTranspose2d)
+ * w (input) and w_prep (output, ollie_prepared_weight_bytes() bytes) are device
+ * buffers of `dtype` elements (BF16 or TF32).  Pure indexing: bit-exact.
+ * --------------------------------------------------------------------------------- */
+size_t       ollie_prepared_weight_bytes(const ollie_conv_shape *shape, ollie_dtype dtype);
+ollie_status ollie_prepare_weight_conv2d(const ollie_conv_shape *shape, ollie_dtype dtype,
+                                         const void *w_fcrs, void *w_prep, ollie_stream_t stream);
+ollie_status ollie_prepare_weight_convtranspose2d(const ollie_conv_shape *shape, ollie_dtype dtype,
+                                                  const void *w_cfrs, void *w_prep, ollie_stream_t stream);
+
+/* Workspace for the unfused plan: T fp32 [n*h*w][ldT] with ldT = r*s*f rounded up to a
+ * multiple of 4 (16-byte rows).  Returns 0 when `plan` resolves to the fused plan. */
+size_t ollie_workspace_bytes(const ollie_conv_shape *shape, ollie_dtype dtype, int plan, int transposed);
+
+/* ---------------------------------------------------------------------------------
+ * The derived layer: a1 (eliminated) + a2 merged GEMM + a3 OffsetAdd (Conv2d) or a4
+ * selective addition (ConvTranspose2d), unfused (T through `ws`) or fused (a8, T lives
+ * only in TMEM / shared memory).
+ *   x_nhwc : [n][h][w][c]            dtype elements (device)
+ *   w_prep : [r*s*f][c]              from ollie_prepare_weight_* (device)
+ *   y_nhwc : [n][OH][OW][f]          dtype elements, fully overwritten (device)
+ *   ws     : ollie_workspace_bytes() bytes (device), may be NULL if that is 0
+ *   plan   : OLLIE_PLAN_AUTO / FUSED / UNFUSED
+ * ConvTranspose2d requires dilation == 1 (the configured workloads); else UNSUPPORTED.
+ * --------------------------------------------------------------------------------- */
+ollie_status ollie_conv2d_derived(const ollie_conv_shape *shape, ollie_dtype dtype,
+                                  const void *x_nhwc, const void *w_prep, void *y_nhwc,
+                                  void *ws, size_t ws_bytes, int plan, ollie_stream_t stream);
+ollie_status ollie_convtranspose2d_derived(const ollie_conv_shape *shape, ollie_dtype dtype,
+                                           const void *x_nhwc, const void *w_prep, void *y_nhwc,
+                                           void *ws, size_t ws_bytes, int plan, ollie_stream_t stream);
+
+/* a2 standalone (the merged Matmul of P:1342-1352 on tcgen05 tensor cores):
+ *   T[m][n] = sum_k A[m][k] * B[n][k]      A [M][K], B [N][K] in `dtype` (BF16 / TF32),
+ *   T fp32 with row stride ldT elements (ldT >= N, ldT % 4 == 0).  K % 8 (bf16) or
+ *   K % 4 (tf32) must be 0 (16-byte rows). */
+ollie_status ollie_merged_gemm(int64_t M, int64_t N, int64_t K, ollie_dtype dtype,
+                               const void *A, const void *B, float *T, int64_t ldT,
+                               ollie_stream_t stream);
+
+/* a3 / a4 standalone eOperator.  T is fp32 [n*h*w][ldT] (ldT >= r*s*f; pass r*s*f for a
+ * dense T), columns in (i, j, f) order.  transposed == 0: OffsetAdd (Conv2d semantics);
+ * transposed == 1: ConvTranspose selective addition (dilation 1).  y is [n][OH][OW][f]
+ * in y_dtype (OLLIE_BF16 rounds fp32 sums RNE; OLLIE_FP32 / OLLIE_TF32 store fp32).
+ * Spatial bounds are checked per dimension (reading Q5). */
+ollie_status ollie_offset_add(const ollie_conv_shape *shape, int transposed, const float *T,
+                              int64_t ldT, ollie_dtype y_dtype, void *y_nhwc, ollie_stream_t stream);
+
+/* ---------------------------------------------------------------------------------
+ * a5-a7 -- scoped index-expression eOperator (SPEC IndexExpr / TensorDecl / Scope /
+ * Compute; general format L_x Sum_y f(T[tau(x,y)])).
+ *
+ * Iterators of a scope are numbered 0..n_trav-1 (traversal, in declared order = the
+ * output layout) then n_trav..n_trav+n_sum-1 (summation, order-free,
+ * P:855-857).  An index is  c0 + sum_t coef_t * atom_t  with atom = iterator,
+ * floordiv(iterator, div) or mod(iterator, div) (div > 0; floor division and
+ * non-negative remainder).  Reads inside a tensor's pad band return 0
+ * (P:871-874); reads outside it are rejected statically (interval arithmetic over the
+ * iterator ranges) with OLLIE_E_OOB, so an accepted eOp never reads out of bounds.
+ * scope[0] is the evaluated (outer) scope; scope[1], if n_scopes == 2, is a nested
+ * instantiated scope referenced as tensor -1 and evaluated inline (chain rule /
+ * expression fusion): its element at coordinate v (v = its traversal
+ * iterator values) is its body summed over its summation space, 0 in its pad band.
+ * The output is dense, shape = scope[0]'s traversal range widths.
+ * --------------------------------------------------------------------------------- */
+#define OLLIE_MAX_DIMS 8
+#define OLLIE_MAX_TERMS 8
+#define OLLIE_MAX_ACCESS 8
+#define OLLIE_MAX_INSTR 32
+#define OLLIE_MAX_INPUTS 8
+
+enum { OLLIE_ATOM_ITER = 0, OLLIE_ATOM_FLOORDIV = 1, OLLIE_ATOM_MOD = 2 };
+enum { OLLIE_OP_PUSH_ACCESS = 0, OLLIE_OP_PUSH_CONST = 1, OLLIE_OP_ADD = 2, OLLIE_OP_MUL = 3,
+       OLLIE_OP_SUB = 4, OLLIE_OP_NEG = 5, OLLIE_OP_MAX = 6, OLLIE_OP_MIN = 7 };
+
+typedef struct { int32_t iter; int32_t kind; int64_t div; int64_t coef; } ollie_term;
+typedef struct { int32_t nterms; ollie_term term[OLLIE_MAX_TERMS]; int64_t c0; } ollie_index;
+typedef struct { int32_t tensor; /* >= 0 input id; -1 = scope[1] */
+                 int32_t ndim; ollie_index idx[OLLIE_MAX_DIMS]; } ollie_access;
+typedef struct { int32_t ndim; int64_t shape[OLLIE_MAX_DIMS];
+                 int64_t pad_lo[OLLIE_MAX_DIMS], pad_hi[OLLIE_MAX_DIMS];
+                 ollie_dtype dtype; } ollie_tensor;
+typedef struct { int32_t op; int32_t arg; float cval; } ollie_instr; /* postfix body f */
+typedef struct {
+    int32_t n_trav; int64_t trav_lo[OLLIE_MAX_DIMS], trav_hi[OLLIE_MAX_DIMS];
+    int32_t n_sum;  int64_t sum_lo[OLLIE_MAX_DIMS],  sum_hi[OLLIE_MAX_DIMS];
+    int32_t n_acc;  ollie_access acc[OLLIE_MAX_ACCESS];
+    int32_t n_ins;  ollie_instr body[OLLIE_MAX_INSTR];
+    int64_t pad_lo[OLLIE_MAX_DIMS], pad_hi[OLLIE_MAX_DIMS]; /* zero band, scope[1] only */
+} ollie_scope;
+typedef struct {
+    int32_t n_in; ollie_tensor in[OLLIE_MAX_INPUTS];
+    ollie_dtype out_dtype;   /* OLLIE_BF16 or OLLIE_FP32; inputs likewise */
+    int32_t n_scopes; ollie_scope scope[2];
+} ollie_eop;
+
+typedef struct {
+    int32_t is_identity;    /* output == input[0] byte for byte            */
+    int32_t pure_indexing;  /* single access, no summation, no arithmetic: bit-exact copy */
+    int64_t out_elems;
+    int64_t bytes_in, bytes_out; /* algorithmic bytes of one evaluation (0 if identity)  */
+} ollie_eop_info;
+
+/* Validate + classify; no launch. */
+ollie_status ollie_eop_analyze(const ollie_eop *eop, ollie_eop_info *info);
+/* Evaluate.  inputs[k] are device pointers to dense tensors of eop->in[k]; output is a
+ * device pointer to the dense output.  An identity eOp whose output aliases input 0
+ * launches nothing; a non-aliased identity is one device-to-device copy. */
+ollie_status ollie_eop_eval(const ollie_eop *eop, const void *const *inputs, void *output,
+                            ollie_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OLLIE_H_ */

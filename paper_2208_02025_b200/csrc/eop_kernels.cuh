@@ -1,0 +1,169 @@
+// eop_kernels.cuh -- the memory-bound eOperators of the derived convolution.
+//
+//  a3  OffsetAdd (E7):
+//        Y[b,oh,ow,f] = sum_{i<R,j<S} T[b, oh*st-p+i*d, ow*st-p+j*d, (i*S+j)*F+f]
+//      taps whose spatial index leaves [0,H)x[0,W) contribute 0, tested per dimension
+//      (reading Q5 -- never on the flattened m = t1*W+t2).
+//  a4  ConvTranspose selective addition, dilation 1:
+//        Y[b,oh,ow,f] = sum over i = (oh+p) mod st + st*k  (likewise j) of
+//                       T[b, (oh+p-i)/st, (ow+p-j)/st, (i*S+j)*F+f]   (in-range rows only)
+//  a0  weight DLT (Eq. layout-K) as a tiled smem transpose.
+//
+// Roofline: HBM.  No data reuse (each T element feeds at most one output),
+// so the kernels only need coalescing, 128-bit vectors and enough loads in flight: one
+// thread owns VEC consecutive f of one output pixel and issues all its r*s tap loads
+// before summing.  Tap order (i, j) is fixed, so results are deterministic.
+#pragma once
+#include "sm100_ptx.cuh"
+
+namespace ollie {
+
+struct OffsetAddArgs {
+    const float *T;
+    int64_t ldT;               // row stride of T (elements)
+    void *y;
+    int64_t n, h, w, f, r, s;
+    int64_t oh, ow;
+    int32_t pad, stride, dil;
+    int64_t items;             // n*oh*ow*(f/VEC)
+};
+
+__device__ __forceinline__ float4 ld_stream_f4(const float *p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_stream_f1(const float *p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+
+template <int VEC, bool kOutBF16>
+__device__ __forceinline__ void store_y(void *y, int64_t off, const float (&acc)[VEC]) {
+    if constexpr (kOutBF16) {
+        uint16_t *yp = reinterpret_cast<uint16_t *>(y) + off;
+        if constexpr (VEC == 4) {
+            uint2 pk;
+            pk.x = (uint32_t)float_to_bf16_rne(acc[0]) | ((uint32_t)float_to_bf16_rne(acc[1]) << 16);
+            pk.y = (uint32_t)float_to_bf16_rne(acc[2]) | ((uint32_t)float_to_bf16_rne(acc[3]) << 16);
+            *reinterpret_cast<uint2 *>(yp) = pk;
+        } else {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) yp[v] = float_to_bf16_rne(acc[v]);
+        }
+    } else {
+        float *yp = reinterpret_cast<float *>(y) + off;
+        if constexpr (VEC == 4)
+            *reinterpret_cast<float4 *>(yp) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        else {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) yp[v] = acc[v];
+        }
+    }
+}
+
+template <int VEC>
+__device__ __forceinline__ void accum_tap(float (&acc)[VEC], const float *src) {
+    if constexpr (VEC == 4) {
+        float4 t = ld_stream_f4(src);
+        acc[0] += t.x; acc[1] += t.y; acc[2] += t.z; acc[3] += t.w;
+    } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[v] += ld_stream_f1(src + v);
+    }
+}
+
+// a3: OffsetAdd.  Taps are issued in (i, j) order; out-of-image taps are skipped.
+template <int VEC, bool kOutBF16>
+__global__ void __launch_bounds__(256) offset_add_kernel(OffsetAddArgs a) {
+    const int64_t fv_per_px = a.f / VEC;
+    const int64_t nt_rsf = a.r * a.s * a.f;
+    (void)nt_rsf;
+    for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < a.items;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t fv = it % fv_per_px;
+        const int64_t px = it / fv_per_px;
+        const int64_t ow = px % a.ow;
+        const int64_t t = px / a.ow;
+        const int64_t oh = t % a.oh;
+        const int64_t b = t / a.oh;
+        float acc[VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
+        const int64_t h0 = oh * a.stride - a.pad, w0 = ow * a.stride - a.pad;
+        const float *Tb = a.T + (b * a.h) * a.w * a.ldT + fv * VEC;
+        for (int64_t i = 0; i < a.r; ++i) {
+            const int64_t t1 = h0 + i * a.dil;
+            if (t1 < 0 || t1 >= a.h) continue;
+            const float *Trow = Tb + t1 * a.w * a.ldT + i * a.s * a.f;
+#pragma unroll 3
+            for (int64_t j = 0; j < a.s; ++j) {
+                const int64_t t2 = w0 + j * a.dil;
+                if (t2 < 0 || t2 >= a.w) continue;
+                accum_tap<VEC>(acc, Trow + t2 * a.ldT + j * a.f);
+            }
+        }
+        store_y<VEC, kOutBF16>(a.y, px * a.f + fv * VEC, acc);
+    }
+}
+
+// a4: ConvTranspose selective addition (dilation 1).  Only the taps i == (oh+p) mod st
+// (mod st) are visited: each output reads exactly the Matmul outputs that land on it.
+template <int VEC, bool kOutBF16>
+__global__ void __launch_bounds__(256) selective_add_kernel(OffsetAddArgs a) {
+    const int64_t fv_per_px = a.f / VEC;
+    const int64_t st = a.stride;
+    for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < a.items;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t fv = it % fv_per_px;
+        const int64_t px = it / fv_per_px;
+        const int64_t ow = px % a.ow;
+        const int64_t t = px / a.ow;
+        const int64_t oh = t % a.oh;
+        const int64_t b = t / a.oh;
+        float acc[VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
+        const int64_t th = oh + a.pad, tw = ow + a.pad;
+        const float *Tb = a.T + (b * a.h) * a.w * a.ldT + fv * VEC;
+        // th = oh + p >= 0, so th % st is the smallest selected kernel row; rows past th
+        // would need a negative input row, and the input row falls as i grows.
+        for (int64_t i = th % st; i < a.r && i <= th; i += st) {
+            const int64_t ih = (th - i) / st;
+            if (ih >= a.h) continue;
+            const float *Trow = Tb + ih * a.w * a.ldT + i * a.s * a.f;
+            for (int64_t j = tw % st; j < a.s && j <= tw; j += st) {
+                const int64_t iw = (tw - j) / st;
+                if (iw >= a.w) continue;
+                accum_tap<VEC>(acc, Trow + iw * a.ldT + j * a.f);
+            }
+        }
+        store_y<VEC, kOutBF16>(a.y, px * a.f + fv * VEC, acc);
+    }
+}
+
+// a0: weight DLT  wp[(ij)*F + f][c] = src[f*sz + c*sc + ij]   (ij = i*S+j)
+//   Conv2d  W[f][c][i][j]: sz = C*RS, sc = RS;   ConvT W[c][f][i][j]: sz = RS, sc = F*RS.
+// Per f a [C x RS] -> [RS x C] transpose through a 32x33 smem tile; pure data movement.
+template <typename E>
+__global__ void __launch_bounds__(256) weight_dlt_kernel(const E *__restrict__ src, E *__restrict__ dst, int64_t F,
+                                                         int64_t C, int64_t RS, int64_t sz, int64_t sc) {
+    __shared__ E tile[32][33];
+    const int64_t f = blockIdx.z;
+    const int64_t c0 = (int64_t)blockIdx.y * 32, ij0 = (int64_t)blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+    for (int k = ty; k < 32; k += 8) {
+        const int64_t c = c0 + k, ij = ij0 + tx;
+        if (c < C && ij < RS) tile[k][tx] = src[f * sz + c * sc + ij];
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+        const int64_t ij = ij0 + k, c = c0 + tx;
+        if (c < C && ij < RS) dst[(ij * F + f) * C + c] = tile[tx][k];
+    }
+}
+
+}  // namespace ollie

@@ -1,0 +1,192 @@
+// merged_gemm.cuh -- step a2 of the hot path: the merged Matmul of Ollie's derived
+// convolution ("merges these matrix multiplications into a single one";
+// operator matching t1,t2 -> m; r,s,f -> n; c -> k):
+//
+//     T[m][n] = sum_k A[m][k] * B[n][k]      A = X as [n*h*w, c] (layout-A is the identity on
+//                                            NHWC), B = W' [(i*S+j)*F+f][c]
+//
+// sm_100a design: persistent, warp-specialised, one CTA per SM.
+//   warp 0     TMA producer: A / B tiles (K-major, SWIZZLE_128B) into a STAGES-deep smem ring
+//   warp 1     MMA issuer:   one thread issues tcgen05.mma (128 x BN x 16|8) into TMEM
+//   warp 2     TMEM allocator (512 columns = two BN<=256 fp32 accumulators, double-buffered)
+//   warps 4-7  epilogue:     tcgen05.ld -> registers -> padded smem -> coalesced st.global
+// BN (the UMMA N) is a runtime parameter (multiple of 16, <= 256) chosen on the host to
+// minimise N-tail waste.  M / N / K tails are handled by TMA zero fill and store guards.
+#pragma once
+#include "sm100_ptx.cuh"
+
+namespace ollie {
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BK_BYTES = 128;           // one SWIZZLE_128B row per operand row per stage
+constexpr int GEMM_STAGES = 4;
+constexpr int GEMM_MAX_BN = 256;
+constexpr int GEMM_A_STAGE_BYTES = GEMM_BM * GEMM_BK_BYTES;          // 16 KB
+constexpr int GEMM_B_STAGE_BYTES = GEMM_MAX_BN * GEMM_BK_BYTES;      // 32 KB (max)
+constexpr int GEMM_STG_FLOATS = 32 * 33;                             // per epilogue warp
+constexpr int GEMM_THREADS = 256;
+constexpr uint32_t GEMM_TMEM_COLS = 512;
+
+constexpr size_t gemm_smem_bytes() {
+    return 1024 /* alignment slack */ + (size_t)GEMM_STAGES * (GEMM_A_STAGE_BYTES + GEMM_B_STAGE_BYTES) +
+           4 * GEMM_STG_FLOATS * sizeof(float) + 256 /* barriers */;
+}
+
+struct GemmArgs {
+    int64_t M, N, K;
+    int32_t BN;          // UMMA N of a tile
+    void *out;           // fp32 or bf16, row-major with leading dimension ldo
+    int64_t ldo;
+};
+
+template <bool kTF32, bool kOutBF16>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+merged_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
+    constexpr int ES = kTF32 ? 4 : 2;
+    constexpr int BK = GEMM_BK_BYTES / ES;       // 64 bf16 / 32 tf32 elements
+    constexpr int UMMA_K_BYTES = 32;             // 16 bf16 / 8 tf32 per tcgen05.mma
+    constexpr int KSTEPS = GEMM_BK_BYTES / UMMA_K_BYTES;
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sA = smem;
+    uint8_t *sB = sA + GEMM_STAGES * GEMM_A_STAGE_BYTES;
+    float *stg = reinterpret_cast<float *>(sB + GEMM_STAGES * GEMM_B_STAGE_BYTES);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(stg + 4 * GEMM_STG_FLOATS);
+    uint64_t *full = bars;                       // [STAGES]
+    uint64_t *empty = bars + GEMM_STAGES;        // [STAGES]
+    uint64_t *tfull = bars + 2 * GEMM_STAGES;    // [2]
+    uint64_t *tempty = tfull + 2;                // [2]
+    uint32_t *tmem_base_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    const int64_t M = args.M, N = args.N, K = args.K;
+    const int BN = args.BN;
+    const int num_m = (int)((M + GEMM_BM - 1) / GEMM_BM);
+    const int num_n = (int)((N + BN - 1) / BN);
+    const int num_tiles = num_m * num_n;
+    const int num_k = (int)((K + BK - 1) / BK);
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+    }
+    if (warp == 1 && lane == 0) {
+        for (int i = 0; i < GEMM_STAGES; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<GEMM_TMEM_COLS>(tmem_base_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_base_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===== TMA producer =====
+            const uint32_t stage_bytes = GEMM_A_STAGE_BYTES + (uint32_t)BN * GEMM_BK_BYTES;
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                const int m_blk = tile / num_n, n_blk = tile % num_n;
+                for (int kb = 0; kb < num_k; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], stage_bytes);
+                    tma_load_2d(sA + stage * GEMM_A_STAGE_BYTES, &tmA, &full[stage], kb * BK, m_blk * GEMM_BM);
+                    tma_load_2d(sB + stage * GEMM_B_STAGE_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
+                    if (++stage == GEMM_STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ===== MMA issuer (single thread) =====
+            const uint32_t idesc = make_idesc(kTF32, GEMM_BM, (uint32_t)BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * GEMM_MAX_BN);
+                for (int kb = 0; kb < num_k; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + stage * GEMM_A_STAGE_BYTES);
+                    const uint32_t b0 = smem_u32(sB + stage * GEMM_B_STAGE_BYTES);
+#pragma unroll
+                    for (int k = 0; k < KSTEPS; ++k) {
+                        umma<kTF32>(d_tmem, make_sdesc_k_sw128(a0 + k * UMMA_K_BYTES),
+                                    make_sdesc_k_sw128(b0 + k * UMMA_K_BYTES), idesc, (kb | k) != 0);
+                    }
+                    umma_commit(&empty[stage]);
+                    if (++stage == GEMM_STAGES) { stage = 0; phase ^= 1; }
+                }
+                umma_commit(&tfull[acc]);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== epilogue: TMEM -> registers -> smem (padded) -> coalesced global stores =====
+        const int ew = warp - 4;                 // == warp % 4: TMEM lane quadrant of this warp
+        float *st = stg + ew * GEMM_STG_FLOATS;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            const int m_blk = tile / num_n, n_blk = tile % num_n;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int64_t row0 = (int64_t)m_blk * GEMM_BM + ew * 32;
+            const int64_t col_base = (int64_t)n_blk * BN;
+            const int64_t col_end = col_base + BN < N ? col_base + BN : N;   // this tile's columns only
+            for (int c = 0; c < BN; c += 32) {
+                if (col_base + c >= col_end) break;
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * GEMM_MAX_BN + c), v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) st[lane * 33 + j] = __uint_as_float(v[j]);
+                __syncwarp();
+                const int64_t col = col_base + c + lane;
+                if (col < col_end) {
+#pragma unroll 4
+                    for (int r = 0; r < 32; ++r) {
+                        const int64_t row = row0 + r;
+                        if (row < M) {
+                            const float val = st[r * 33 + lane];
+                            if constexpr (kOutBF16)
+                                reinterpret_cast<uint16_t *>(args.out)[row * args.ldo + col] = float_to_bf16_rne(val);
+                            else
+                                reinterpret_cast<float *>(args.out)[row * args.ldo + col] = val;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<GEMM_TMEM_COLS>(tmem_base);
+    }
+}
+
+}  // namespace ollie

@@ -1,0 +1,771 @@
+// ollie.cu -- libollie: the C ABI of include/ollie.h.  Host-side validation, plan choice,
+// TMA tensor-map encoding, eOperator analysis (interval-arithmetic bounds, identity
+// elimination) and kernel launches.  No device memory is allocated here; every buffer
+// is caller-owned.  There is no CPU fallback: every step of the path runs in the
+// kernels of merged_gemm.cuh / eop_kernels.cuh / eop_eval.cuh.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ollie.h"
+#include "eop_eval.cuh"
+#include "eop_kernels.cuh"
+#include "fused_conv.cuh"
+#include "merged_gemm.cuh"
+
+using namespace ollie;
+
+// ------------------------------------------------------------------------ errors
+static thread_local std::string g_last_error;
+
+static ollie_status fail(ollie_status st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+static ollie_status ok() {
+    g_last_error.clear();
+    return OLLIE_OK;
+}
+#define CUDA_TRY(expr)                                                                              \
+    do {                                                                                            \
+        cudaError_t _e = (expr);                                                                    \
+        if (_e != cudaSuccess) return fail(OLLIE_E_CUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+    } while (0)
+#define CHECK_LAUNCH()                                                                                   \
+    do {                                                                                                 \
+        cudaError_t _e = cudaGetLastError();                                                             \
+        if (_e != cudaSuccess) return fail(OLLIE_E_CUDA, "kernel launch: %s", cudaGetErrorString(_e)); \
+    } while (0)
+
+extern "C" int ollie_abi_version(void) { return OLLIE_ABI_VERSION; }
+
+extern "C" const char *ollie_status_string(ollie_status st) {
+    switch (st) {
+        case OLLIE_OK: return "OLLIE_OK";
+        case OLLIE_E_INVALID: return "OLLIE_E_INVALID";
+        case OLLIE_E_UNSUPPORTED: return "OLLIE_E_UNSUPPORTED";
+        case OLLIE_E_WORKSPACE: return "OLLIE_E_WORKSPACE";
+        case OLLIE_E_OOB: return "OLLIE_E_OOB";
+        case OLLIE_E_ALIGN: return "OLLIE_E_ALIGN";
+        case OLLIE_E_CUDA: return "OLLIE_E_CUDA";
+    }
+    return "OLLIE_E_UNKNOWN";
+}
+extern "C" const char *ollie_last_error(void) { return g_last_error.c_str(); }
+
+// ------------------------------------------------------------------------ device info
+static int num_sms() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 148;
+    if (!cached[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = v > 0 ? v : 148;
+    }
+    return cached[dev];
+}
+
+static size_t elem_size(ollie_dtype d) { return d == OLLIE_BF16 ? 2 : 4; }
+static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------------------ TMA
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                    const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(p);
+    });
+    return fn;
+}
+
+// 2-D K-major operand: dims {inner, outer}, row stride in bytes, box {box_inner, box_outer}.
+static ollie_status make_tmap_2d(CUtensorMap *m, const void *base, bool tf32, uint64_t inner, uint64_t outer,
+                                 uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                     const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return OLLIE_OK;
+}
+
+// 4-D activation map NHWC: dims {c, w, h, n}; box {box_c, box_w, box_h, box_n}.
+static ollie_status make_tmap_nhwc(CUtensorMap *m, const void *base, bool tf32, int64_t n, int64_t h, int64_t w,
+                                   int64_t c, uint32_t bc, uint32_t bw, uint32_t bh, uint32_t bn) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
+    const uint64_t es = tf32 ? 4 : 2;
+    cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+    cuuint64_t strides[3] = {(cuuint64_t)(c * es), (cuuint64_t)(w * c * es), (cuuint64_t)(h * w * c * es)};
+    cuuint32_t box[4] = {bc, bw, bh, bn};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(m, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                     const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (4d) failed (%d)", (int)r);
+    return OLLIE_OK;
+}
+
+// ------------------------------------------------------------------------ merged GEMM launch
+// UMMA N per tile: multiple of 16 in [16, 256] minimising the padded N, larger on ties.
+static int choose_bn(int64_t N) {
+    int best = 256;
+    int64_t best_pad = ceil_div(N, 256) * 256;
+    for (int bn = 256; bn >= 16; bn -= 16) {
+        int64_t padded = ceil_div(N, bn) * bn;
+        if (padded < best_pad) {
+            best_pad = padded;
+            best = bn;
+        }
+    }
+    return best;
+}
+
+template <bool TF32, bool OUTBF16>
+static ollie_status launch_gemm_t(const CUtensorMap &ta, const CUtensorMap &tb, const GemmArgs &ga,
+                                  cudaStream_t stream) {
+    auto kern = merged_gemm_kernel<TF32, OUTBF16>;
+    static bool attr_done[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_done[dev & 63]) {
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes()));
+        attr_done[dev & 63] = true;
+    }
+    const int64_t tiles = ceil_div(ga.M, GEMM_BM) * ceil_div(ga.N, ga.BN);
+    const int grid = (int)std::min<int64_t>(tiles, num_sms());
+    kern<<<grid, GEMM_THREADS, gemm_smem_bytes(), stream>>>(ta, tb, ga);
+    CHECK_LAUNCH();
+    return OLLIE_OK;
+}
+
+// out = A[M,K] * B[N,K]^T ; out fp32 (out_bf16 = false) or bf16, leading dim ldo.
+static ollie_status run_gemm(int64_t M, int64_t N, int64_t K, bool tf32, const void *A, const void *B, void *out,
+                             int64_t ldo, bool out_bf16, cudaStream_t stream) {
+    const size_t es = tf32 ? 4 : 2;
+    if ((K * es) % 16 != 0)
+        return fail(OLLIE_E_ALIGN, "K*sizeof(elem) = %lld is not a multiple of 16 (TMA rule); pad channels",
+                    (long long)(K * es));
+    if (!aligned16(A) || !aligned16(B)) return fail(OLLIE_E_ALIGN, "GEMM operand base not 16-byte aligned");
+    if (M >= (1ll << 31) || N >= (1ll << 31) || K >= (1ll << 31))
+        return fail(OLLIE_E_UNSUPPORTED, "GEMM extent exceeds int32 TMA coordinates");
+    const int BN = choose_bn(N);
+    const uint32_t BK = (uint32_t)(GEMM_BK_BYTES / es);
+    CUtensorMap ta, tb;
+    ollie_status st = make_tmap_2d(&ta, A, tf32, (uint64_t)K, (uint64_t)M, (uint64_t)(K * es), BK, GEMM_BM);
+    if (st != OLLIE_OK) return st;
+    st = make_tmap_2d(&tb, B, tf32, (uint64_t)K, (uint64_t)N, (uint64_t)(K * es), BK, (uint32_t)BN);
+    if (st != OLLIE_OK) return st;
+    GemmArgs ga{M, N, K, BN, out, ldo};
+    if (tf32) return out_bf16 ? launch_gemm_t<true, true>(ta, tb, ga, stream) : launch_gemm_t<true, false>(ta, tb, ga, stream);
+    return out_bf16 ? launch_gemm_t<false, true>(ta, tb, ga, stream) : launch_gemm_t<false, false>(ta, tb, ga, stream);
+}
+
+extern "C" ollie_status ollie_merged_gemm(int64_t M, int64_t N, int64_t K, ollie_dtype dtype, const void *A,
+                                          const void *B, float *T, int64_t ldT, ollie_stream_t stream) {
+    if (M <= 0 || N <= 0 || K <= 0) return fail(OLLIE_E_INVALID, "GEMM extents must be positive");
+    if (dtype != OLLIE_BF16 && dtype != OLLIE_TF32) return fail(OLLIE_E_UNSUPPORTED, "GEMM dtype must be BF16 or TF32");
+    if (!A || !B || !T) return fail(OLLIE_E_INVALID, "null pointer");
+    if (ldT < N) return fail(OLLIE_E_INVALID, "ldT < N");
+    ollie_status st = run_gemm(M, N, K, dtype == OLLIE_TF32, A, B, T, ldT, false, (cudaStream_t)stream);
+    return st == OLLIE_OK ? ok() : st;
+}
+
+// ------------------------------------------------------------------------ shapes
+static ollie_status check_shape(const ollie_conv_shape *s, int transposed, int64_t *oh, int64_t *ow) {
+    if (!s) return fail(OLLIE_E_INVALID, "null shape");
+    if (s->n <= 0 || s->c <= 0 || s->h <= 0 || s->w <= 0 || s->f <= 0 || s->r <= 0 || s->s <= 0)
+        return fail(OLLIE_E_INVALID, "EmptyRange: every extent must be positive");
+    if (s->pad < 0 || s->stride < 1 || s->dilation < 1 || s->output_padding < 0)
+        return fail(OLLIE_E_INVALID, "pad >= 0, stride >= 1, dilation >= 1, output_padding >= 0 required");
+    int64_t H, W;
+    if (!transposed) {
+        if (s->output_padding != 0) return fail(OLLIE_E_INVALID, "output_padding is ConvTranspose2d-only");
+        H = (s->h + 2 * s->pad - (int64_t)s->dilation * (s->r - 1) - 1) / s->stride + 1;
+        W = (s->w + 2 * s->pad - (int64_t)s->dilation * (s->s - 1) - 1) / s->stride + 1;
+        if (s->h + 2 * s->pad - (int64_t)s->dilation * (s->r - 1) - 1 < 0 ||
+            s->w + 2 * s->pad - (int64_t)s->dilation * (s->s - 1) - 1 < 0)
+            H = W = 0;
+    } else {
+        if (s->output_padding >= std::max(s->stride, s->dilation))
+            return fail(OLLIE_E_INVALID, "output_padding must be < max(stride, dilation)");
+        H = (s->h - 1) * s->stride - 2 * (int64_t)s->pad + (int64_t)s->dilation * (s->r - 1) + s->output_padding + 1;
+        W = (s->w - 1) * s->stride - 2 * (int64_t)s->pad + (int64_t)s->dilation * (s->s - 1) + s->output_padding + 1;
+    }
+    if (H <= 0 || W <= 0) return fail(OLLIE_E_INVALID, "EmptyRange: output size is not positive");
+    if (oh) *oh = H;
+    if (ow) *ow = W;
+    return OLLIE_OK;
+}
+
+extern "C" ollie_status ollie_output_hw(const ollie_conv_shape *shape, int transposed, int64_t *oh, int64_t *ow) {
+    ollie_status st = check_shape(shape, transposed, oh, ow);
+    return st == OLLIE_OK ? ok() : st;
+}
+
+static int64_t ldT_of(const ollie_conv_shape *s) { return ceil_div(s->r * s->s * s->f, 4) * 4; }
+
+// ------------------------------------------------------------------------ a0 weight DLT
+extern "C" size_t ollie_prepared_weight_bytes(const ollie_conv_shape *s, ollie_dtype dtype) {
+    if (!s || s->r <= 0 || s->s <= 0 || s->f <= 0 || s->c <= 0) return 0;
+    return (size_t)(s->r * s->s * s->f * s->c) * elem_size(dtype);
+}
+
+static ollie_status prepare_weight(const ollie_conv_shape *s, ollie_dtype dtype, const void *w, void *wp,
+                                   cudaStream_t stream, bool transposed) {
+    ollie_status st = check_shape(s, transposed, nullptr, nullptr);
+    if (st != OLLIE_OK) return st;
+    if (dtype != OLLIE_BF16 && dtype != OLLIE_TF32) return fail(OLLIE_E_UNSUPPORTED, "weight dtype must be BF16 or TF32");
+    if (!w || !wp) return fail(OLLIE_E_INVALID, "null pointer");
+    const int64_t F = s->f, C = s->c, RS = s->r * s->s;
+    if (F > 65535) return fail(OLLIE_E_UNSUPPORTED, "f > 65535");
+    const int64_t sz = transposed ? RS : C * RS;
+    const int64_t sc = transposed ? F * RS : RS;
+    dim3 grid((unsigned)ceil_div(RS, 32), (unsigned)ceil_div(C, 32), (unsigned)F);
+    if (dtype == OLLIE_BF16)
+        weight_dlt_kernel<uint16_t><<<grid, 256, 0, stream>>>((const uint16_t *)w, (uint16_t *)wp, F, C, RS, sz, sc);
+    else
+        weight_dlt_kernel<float><<<grid, 256, 0, stream>>>((const float *)w, (float *)wp, F, C, RS, sz, sc);
+    CHECK_LAUNCH();
+    return ok();
+}
+
+extern "C" ollie_status ollie_prepare_weight_conv2d(const ollie_conv_shape *shape, ollie_dtype dtype,
+                                                    const void *w_fcrs, void *w_prep, ollie_stream_t stream) {
+    return prepare_weight(shape, dtype, w_fcrs, w_prep, (cudaStream_t)stream, false);
+}
+extern "C" ollie_status ollie_prepare_weight_convtranspose2d(const ollie_conv_shape *shape, ollie_dtype dtype,
+                                                             const void *w_cfrs, void *w_prep, ollie_stream_t stream) {
+    return prepare_weight(shape, dtype, w_cfrs, w_prep, (cudaStream_t)stream, true);
+}
+
+// ------------------------------------------------------------------------ a3 / a4 standalone
+static ollie_status run_offset_add(const ollie_conv_shape *s, int transposed, const float *T, int64_t ldT, bool out_bf16,
+                                   void *y, int64_t OH, int64_t OW, cudaStream_t stream) {
+    OffsetAddArgs a;
+    a.T = T;
+    a.ldT = ldT;
+    a.y = y;
+    a.n = s->n; a.h = s->h; a.w = s->w; a.f = s->f; a.r = s->r; a.s = s->s;
+    a.oh = OH; a.ow = OW;
+    a.pad = s->pad; a.stride = s->stride; a.dil = s->dilation;
+    const bool vec4 = (s->f % 4 == 0) && (ldT % 4 == 0) && aligned16(T) && (out_bf16 ? (reinterpret_cast<uintptr_t>(y) & 7) == 0 : aligned16(y));
+    const int VEC = vec4 ? 4 : 1;
+    a.items = s->n * OH * OW * (s->f / VEC);
+    const int64_t blocks = std::min<int64_t>(ceil_div(a.items, 256), (int64_t)num_sms() * 16);
+    const unsigned g = (unsigned)std::max<int64_t>(blocks, 1);
+    if (!transposed) {
+        if (vec4) {
+            if (out_bf16) offset_add_kernel<4, true><<<g, 256, 0, stream>>>(a);
+            else offset_add_kernel<4, false><<<g, 256, 0, stream>>>(a);
+        } else {
+            if (out_bf16) offset_add_kernel<1, true><<<g, 256, 0, stream>>>(a);
+            else offset_add_kernel<1, false><<<g, 256, 0, stream>>>(a);
+        }
+    } else {
+        if (vec4) {
+            if (out_bf16) selective_add_kernel<4, true><<<g, 256, 0, stream>>>(a);
+            else selective_add_kernel<4, false><<<g, 256, 0, stream>>>(a);
+        } else {
+            if (out_bf16) selective_add_kernel<1, true><<<g, 256, 0, stream>>>(a);
+            else selective_add_kernel<1, false><<<g, 256, 0, stream>>>(a);
+        }
+    }
+    CHECK_LAUNCH();
+    return OLLIE_OK;
+}
+
+extern "C" ollie_status ollie_offset_add(const ollie_conv_shape *shape, int transposed, const float *T, int64_t ldT,
+                                         ollie_dtype y_dtype, void *y_nhwc, ollie_stream_t stream) {
+    int64_t OH, OW;
+    ollie_status st = check_shape(shape, transposed, &OH, &OW);
+    if (st != OLLIE_OK) return st;
+    if (transposed && shape->dilation != 1)
+        return fail(OLLIE_E_UNSUPPORTED, "selective addition implemented for dilation 1 only");
+    if (!T || !y_nhwc) return fail(OLLIE_E_INVALID, "null pointer");
+    if (ldT < shape->r * shape->s * shape->f) return fail(OLLIE_E_INVALID, "ldT < r*s*f");
+    st = run_offset_add(shape, transposed, T, ldT, y_dtype == OLLIE_BF16, y_nhwc, OH, OW, (cudaStream_t)stream);
+    return st == OLLIE_OK ? ok() : st;
+}
+
+// ------------------------------------------------------------------------ derived layers
+static bool is_identity_offset_add(const ollie_conv_shape *s, int transposed) {
+    // r = s = 1, pad 0, stride 1: OffsetAdd / selective add is the identity eOperator
+    // (SURVEY 8(d) note) and is eliminated -- the GEMM epilogue writes Y.
+    return s->r == 1 && s->s == 1 && s->pad == 0 && s->stride == 1 && (!transposed || s->output_padding == 0);
+}
+
+static int resolve_plan(const ollie_conv_shape *s, ollie_dtype dtype, int plan, int transposed) {
+    if (plan == OLLIE_PLAN_FUSED || plan == OLLIE_PLAN_UNFUSED) return plan;
+    if (is_identity_offset_add(s, transposed)) return OLLIE_PLAN_UNFUSED;
+    return fused_supported(s, dtype == OLLIE_TF32, transposed) ? OLLIE_PLAN_FUSED : OLLIE_PLAN_UNFUSED;
+}
+
+extern "C" size_t ollie_workspace_bytes(const ollie_conv_shape *s, ollie_dtype dtype, int plan, int transposed) {
+    if (!s || check_shape(s, transposed, nullptr, nullptr) != OLLIE_OK) return 0;
+    if (resolve_plan(s, dtype, plan, transposed) != OLLIE_PLAN_UNFUSED) return 0;
+    if (is_identity_offset_add(s, transposed)) return 0;
+    return (size_t)(s->n * s->h * s->w) * (size_t)ldT_of(s) * sizeof(float);
+}
+
+static ollie_status derived_layer(const ollie_conv_shape *s, ollie_dtype dtype, const void *x, const void *wp, void *y,
+                                  void *ws, size_t ws_bytes, int plan, cudaStream_t stream, int transposed) {
+    int64_t OH, OW;
+    ollie_status st = check_shape(s, transposed, &OH, &OW);
+    if (st != OLLIE_OK) return st;
+    if (dtype != OLLIE_BF16 && dtype != OLLIE_TF32) return fail(OLLIE_E_UNSUPPORTED, "dtype must be BF16 or TF32");
+    if (transposed && s->dilation != 1) return fail(OLLIE_E_UNSUPPORTED, "ConvTranspose2d with dilation != 1");
+    if (!x || !wp || !y) return fail(OLLIE_E_INVALID, "null pointer");
+    if (!aligned16(x) || !aligned16(wp) || !aligned16(y)) return fail(OLLIE_E_ALIGN, "base pointers must be 16-byte aligned");
+    const bool tf32 = dtype == OLLIE_TF32;
+    if ((s->c * elem_size(dtype)) % 16 != 0)
+        return fail(OLLIE_E_ALIGN, "c*sizeof(elem) = %lld not a multiple of 16: channel-pad x with an eOperator",
+                    (long long)(s->c * elem_size(dtype)));
+    const int rp = resolve_plan(s, dtype, plan, transposed);
+    const int64_t M = s->n * s->h * s->w, N = s->r * s->s * s->f, K = s->c;
+    if (rp == OLLIE_PLAN_FUSED) {
+        if (!fused_supported(s, tf32, transposed))
+            return fail(OLLIE_E_UNSUPPORTED, "fused plan not available for this shape/dtype");
+        st = run_fused(s, tf32, transposed, x, wp, y, OH, OW, stream);
+        return st == OLLIE_OK ? ok() : st;
+    }
+    if (is_identity_offset_add(s, transposed)) {
+        // a6: identity eOperator eliminated -- the GEMM writes Y = X W'^T directly.
+        st = run_gemm(M, N, K, tf32, x, wp, y, N, !tf32, stream);
+        return st == OLLIE_OK ? ok() : st;
+    }
+    const int64_t ldT = ldT_of(s);
+    const size_t need = (size_t)M * (size_t)ldT * sizeof(float);
+    if (!ws || ws_bytes < need)
+        return fail(OLLIE_E_WORKSPACE, "unfused plan needs %zu workspace bytes for T (got %zu)", need, ws_bytes);
+    if (!aligned16(ws)) return fail(OLLIE_E_ALIGN, "workspace must be 16-byte aligned");
+    st = run_gemm(M, N, K, tf32, x, wp, ws, ldT, false, stream);
+    if (st != OLLIE_OK) return st;
+    st = run_offset_add(s, transposed, (const float *)ws, ldT, !tf32, y, OH, OW, stream);
+    return st == OLLIE_OK ? ok() : st;
+}
+
+extern "C" ollie_status ollie_conv2d_derived(const ollie_conv_shape *shape, ollie_dtype dtype, const void *x_nhwc,
+                                             const void *w_prep, void *y_nhwc, void *ws, size_t ws_bytes, int plan,
+                                             ollie_stream_t stream) {
+    return derived_layer(shape, dtype, x_nhwc, w_prep, y_nhwc, ws, ws_bytes, plan, (cudaStream_t)stream, 0);
+}
+extern "C" ollie_status ollie_convtranspose2d_derived(const ollie_conv_shape *shape, ollie_dtype dtype,
+                                                      const void *x_nhwc, const void *w_prep, void *y_nhwc, void *ws,
+                                                      size_t ws_bytes, int plan, ollie_stream_t stream) {
+    return derived_layer(shape, dtype, x_nhwc, w_prep, y_nhwc, ws, ws_bytes, plan, (cudaStream_t)stream, 1);
+}
+
+// ------------------------------------------------------------------------ eOperators
+namespace {
+
+struct Interval {
+    int64_t lo, hi;  // inclusive
+};
+
+int64_t fdiv(int64_t a, int64_t d) {
+    int64_t q = a / d;
+    return (q * d > a) ? q - 1 : q;
+}
+
+// Symbolic simplification used by both the bounds check and the identity test:
+// coef_div * (x // d) + coef_mod * (x % d) == coef_mod * x  when coef_div == coef_mod * d.
+struct NormTerm {
+    int32_t iter, kind;
+    int64_t div, coef;
+};
+std::vector<NormTerm> normalize(const ollie_index &ix) {
+    std::vector<NormTerm> ts;
+    for (int t = 0; t < ix.nterms; ++t) ts.push_back({ix.term[t].iter, ix.term[t].kind, ix.term[t].div, ix.term[t].coef});
+    bool changed = true;
+    while (changed) {
+        changed = false;
+        for (size_t a = 0; a < ts.size() && !changed; ++a) {
+            if (ts[a].kind != OLLIE_ATOM_FLOORDIV) continue;
+            for (size_t b = 0; b < ts.size() && !changed; ++b) {
+                if (ts[b].kind == OLLIE_ATOM_MOD && ts[b].iter == ts[a].iter && ts[b].div == ts[a].div &&
+                    ts[a].coef == ts[b].coef * ts[a].div) {
+                    NormTerm m{ts[a].iter, OLLIE_ATOM_ITER, 1, ts[b].coef};
+                    std::vector<NormTerm> nt;
+                    for (size_t k = 0; k < ts.size(); ++k)
+                        if (k != a && k != b) nt.push_back(ts[k]);
+                    nt.push_back(m);
+                    ts.swap(nt);
+                    changed = true;
+                }
+            }
+        }
+    }
+    // merge plain terms of the same iterator
+    std::vector<NormTerm> out;
+    for (auto &t : ts) {
+        bool merged = false;
+        for (auto &o : out)
+            if (o.kind == t.kind && o.iter == t.iter && o.div == t.div) {
+                o.coef += t.coef;
+                merged = true;
+            }
+        if (!merged) out.push_back(t);
+    }
+    std::vector<NormTerm> nz;
+    for (auto &o : out)
+        if (o.coef != 0) nz.push_back(o);
+    return nz;
+}
+
+Interval index_interval(const ollie_index &ix, const int64_t *lo, const int64_t *hi /*exclusive*/) {
+    Interval r{ix.c0, ix.c0};
+    for (const NormTerm &t : normalize(ix)) {
+        int64_t a = lo[t.iter], b = hi[t.iter] - 1;
+        Interval at;
+        if (t.kind == OLLIE_ATOM_ITER) at = {a, b};
+        else if (t.kind == OLLIE_ATOM_FLOORDIV) at = {fdiv(a, t.div), fdiv(b, t.div)};
+        else {
+            if (b - a + 1 >= t.div) at = {0, t.div - 1};
+            else {
+                int64_t ma = a - fdiv(a, t.div) * t.div, mb = b - fdiv(b, t.div) * t.div;
+                at = ma <= mb ? Interval{ma, mb} : Interval{0, t.div - 1};
+            }
+        }
+        if (t.coef >= 0) {
+            r.lo += t.coef * at.lo;
+            r.hi += t.coef * at.hi;
+        } else {
+            r.lo += t.coef * at.hi;
+            r.hi += t.coef * at.lo;
+        }
+    }
+    return r;
+}
+
+ollie_status validate_scope(const ollie_eop *e, int k) {
+    const ollie_scope &s = e->scope[k];
+    if (s.n_trav < 1 || s.n_trav > OLLIE_MAX_DIMS || s.n_sum < 0 || s.n_sum > OLLIE_MAX_DIMS ||
+        s.n_trav + s.n_sum > EOPD_MAX_ITERS)
+        return fail(OLLIE_E_INVALID, "scope %d: iterator counts out of range", k);
+    for (int d = 0; d < s.n_trav; ++d)
+        if (s.trav_lo[d] >= s.trav_hi[d]) return fail(OLLIE_E_INVALID, "scope %d: EmptyRange (traversal %d)", k, d);
+    for (int d = 0; d < s.n_sum; ++d)
+        if (s.sum_lo[d] >= s.sum_hi[d]) return fail(OLLIE_E_INVALID, "scope %d: EmptyRange (summation %d)", k, d);
+    if (s.n_acc < 0 || s.n_acc > OLLIE_MAX_ACCESS) return fail(OLLIE_E_INVALID, "scope %d: too many accesses", k);
+    if (s.n_ins < 1 || s.n_ins > OLLIE_MAX_INSTR) return fail(OLLIE_E_INVALID, "scope %d: body length", k);
+    const int nit = s.n_trav + s.n_sum;
+    int64_t lo[EOPD_MAX_ITERS], hi[EOPD_MAX_ITERS];
+    for (int d = 0; d < s.n_trav; ++d) { lo[d] = s.trav_lo[d]; hi[d] = s.trav_hi[d]; }
+    for (int d = 0; d < s.n_sum; ++d) { lo[s.n_trav + d] = s.sum_lo[d]; hi[s.n_trav + d] = s.sum_hi[d]; }
+    for (int a = 0; a < s.n_acc; ++a) {
+        const ollie_access &ac = s.acc[a];
+        const int64_t *ext_lo, *ext_hi;
+        int64_t elo[OLLIE_MAX_DIMS], ehi[OLLIE_MAX_DIMS];
+        int nd;
+        if (ac.tensor >= 0) {
+            if (ac.tensor >= e->n_in) return fail(OLLIE_E_INVALID, "scope %d access %d: unknown tensor", k, a);
+            const ollie_tensor &t = e->in[ac.tensor];
+            nd = t.ndim;
+            for (int d = 0; d < nd; ++d) { elo[d] = -t.pad_lo[d]; ehi[d] = t.shape[d] + t.pad_hi[d]; }
+        } else {
+            if (ac.tensor != -1 || k != 0 || e->n_scopes != 2)
+                return fail(OLLIE_E_INVALID, "scope %d access %d: nested-scope reference invalid", k, a);
+            const ollie_scope &s1 = e->scope[1];
+            nd = s1.n_trav;
+            for (int d = 0; d < nd; ++d) { elo[d] = s1.trav_lo[d] - s1.pad_lo[d]; ehi[d] = s1.trav_hi[d] + s1.pad_hi[d]; }
+        }
+        ext_lo = elo;
+        ext_hi = ehi;
+        if (ac.ndim != nd) return fail(OLLIE_E_INVALID, "scope %d access %d: ArityMismatch (%d vs %d)", k, a, ac.ndim, nd);
+        for (int d = 0; d < nd; ++d) {
+            const ollie_index &ix = ac.idx[d];
+            if (ix.nterms < 0 || ix.nterms > OLLIE_MAX_TERMS) return fail(OLLIE_E_INVALID, "too many terms");
+            for (int t = 0; t < ix.nterms; ++t) {
+                const ollie_term &tm = ix.term[t];
+                if (tm.iter < 0 || tm.iter >= nit)
+                    return fail(OLLIE_E_INVALID, "scope %d access %d dim %d: UndeclaredIterator %d", k, a, d, tm.iter);
+                if (tm.kind < 0 || tm.kind > 2) return fail(OLLIE_E_INVALID, "bad atom kind");
+                if (tm.kind != OLLIE_ATOM_ITER && tm.div <= 0) return fail(OLLIE_E_INVALID, "divisor must be > 0");
+                if (tm.div > INT32_MAX || tm.coef > INT32_MAX || tm.coef < INT32_MIN)
+                    return fail(OLLIE_E_UNSUPPORTED, "coefficient / divisor exceeds int32");
+            }
+            Interval iv = index_interval(ix, lo, hi);
+            if (iv.lo < ext_lo[d] || iv.hi >= ext_hi[d])
+                return fail(OLLIE_E_OOB, "scope %d access %d dim %d reads [%lld, %lld] outside the pad band [%lld, %lld)",
+                            k, a, d, (long long)iv.lo, (long long)iv.hi, (long long)ext_lo[d], (long long)ext_hi[d]);
+        }
+    }
+    // body: postfix well-formedness
+    int depth = 0;
+    for (int p = 0; p < s.n_ins; ++p) {
+        const ollie_instr &in = s.body[p];
+        switch (in.op) {
+            case OLLIE_OP_PUSH_ACCESS:
+                if (in.arg < 0 || in.arg >= s.n_acc) return fail(OLLIE_E_INVALID, "body: bad access id");
+                depth++;
+                break;
+            case OLLIE_OP_PUSH_CONST: depth++; break;
+            case OLLIE_OP_NEG:
+                if (depth < 1) return fail(OLLIE_E_INVALID, "body: stack underflow");
+                break;
+            case OLLIE_OP_ADD: case OLLIE_OP_MUL: case OLLIE_OP_SUB: case OLLIE_OP_MAX: case OLLIE_OP_MIN:
+                if (depth < 2) return fail(OLLIE_E_INVALID, "body: stack underflow");
+                depth--;
+                break;
+            default: return fail(OLLIE_E_INVALID, "body: unknown op %d", in.op);
+        }
+        if (depth > EOPD_STACK) return fail(OLLIE_E_UNSUPPORTED, "body: stack deeper than %d", EOPD_STACK);
+    }
+    if (depth != 1) return fail(OLLIE_E_INVALID, "body leaves %d values on the stack", depth);
+    return OLLIE_OK;
+}
+
+ollie_status validate_eop(const ollie_eop *e) {
+    if (!e) return fail(OLLIE_E_INVALID, "null eop");
+    if (e->n_in < 0 || e->n_in > OLLIE_MAX_INPUTS) return fail(OLLIE_E_INVALID, "n_in out of range");
+    if (e->n_scopes < 1 || e->n_scopes > 2) return fail(OLLIE_E_INVALID, "n_scopes must be 1 or 2");
+    if (e->out_dtype != OLLIE_BF16 && e->out_dtype != OLLIE_FP32) return fail(OLLIE_E_UNSUPPORTED, "out dtype");
+    for (int k = 0; k < e->n_in; ++k) {
+        const ollie_tensor &t = e->in[k];
+        if (t.ndim < 1 || t.ndim > OLLIE_MAX_DIMS) return fail(OLLIE_E_INVALID, "input %d: ndim", k);
+        if (t.dtype != OLLIE_BF16 && t.dtype != OLLIE_FP32) return fail(OLLIE_E_UNSUPPORTED, "input %d dtype", k);
+        for (int d = 0; d < t.ndim; ++d)
+            if (t.shape[d] <= 0 || t.pad_lo[d] < 0 || t.pad_hi[d] < 0)
+                return fail(OLLIE_E_INVALID, "input %d: EmptyRange / negative pad", k);
+    }
+    if (e->n_scopes == 2) {
+        const ollie_scope &s1 = e->scope[1];
+        for (int d = 0; d < s1.n_trav && d < OLLIE_MAX_DIMS; ++d)
+            if (s1.pad_lo[d] < 0 || s1.pad_hi[d] < 0) return fail(OLLIE_E_INVALID, "scope 1: negative pad");
+        for (int a = 0; a < s1.n_acc && a < OLLIE_MAX_ACCESS; ++a)
+            if (s1.acc[a].tensor < 0) return fail(OLLIE_E_INVALID, "scope 1 may only read inputs");
+    }
+    for (int k = 0; k < e->n_scopes; ++k) {
+        ollie_status st = validate_scope(e, k);
+        if (st != OLLIE_OK) return st;
+    }
+    return OLLIE_OK;
+}
+
+int64_t out_elems_of(const ollie_eop *e) {
+    int64_t n = 1;
+    for (int d = 0; d < e->scope[0].n_trav; ++d) n *= e->scope[0].trav_hi[d] - e->scope[0].trav_lo[d];
+    return n;
+}
+
+bool is_pure_indexing(const ollie_eop *e) {
+    const ollie_scope &s = e->scope[0];
+    return e->n_scopes == 1 && s.n_sum == 0 && s.n_acc == 1 && s.n_ins == 1 && s.body[0].op == OLLIE_OP_PUSH_ACCESS &&
+           s.acc[0].tensor >= 0;
+}
+
+// Identity eOperator: squash input and output to 1-D and check the map is
+// the identity.  Symbolic for affine maps (after the div/mod recombination above);
+// exhaustive enumeration for other maps up to 2^22 elements; otherwise "not identity".
+bool is_identity(const ollie_eop *e) {
+    if (!is_pure_indexing(e) || e->n_in != 1) return false;
+    const ollie_scope &s = e->scope[0];
+    const ollie_tensor &t = e->in[s.acc[0].tensor];
+    if (t.dtype != e->out_dtype) return false;
+    int64_t in_elems = 1;
+    for (int d = 0; d < t.ndim; ++d) in_elems *= t.shape[d];
+    const int64_t oe = out_elems_of(e);
+    if (in_elems != oe) return false;
+    int64_t lo[EOPD_MAX_ITERS], hi[EOPD_MAX_ITERS];
+    for (int d = 0; d < s.n_trav; ++d) { lo[d] = s.trav_lo[d]; hi[d] = s.trav_hi[d]; }
+    // no pad-band reads allowed
+    for (int d = 0; d < t.ndim; ++d) {
+        Interval iv = index_interval(s.acc[0].idx[d], lo, hi);
+        if (iv.lo < 0 || iv.hi >= t.shape[d]) return false;
+    }
+    int64_t istride[OLLIE_MAX_DIMS], ostride[OLLIE_MAX_DIMS];
+    istride[t.ndim - 1] = 1;
+    for (int d = t.ndim - 2; d >= 0; --d) istride[d] = istride[d + 1] * t.shape[d + 1];
+    ostride[s.n_trav - 1] = 1;
+    for (int d = s.n_trav - 2; d >= 0; --d) ostride[d] = ostride[d + 1] * (s.trav_hi[d + 1] - s.trav_lo[d + 1]);
+    // symbolic attempt
+    bool affine = true;
+    int64_t coef[EOPD_MAX_ITERS] = {0};
+    int64_t c = 0;
+    for (int d = 0; d < t.ndim && affine; ++d) {
+        c += istride[d] * s.acc[0].idx[d].c0;
+        for (const NormTerm &nt : normalize(s.acc[0].idx[d])) {
+            if (nt.kind != OLLIE_ATOM_ITER) { affine = false; break; }
+            coef[nt.iter] += istride[d] * nt.coef;
+        }
+    }
+    if (affine) {
+        // in_linear(x) = c + sum_k coef[k] x_k must equal out_linear(x) = sum_k ostride[k] (x_k - lo_k)
+        // on the whole box: equal slopes on every non-degenerate iterator, equal at x = lo.
+        int64_t at_lo = c;
+        for (int k = 0; k < s.n_trav; ++k) {
+            if (s.trav_hi[k] - s.trav_lo[k] > 1 && coef[k] != ostride[k]) return false;
+            at_lo += coef[k] * s.trav_lo[k];
+        }
+        return at_lo == 0;
+    }
+    if (oe > (1ll << 22)) return false;
+    int64_t it[EOPD_MAX_ITERS];
+    for (int64_t o = 0; o < oe; ++o) {
+        int64_t q = o;
+        for (int d = s.n_trav - 1; d >= 0; --d) {
+            const int64_t wdt = s.trav_hi[d] - s.trav_lo[d];
+            it[d] = s.trav_lo[d] + q % wdt;
+            q /= wdt;
+        }
+        int64_t lin = 0;
+        for (int d = 0; d < t.ndim; ++d) {
+            const ollie_index &ix = s.acc[0].idx[d];
+            int64_t v = ix.c0;
+            for (int k = 0; k < ix.nterms; ++k) {
+                int64_t a = it[ix.term[k].iter];
+                if (ix.term[k].kind == OLLIE_ATOM_FLOORDIV) a = fdiv(a, ix.term[k].div);
+                else if (ix.term[k].kind == OLLIE_ATOM_MOD) a = a - fdiv(a, ix.term[k].div) * ix.term[k].div;
+                v += ix.term[k].coef * a;
+            }
+            lin += v * istride[d];
+        }
+        if (lin != o) return false;
+    }
+    return true;
+}
+
+ollie_status compile_eop(const ollie_eop *e, const void *const *inputs, void *out, EopDev *dv) {
+    memset(dv, 0, sizeof *dv);
+    for (int k = 0; k < e->n_in; ++k) {
+        dv->in[k] = inputs[k];
+        dv->in_bf16[k] = e->in[k].dtype == OLLIE_BF16;
+    }
+    dv->out = out;
+    dv->out_bf16 = e->out_dtype == OLLIE_BF16;
+    dv->n_scopes = e->n_scopes;
+    dv->out_elems = out_elems_of(e);
+    int nt = 0, nd = 0, na = 0;
+    for (int k = 0; k < e->n_scopes; ++k) {
+        const ollie_scope &s = e->scope[k];
+        DScope &d = dv->sc[k];
+        d.n_trav = s.n_trav;
+        d.n_sum = s.n_sum;
+        d.n_ins = s.n_ins;
+        d.n_acc = s.n_acc;
+        d.a_begin = na;
+        d.sum_count = 1;
+        for (int i = 0; i < s.n_trav; ++i) { d.lo[i] = s.trav_lo[i]; d.width[i] = s.trav_hi[i] - s.trav_lo[i]; }
+        for (int i = 0; i < s.n_sum; ++i) {
+            d.lo[s.n_trav + i] = s.sum_lo[i];
+            d.width[s.n_trav + i] = s.sum_hi[i] - s.sum_lo[i];
+            d.sum_count *= d.width[s.n_trav + i];
+        }
+        for (int p = 0; p < s.n_ins; ++p) { d.op[p] = s.body[p].op; d.arg[p] = s.body[p].arg; d.cval[p] = s.body[p].cval; }
+        for (int a = 0; a < s.n_acc; ++a) {
+            if (na >= 2 * EOPD_MAX_ACC) return fail(OLLIE_E_UNSUPPORTED, "too many accesses");
+            const ollie_access &ac = s.acc[a];
+            DAcc &da = dv->acc[na++];
+            da.tensor = ac.tensor;
+            da.d_begin = nd;
+            da.ndim = ac.ndim;
+            int64_t stride = 1;
+            for (int dd = ac.ndim - 1; dd >= 0; --dd) {
+                if (nd >= EOPD_MAX_DIMS) return fail(OLLIE_E_UNSUPPORTED, "eop too large: > %d access dims", EOPD_MAX_DIMS);
+                DDim &dm = dv->dims[da.d_begin + dd];
+                const ollie_index &ix = ac.idx[dd];
+                dm.c0 = ix.c0;
+                if (ac.tensor >= 0) {
+                    dm.extent = e->in[ac.tensor].shape[dd];
+                    dm.lo = 0;
+                    dm.stride = stride;
+                    stride *= dm.extent;
+                } else {
+                    dm.extent = e->scope[1].trav_hi[dd] - e->scope[1].trav_lo[dd];
+                    dm.lo = e->scope[1].trav_lo[dd];
+                    dm.stride = 0;
+                }
+            }
+            nd += ac.ndim;
+            for (int dd = 0; dd < ac.ndim; ++dd) {
+                DDim &dm = dv->dims[da.d_begin + dd];
+                const ollie_index &ix = ac.idx[dd];
+                dm.t_begin = nt;
+                dm.t_count = ix.nterms;
+                for (int t = 0; t < ix.nterms; ++t) {
+                    if (nt >= EOPD_MAX_TERMS) return fail(OLLIE_E_UNSUPPORTED, "eop too large: > %d terms", EOPD_MAX_TERMS);
+                    DTerm &tm = dv->terms[nt++];
+                    tm.iter = ix.term[t].iter;
+                    tm.kind = ix.term[t].kind;
+                    tm.div = (int32_t)ix.term[t].div;
+                    tm.coef = (int32_t)ix.term[t].coef;
+                }
+            }
+        }
+    }
+    return OLLIE_OK;
+}
+
+int64_t tensor_bytes(const ollie_tensor &t) {
+    int64_t n = 1;
+    for (int d = 0; d < t.ndim; ++d) n *= t.shape[d];
+    return n * (int64_t)elem_size(t.dtype);
+}
+
+}  // namespace
+
+extern "C" ollie_status ollie_eop_analyze(const ollie_eop *eop, ollie_eop_info *info) {
+    ollie_status st = validate_eop(eop);
+    if (st != OLLIE_OK) return st;
+    if (!info) return fail(OLLIE_E_INVALID, "null info");
+    info->is_identity = is_identity(eop);
+    info->pure_indexing = is_pure_indexing(eop);
+    info->out_elems = out_elems_of(eop);
+    int64_t bi = 0;
+    for (int k = 0; k < eop->n_in; ++k) bi += tensor_bytes(eop->in[k]);
+    info->bytes_in = info->is_identity ? 0 : bi;
+    info->bytes_out = info->is_identity ? 0 : info->out_elems * (int64_t)elem_size(eop->out_dtype);
+    return ok();
+}
+
+extern "C" ollie_status ollie_eop_eval(const ollie_eop *eop, const void *const *inputs, void *output,
+                                       ollie_stream_t stream) {
+    ollie_status st = validate_eop(eop);
+    if (st != OLLIE_OK) return st;
+    if (!output || (eop->n_in > 0 && !inputs)) return fail(OLLIE_E_INVALID, "null pointer");
+    for (int k = 0; k < eop->n_in; ++k)
+        if (!inputs[k]) return fail(OLLIE_E_INVALID, "null input %d", k);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (is_identity(eop)) {
+        // a6: identity eOperator elimination -- nothing to launch when aliased.
+        if (inputs[0] == output) return ok();
+        CUDA_TRY(cudaMemcpyAsync(output, inputs[0], (size_t)tensor_bytes(eop->in[0]), cudaMemcpyDeviceToDevice, s));
+        return ok();
+    }
+    EopDev dv;
+    st = compile_eop(eop, inputs, output, &dv);
+    if (st != OLLIE_OK) return st;
+    const int64_t blocks = std::min<int64_t>(ceil_div(dv.out_elems, 256), (int64_t)num_sms() * 32);
+    eop_eval_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(dv);
+    CHECK_LAUNCH();
+    return ok();
+}

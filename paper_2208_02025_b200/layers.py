@@ -1,0 +1,57 @@
+"""Layer objects over the C ABI: own the prepared weight (compile-time DLT)
+and the unfused-plan workspace; calling one runs the derived program on the GPU.
+Device memory comes from torch; every computation is a libollie kernel."""
+from __future__ import annotations
+
+import torch
+
+from . import ollie as _o
+
+_DT = {"bf16": _o.BF16, "tf32": _o.TF32}
+_TORCH = {"bf16": torch.bfloat16, "tf32": torch.float32}
+
+
+class DerivedConv:
+    """Conv2d (transposed=False) or ConvTranspose2d (transposed=True) as the derived
+    program merged-GEMM + OffsetAdd / selective addition."""
+
+    def __init__(self, n, c, h, w, f, r, s, pad=0, stride=1, dilation=1, output_padding=0,
+                 transposed=False, dtype="bf16", plan=_o.PLAN_AUTO, device="cuda"):
+        self.shape = _o.conv_shape(n, c, h, w, f, r, s, pad, stride, dilation, output_padding)
+        self.transposed = bool(transposed)
+        self.dtype = dtype
+        self.code = _DT[dtype]
+        self.plan = plan
+        self.device = torch.device(device)
+        self.oh, self.ow = _o.output_hw(self.shape, self.transposed)
+        self.w_prep = torch.empty(r * s * f, c, dtype=_TORCH[dtype], device=self.device)
+        nbytes = _o.workspace_bytes(self.shape, self.code, plan, self.transposed)
+        self.ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device) if nbytes else None
+        self.ws_bytes = nbytes
+
+    @classmethod
+    def from_layer(cls, layer, plan=_o.PLAN_AUTO, device="cuda"):
+        return cls(layer.n, layer.c, layer.h, layer.w, layer.f, layer.r, layer.s, layer.pad, layer.stride,
+                   layer.dilation, layer.output_padding, layer.transposed, layer.dtype, plan, device)
+
+    def prepare(self, weight: torch.Tensor, stream=None):
+        """a0: weight DLT, once ("compile time").  weight is PyTorch-layout, on the device."""
+        weight = weight.contiguous()
+        if self.transposed:
+            _o.prepare_weight_convtranspose2d(self.shape, self.code, weight, self.w_prep, stream)
+        else:
+            _o.prepare_weight_conv2d(self.shape, self.code, weight, self.w_prep, stream)
+        return self
+
+    def out_shape(self):
+        return (self.shape.n, self.oh, self.ow, self.shape.f)
+
+    def new_output(self):
+        return torch.empty(self.out_shape(), dtype=_TORCH[self.dtype], device=self.device)
+
+    def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        if y is None:
+            y = self.new_output()
+        fn = _o.convtranspose2d_derived if self.transposed else _o.conv2d_derived
+        fn(self.shape, self.code, x, self.w_prep, y, self.ws, self.ws_bytes, self.plan, stream)
+        return y
