@@ -1,0 +1,548 @@
+#!/usr/bin/env python
+"""Benchmark of the derived-convolution hot path (Ollie, arXiv 2208.02025) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config resnet18] [--impl ours|reference]
+
+A "step" is one pass of the whole hot path over one batch of the configured workload:
+every layer of the config runs as its derived program (merged tcgen05 GEMM + OffsetAdd /
+selective add, fused or unfused, plus the layout eOperators it needs) through the C ABI.
+Default workload = BASELINE.json configs[1]: the four ResNet-18 3x3 conv layers at
+batch 16 and at batch 1, bf16.  Metric: useful TFLOP/s
+(2*n*OH*OW*f*c*r*s per layer) of the whole step; higher is better.
+
+Timing: W untimed warm-up steps; then exactly K steps, each preceded by an
+L2 flush (a 2x L2-size write, outside the per-step events), each captured as one CUDA
+graph replay bracketed by CUDA events on the launching stream; a barrier +
+synchronize on both sides of the K steps; max over ranks.  N > 1 (torchrun, NCCL):
+every rank runs its own batch (weak scaling); `--allgather` adds the a9 output
+all-gather to every step.
+
+`--impl reference` times the fp64 CPU oracle on a bounded sample of the same workload
+(the reference arm for this tier); it is the only other place besides tests/ and
+__graft_entry__.smoke() that executes oracle/ code, together with the cpu_baseline leg.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import ollie_synth as syn  # noqa: E402
+
+CHAINED = {"fsrcnn", "dcgan"}
+CONFIG_TEXT = {
+    "resnet18": "ResNet-18 3x3 conv layers (c=f=64..512, 56x56..7x7) batch 1 and 16, bf16",
+    "csrnet": "CSRNet dilated 3x3 conv (dilation=2, c=f=512, 64x64) batch 16",
+    "infogan": "InfoGAN ConvTranspose2d 4x4 stride 2 (256->448, 2x2) batch 16",
+    "dcgan": "DCGAN ConvTranspose2d 4x4 stride 2 generator stack batch 16",
+    "fsrcnn": "FSRCNN full conv+convT stack batch 64",
+    "motivating": "motivating example 3x3 Conv2d n=1 c=4 h=w=8 f=4 (TF32)",
+    "paper_conv3x3": "paper Table Conv3x3 [1,512,7,7] (TF32)",
+    "resnet18_s2": "ResNet-18 stride-2 3x3 layers batch 16 (strided extension)",
+}
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            mp = json.load(fh)
+        return {"hbm_gbs": mp["hbm_gbs"], "bf16_tflops": mp["bf16_tflops"],
+                "bf16_tflops_sustained": mp.get("bf16_tflops_sustained"), "source": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+# ------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [v.strip() for v in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        loaded = [v for v in sm if v > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------- oracle arm
+def _oracle_sample(layers, chained, max_flop):
+    """Bounded sample of the workload for the CPU oracle: the first images of each layer
+    (a conv's images are independent), sized to ~max_flop useful flops."""
+    per_layer = max_flop / max(1, len(layers))
+    plan = []
+    for li, lay in enumerate(layers):
+        per_img = lay.useful_flops / lay.n
+        k = int(max(1, min(lay.n, per_layer // per_img)))
+        plan.append((li, lay, k))
+    return plan
+
+
+def run_oracle_sample(cfg, layers, plan):
+    import oracle
+    flops = 0
+    t0 = time.perf_counter()
+    for li, lay, k in plan:
+        x, w = syn.layer_inputs(lay.with_batch(k), syn.config_seed(cfg, li))
+        if lay.transposed:
+            oracle.conv_transpose2d(x, w, lay.pad, lay.stride, lay.dilation, lay.output_padding)
+        else:
+            oracle.conv2d(x, w, lay.pad, lay.stride, lay.dilation)
+        flops += lay.useful_flops / lay.n * k
+    return flops, time.perf_counter() - t0
+
+
+def reference_main(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    cfg = args.config
+    layers = syn.CONFIGS[cfg]
+    plan = _oracle_sample(layers, cfg in CHAINED, args.ref_flop)
+    for _ in range(args.warmup):
+        run_oracle_sample(cfg, layers, plan)
+    times, flops = [], 0
+    for _ in range(args.steps):
+        f, t = run_oracle_sample(cfg, layers, plan)
+        times.append(t)
+        flops = f
+    ms = 1e3 * statistics.mean(times)
+    val = flops / (ms * 1e-3) / 1e12
+    sample = "; ".join(f"{lay.name}: {k}/{lay.n} images" for _, lay, k in plan)
+    line = {"metric": "derived conv useful TFLOP/s (whole step)", "value": val, "unit": "TFLOP/s",
+            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded, ollie_synth)",
+            "config": {"workload": CONFIG_TEXT.get(cfg, cfg), "name": cfg, "sample": sample},
+            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------- GPU arm
+def _alg_bytes_gemm(lay, es_in):
+    M, N, K = lay.gemm_mnk
+    return M * K * es_in + N * K * es_in + M * N * 4
+
+
+def _alg_bytes_offset_add(lay, es_out):
+    """In-bounds (pixel, tap) T reads (fp32) + Y writes: counted exactly per output."""
+    taps = 0
+    if lay.transposed:
+        for oh in range(lay.oh):
+            for i in range(lay.r):
+                a = oh + lay.pad - i
+                if a >= 0 and a % lay.stride == 0 and a // lay.stride < lay.h:
+                    taps += 1
+        th = taps
+        taps = 0
+        for ow in range(lay.ow):
+            for j in range(lay.s):
+                a = ow + lay.pad - j
+                if a >= 0 and a % lay.stride == 0 and a // lay.stride < lay.w:
+                    taps += 1
+        tw = taps
+    else:
+        th = sum(1 for oh in range(lay.oh) for i in range(lay.r)
+                 if 0 <= oh * lay.stride - lay.pad + i * lay.dilation < lay.h)
+        tw = sum(1 for ow in range(lay.ow) for j in range(lay.s)
+                 if 0 <= ow * lay.stride - lay.pad + j * lay.dilation < lay.w)
+    return lay.n * th * tw * lay.f * 4 + lay.n * lay.oh * lay.ow * lay.f * es_out
+
+
+def gpu_main(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    from paper_2208_02025_b200 import ollie as O
+    from paper_2208_02025_b200.stack import DerivedStack
+
+    cfg = args.config
+    layers = syn.CONFIGS[cfg]
+    chained = cfg in CHAINED
+    plan = {"auto": O.PLAN_AUTO, "fused": O.PLAN_FUSED, "unfused": O.PLAN_UNFUSED}[args.plan]
+    stack = DerivedStack(layers, chained, plan=plan, device=dev)
+    # inputs: seeded per (config, layer, rank) -- each rank's batch is its own (weak scaling)
+    xs_host, ws_dev = [], []
+    for li, lay in enumerate(layers):
+        x, w = syn.layer_inputs(lay, syn.config_seed(cfg, li) + 7919 * rank)
+        xs_host.append(x)
+        ws_dev.append(w.to(dev))
+    stack.prepare(ws_dev)
+    if chained:
+        x_dev = xs_host[0].to(dev)
+        inputs = x_dev
+        in_host = [xs_host[0].pin_memory()]
+        in_dev = [x_dev]
+    else:
+        in_dev = [x.to(dev) for x in xs_host]
+        inputs = in_dev
+        in_host = [x.pin_memory() for x in xs_host]
+    outs = [sl.y for sl in stack.layers]
+    out_dev = [outs[-1]] if chained else outs
+    out_host = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in out_dev]
+    h2d = sum(t.numel() * t.element_size() for t in in_host)
+    d2h = sum(t.numel() * t.element_size() for t in out_host)
+
+    gather_bufs = None
+    if args.allgather and world > 1:
+        gather_bufs = [torch.empty((world * o.shape[0],) + tuple(o.shape[1:]), dtype=o.dtype, device=dev)
+                       for o in out_dev]
+
+    flops = sum(l.useful_flops for l in layers)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(max(2 * l2, 64 << 20), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        stack(inputs, stream=stream.cuda_stream)
+
+    def gather():
+        if gather_bufs is not None:
+            for o, g in zip(out_dev, gather_bufs):
+                dist.all_gather_into_tensor(g, o)
+
+    # warm-up + graph capture of one step (the per-layer launches of the derived program)
+    with torch.cuda.stream(stream):
+        for _ in range(max(1, args.warmup)):
+            step()
+    stream.synchronize()
+    graph = None
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            step()
+        torch.cuda.synchronize()
+
+    def replay():
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            replay()
+            gather()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: K steps, L2 flushed before each, events per step
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        time.sleep(0.3)
+        t_wall0 = time.perf_counter()
+        with torch.cuda.stream(stream):
+            for k in range(args.steps):
+                flush.fill_(k & 0xFF)
+                starts[k].record(stream)
+                replay()
+                gather()
+                ends[k].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t_wall = time.perf_counter() - t_wall0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms = statistics.mean(step_ms)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * flops / (ms * 1e-3) / 1e12
+
+    # ---------------- e2e: same step through the public API with host buffers
+    e2e_s, e2e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with torch.cuda.stream(stream):
+        e2e_s.record(stream)
+        for k in range(args.steps):
+            for hd, dd in zip(in_host, in_dev):
+                dd.copy_(hd, non_blocking=True)
+            step()
+            gather()
+            for dd, hh in zip(out_dev, out_host):
+                hh.copy_(dd, non_blocking=True)
+        e2e_e.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e2e_s.elapsed_time(e2e_e) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_val = world * flops / (e2e_ms * 1e-3) / 1e12
+
+    # ---------------- roofline: per-kernel CUDA events on the launching stream
+    peaks = _peaks()
+    per = {}
+    es_in = 2 if layers[0].dtype == "bf16" else 4
+    reps = max(3, min(args.steps, 20))
+    with torch.cuda.stream(stream):
+        for rep in range(reps):
+            x = inputs if chained else None
+            for li, sl in enumerate(stack.layers):
+                src = x if chained else inputs[li]
+                lay = sl.padded
+                if sl.pad_eop is not None:
+                    flush.fill_(rep & 0xFF)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    O.eop_eval(sl.pad_eop, [src], sl.x_pad, stream.cuda_stream)
+                    e1.record(stream)
+                    b = src.numel() * src.element_size() + sl.x_pad.numel() * sl.x_pad.element_size()
+                    per.setdefault("eop_channel_pad", []).append((e0, e1, b, 0, "hbm"))
+                    src = sl.x_pad
+                conv = sl.conv
+                flush.fill_(rep & 0xFF)
+                if conv.ws_bytes:      # unfused: time the two kernels of the derived program separately
+                    M, N, K = lay.gemm_mnk
+                    ldT = -(-N // 4) * 4
+                    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                    e0.record(stream)
+                    O.merged_gemm(M, N, K, conv.code, src, conv.w_prep, conv.ws, ldT, stream.cuda_stream)
+                    e1.record(stream)
+                    O.offset_add(conv.shape, conv.transposed, conv.ws, ldT,
+                                 O.BF16 if lay.dtype == "bf16" else O.FP32, sl.y, stream.cuda_stream)
+                    e2.record(stream)
+                    per.setdefault("merged_gemm", []).append((e0, e1, _alg_bytes_gemm(lay, es_in), 2 * M * N * K, "hbm"))
+                    per.setdefault("offset_add" if not lay.transposed else "selective_add", []).append(
+                        (e1, e2, _alg_bytes_offset_add(lay, es_in), 0, "hbm"))
+                else:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    conv(src, sl.y, stream.cuda_stream)
+                    e1.record(stream)
+                    b = (lay.n * lay.h * lay.w * lay.c + lay.r * lay.s * lay.f * lay.c +
+                         lay.n * lay.oh * lay.ow * lay.f) * es_in
+                    ai = lay.useful_flops / b
+                    bound = "tensor" if ai * peaks["hbm_gbs"] * 1e9 > peaks["bf16_tflops"] * 1e12 else "hbm"
+                    per.setdefault("fused_conv", []).append((e0, e1, b, lay.useful_flops, bound))
+                x = sl.y
+    torch.cuda.synchronize()
+    kern = {}
+    for name, recs in per.items():
+        tot_ms = sum(a.elapsed_time(b) for a, b, *_ in recs)
+        byts = sum(r[2] for r in recs)
+        fl = sum(r[3] for r in recs)
+        bound = max(set(r[4] for r in recs), key=[r[4] for r in recs].count)
+        kern[name] = {"ms_per_step": tot_ms / reps, "gbs": byts / (tot_ms * 1e-3) / 1e9,
+                      "tflops": fl / (tot_ms * 1e-3) / 1e12, "bound": bound, "launches_per_step": len(recs) // reps}
+    dom = max(kern, key=lambda k: kern[k]["ms_per_step"])
+    d = kern[dom]
+    if d["bound"] == "tensor":
+        peak = peaks["bf16_tflops"] if es_in == 2 else peaks["bf16_tflops"] / 2
+        roof = {"kernel": dom, "bound": "tensor", "achieved": d["tflops"], "peak": peak, "unit": "TFLOP/s",
+                "frac": d["tflops"] / peak}
+    else:
+        roof = {"kernel": dom, "bound": "hbm", "achieved": d["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": d["gbs"] / peaks["hbm_gbs"]}
+    roof["peak_source"] = peaks["source"]
+    roof["traffic"] = _traffic_from_profiles(cfg, dom)
+    roof["share_of_step"] = d["ms_per_step"] / sum(v["ms_per_step"] for v in kern.values())
+
+    # ---------------- cuDNN on the same box, same inputs, same flush + event method
+    cudnn = None
+    if not args.no_cudnn and rank == 0:
+        cudnn = _time_cudnn(layers, chained, xs_host, ws_dev, dev, flush, args.steps, stream)
+
+    result = None
+    if rank == 0:
+        clocks = clk.summary()
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            import oracle
+            splan = _oracle_sample(layers, chained, args.cpu_flop)
+            f, t = run_oracle_sample(cfg, layers, splan)
+            cpu = {"value": f / t / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
+                   "sample": "; ".join(f"{lay.name}: {k}/{lay.n} images" for _, lay, k in splan),
+                   "seconds": t}
+        result = {
+            "metric": "derived conv useful TFLOP/s (whole step)", "value": value, "unit": "TFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": layers[0].dtype, "data": "synthetic (seeded, ollie_synth)",
+            "config": {"workload": CONFIG_TEXT.get(cfg, cfg), "name": cfg,
+                       "layers": [l.name for l in layers], "plan": args.plan,
+                       "l2": "flushed before every step (2x L2 write outside the per-step events)",
+                       "timing": "CUDA graph replay per step, CUDA events on the launching stream, max over ranks",
+                       "allgather": bool(gather_bufs is not None),
+                       "parallelism": f"batch-sharded x{world}" if world > 1 else "1 GPU"},
+            "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_ms},
+            "gpu_launches": stack.launches() * args.steps,
+            "roofline": roof,
+            "kernels": kern,
+            "cudnn": cudnn,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "wall_s_timed_region": t_wall,
+            "per_step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
+        }
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def _traffic_from_profiles(cfg, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(cfg, {}).get(kernel)
+    except Exception:
+        return None
+
+
+def _time_cudnn(layers, chained, xs_host, ws_dev, dev, flush, steps, stream):
+    import torch
+    import torch.nn.functional as F
+    torch.backends.cudnn.benchmark = True
+    torch.backends.cuda.matmul.allow_tf32 = True
+    torch.backends.cudnn.allow_tf32 = True
+    xs = [x.to(dev).permute(0, 3, 1, 2).contiguous(memory_format=torch.channels_last) for x in xs_host]
+    ws = [w.contiguous(memory_format=torch.channels_last) for w in ws_dev]
+
+    def run():
+        x = xs[0]
+        outs = []
+        for li, lay in enumerate(layers):
+            src = x if chained else xs[li]
+            if lay.transposed:
+                y = F.conv_transpose2d(src, ws[li], stride=lay.stride, padding=lay.pad,
+                                       output_padding=lay.output_padding, dilation=lay.dilation)
+            else:
+                y = F.conv2d(src, ws[li], stride=lay.stride, padding=lay.pad, dilation=lay.dilation)
+            outs.append(y)
+            x = y
+        return outs
+
+    with torch.cuda.stream(stream):
+        for _ in range(5):
+            run()
+    torch.cuda.synchronize()
+    per_layer = [0.0] * len(layers)
+    tot = []
+    with torch.cuda.stream(stream):
+        for k in range(steps):
+            flush.fill_(k & 0xFF)
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(layers) + 1)]
+            evs[0].record(stream)
+            x = xs[0]
+            for li, lay in enumerate(layers):
+                src = x if chained else xs[li]
+                if lay.transposed:
+                    x = F.conv_transpose2d(src, ws[li], stride=lay.stride, padding=lay.pad,
+                                           output_padding=lay.output_padding, dilation=lay.dilation)
+                else:
+                    x = F.conv2d(src, ws[li], stride=lay.stride, padding=lay.pad, dilation=lay.dilation)
+                evs[li + 1].record(stream)
+            tot.append(evs)
+    torch.cuda.synchronize()
+    for evs in tot:
+        for li in range(len(layers)):
+            per_layer[li] += evs[li].elapsed_time(evs[li + 1]) / steps
+    ms = statistics.mean(e[0].elapsed_time(e[-1]) for e in tot)
+    flops = sum(l.useful_flops for l in layers)
+    return {"ms_per_step": ms, "tflops": flops / (ms * 1e-3) / 1e12,
+            "per_layer_us": {l.name: 1e3 * t for l, t in zip(layers, per_layer)},
+            "note": "torch F.conv2d/conv_transpose2d channels_last, cudnn.benchmark=True, eager (no graph)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="resnet18", choices=sorted(syn.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--plan", default="auto", choices=["auto", "fused", "unfused"])
+    ap.add_argument("--allgather", action="store_true", help="add the a9 output all-gather to every step (N>1)")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cudnn", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-flop", type=float, default=6e9, help="oracle sample per reference-arm step (flops)")
+    ap.add_argument("--cpu-flop", type=float, default=4e11, help="oracle sample for cpu_baseline (flops)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return reference_main(args)
+    return gpu_main(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
