@@ -199,6 +199,141 @@ extern "C" ollie_status ollie_merged_gemm(int64_t M, int64_t N, int64_t K, ollie
     return st == OLLIE_OK ? ok() : st;
 }
 
+// ------------------------------------------------------------------------ fused plan (a8)
+// Tile geometry + f-slice choice for fused_conv_kernel; see fused_conv.cuh for the design.
+static bool plan_fused(const ollie_conv_shape *s, bool tf32, int transposed, FusedArgs *out, int64_t OH, int64_t OW) {
+    if (transposed || s->stride != 1) return false;
+    const int es = tf32 ? 4 : 2;
+    if ((s->c * es) % 16 != 0) return false;
+    if (s->n > INT32_MAX || s->h > 32768 || s->w > 32768 || s->c > 65535 || s->f > 65535) return false;
+    const int CI = 16 / es, KI = 32 / es, BKfull = 128 / es;
+    FusedArgs a{};
+    a.n = (int)s->n; a.H = (int)s->h; a.W = (int)s->w; a.C = (int)s->c; a.F = (int)s->f;
+    a.R = (int)s->r; a.S = (int)s->s; a.pad = s->pad; a.dil = s->dilation;
+    a.OH = (int)OH; a.OW = (int)OW;
+    a.BK = s->c >= BKfull ? BKfull : (int)((s->c + KI - 1) / KI * KI);
+    a.kchunks = (int)ceil_div(s->c, a.BK);
+    const int nchunk = a.BK / CI;
+    // geometry: minimise tiles per image (128 lanes each), tie-break the smaller patch
+    int best_tiles = INT32_MAX, best_bytes = INT32_MAX;
+    for (int XB = (int)std::min<int64_t>(OW, 128); XB >= 1; --XB) {
+        const int Xb = XB + (a.S - 1) * a.dil;
+        if (Xb > 256) continue;
+        int Yb = std::min<int>((int)OH, (128 - XB) / Xb + 1);
+        if (Yb < 1) continue;
+        const int Yp = Yb + (a.R - 1) * a.dil;
+        if (Yp > 256) continue;
+        const int max_off = ((a.R - 1) * Xb + (a.S - 1)) * a.dil;
+        const int box = 16 * Xb * Yp * nchunk;
+        const int need = (nchunk - 1) * 16 * Xb * Yp + (max_off + 128) * 16;
+        const int stage = (int)ceil_div(std::max(box, need), 1024) * 1024;
+        if (2 * stage + 2 * 16 * 128 > FC_SMEM_BUDGET) continue;
+        const int tiles = (int)(ceil_div(OW, XB) * ceil_div(OH, Yb));
+        if (tiles < best_tiles || (tiles == best_tiles && stage < best_bytes)) {
+            best_tiles = tiles;
+            best_bytes = stage;
+            a.XB = XB; a.Xb = Xb; a.Yb = Yb; a.Yp = Yp;
+            a.a_box_bytes = box;
+            a.a_stage_bytes = stage;
+        }
+    }
+    if (best_tiles == INT32_MAX) return false;
+    a.lbo = 16 * a.Xb * a.Yp;
+    a.tiles_x = (int)ceil_div(OW, a.XB);
+    a.tiles_y = (int)ceil_div(OH, a.Yb);
+    // f-slice (UMMA N): estimated time = waves * taps * K-steps * max(FS/2, 32) cycles
+    const int64_t Fp = ceil_div(s->f, 16) * 16;
+    const int sms = num_sms();
+    double best_t = 1e30;
+    const int taps = a.R * a.S;
+    const int ksteps = a.kchunks * (a.BK / KI);
+    for (int FS : {(int)std::min<int64_t>(Fp, 256), 256, 192, 128, 96, 64, 48, 32, 16}) {
+        if (FS > Fp) continue;
+        const int64_t slices = ceil_div(s->f, FS);
+        const int64_t tiles = (int64_t)a.n * a.tiles_x * a.tiles_y * slices;
+        if (tiles > INT32_MAX) continue;
+        const double waves = (double)ceil_div(tiles, sms);
+        const double t = waves * ((double)taps * ksteps * std::max(FS / 2.0, 32.0) + 200.0);
+        if (t < best_t * 0.999) {
+            best_t = t;
+            a.FS = FS;
+        }
+    }
+    a.f_slices = (int)ceil_div(s->f, a.FS);
+    a.num_tiles = (int)((int64_t)a.n * a.tiles_x * a.tiles_y * a.f_slices);
+    a.b_stage_bytes = a.FS * 128;
+    int budget = FC_SMEM_BUDGET - 1024 - 512;
+    a.na = budget >= 3 * a.a_stage_bytes + 4 * a.b_stage_bytes ? 3 : 2;
+    budget -= a.na * a.a_stage_bytes;
+    a.nb = std::min(8, budget / a.b_stage_bytes);
+    if (a.nb < 2) return false;
+    *out = a;
+    return true;
+}
+
+static size_t fused_smem_bytes(const FusedArgs &a) {
+    return 1024 + (size_t)a.na * a.a_stage_bytes + (size_t)a.nb * a.b_stage_bytes + 512;
+}
+
+static bool fused_supported(const ollie_conv_shape *s, bool tf32, int transposed) {
+    int64_t OH, OW;
+    if (transposed || s->stride != 1) return false;
+    OH = (s->h + 2 * s->pad - (int64_t)s->dilation * (s->r - 1) - 1) / s->stride + 1;
+    OW = (s->w + 2 * s->pad - (int64_t)s->dilation * (s->s - 1) - 1) / s->stride + 1;
+    if (OH <= 0 || OW <= 0) return false;
+    FusedArgs a;
+    return plan_fused(s, tf32, transposed, &a, OH, OW);
+}
+
+template <bool TF32>
+static ollie_status launch_fused_t(const CUtensorMap &tx, const CUtensorMap &tw, const FusedArgs &a, cudaStream_t stream) {
+    auto kern = fused_conv_kernel<TF32>;
+    static bool attr_done[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_done[dev & 63]) {
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_done[dev & 63] = true;
+    }
+    const int grid = (int)std::min<int64_t>(a.num_tiles, num_sms());
+    kern<<<grid, FC_THREADS, fused_smem_bytes(a), stream>>>(tx, tw, a);
+    CHECK_LAUNCH();
+    return OLLIE_OK;
+}
+
+static ollie_status run_fused(const ollie_conv_shape *s, bool tf32, int transposed, const void *x, const void *wp,
+                              void *y, int64_t OH, int64_t OW, cudaStream_t stream) {
+    FusedArgs a;
+    if (!plan_fused(s, tf32, transposed, &a, OH, OW)) return fail(OLLIE_E_UNSUPPORTED, "no fused plan for this shape");
+    a.y = y;
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
+    const int es = tf32 ? 4 : 2, CI = 16 / es;
+    const CUtensorMapDataType dt = tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    CUtensorMap tx, tw;
+    {   // X as 5-D planar view {c_in (16 B), w, h, n, c_out}
+        cuuint64_t dims[5] = {(cuuint64_t)CI, (cuuint64_t)s->w, (cuuint64_t)s->h, (cuuint64_t)s->n,
+                              (cuuint64_t)(s->c / CI)};
+        cuuint64_t strides[4] = {(cuuint64_t)(s->c * es), (cuuint64_t)(s->w * s->c * es),
+                                 (cuuint64_t)(s->h * s->w * s->c * es), 16};
+        cuuint32_t box[5] = {(cuuint32_t)CI, (cuuint32_t)a.Xb, (cuuint32_t)a.Yp, 1, (cuuint32_t)(a.BK / CI)};
+        cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+        CUresult r = enc(&tx, dt, 5, const_cast<void *>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (patch) failed (%d)", (int)r);
+    }
+    {   // W' as 3-D {c, f, tap}: f >= F reads are out of bounds -> zero
+        cuuint64_t dims[3] = {(cuuint64_t)s->c, (cuuint64_t)s->f, (cuuint64_t)(s->r * s->s)};
+        cuuint64_t strides[2] = {(cuuint64_t)(s->c * es), (cuuint64_t)(s->f * s->c * es)};
+        cuuint32_t box[3] = {(cuuint32_t)(128 / es), (cuuint32_t)a.FS, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = enc(&tw, dt, 3, const_cast<void *>(wp), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (weights) failed (%d)", (int)r);
+    }
+    return tf32 ? launch_fused_t<true>(tx, tw, a, stream) : launch_fused_t<false>(tx, tw, a, stream);
+}
+
 // ------------------------------------------------------------------------ shapes
 static ollie_status check_shape(const ollie_conv_shape *s, int transposed, int64_t *oh, int64_t *ow) {
     if (!s) return fail(OLLIE_E_INVALID, "null shape");

@@ -39,7 +39,12 @@ def _run_layer(O, lay, x, w, plan):
     from paper_2208_02025_b200 import DerivedConv
     conv = DerivedConv.from_layer(lay, plan=plan)
     conv.prepare(_dev(w))
-    y = conv(_dev(x))
+    try:
+        y = conv(_dev(x))
+    except O.OllieError as e:
+        if plan == O.PLAN_FUSED and e.status == O.E_UNSUPPORTED:
+            pytest.skip("no fused plan for this layer")
+        raise
     torch.cuda.synchronize()
     return y.float().cpu().numpy()
 
@@ -129,10 +134,16 @@ SMALL = [
     syn.Layer("convt_9x9", 1, 56, 6, 5, 1, 9, 9, pad=4, stride=2, output_padding=1, transposed=True),
     syn.Layer("convt_tf32", 1, 32, 4, 4, 20, 4, 4, pad=1, stride=2, transposed=True, dtype="tf32"),
     syn.Layer("convt_1x1", 1, 16, 5, 5, 8, 1, 1, transposed=True),
+    syn.Layer("r18_7x7_multi", 3, 512, 7, 7, 512, 3, 3, pad=1),
+    syn.Layer("wide_cols", 1, 16, 5, 300, 24, 3, 3, pad=1),
+    syn.Layer("tall_f_tail", 2, 40, 9, 11, 200, 3, 3, pad=0),
+    syn.Layer("dil2_wide", 1, 64, 20, 70, 64, 3, 3, pad=2, dilation=2),
+    syn.Layer("k5_c8", 2, 8, 19, 23, 56, 5, 5, pad=2),
+    syn.Layer("tf32_fused", 2, 36, 13, 9, 40, 3, 3, pad=1, dtype="tf32"),
 ]
 
 
-@pytest.mark.parametrize("plan", [0, 2])
+@pytest.mark.parametrize("plan", [0, 1, 2])
 @pytest.mark.parametrize("lay", SMALL, ids=[l.name for l in SMALL])
 def test_derived_layer_integer_exact(O, lay, plan):
     x, w = syn.layer_inputs(lay, 100, exact_int=True)
@@ -142,7 +153,7 @@ def test_derived_layer_integer_exact(O, lay, plan):
     assert np.array_equal(got, _round_like(ref, lay.dtype))
 
 
-@pytest.mark.parametrize("plan", [0, 2])
+@pytest.mark.parametrize("plan", [0, 1, 2])
 @pytest.mark.parametrize("lay", SMALL, ids=[l.name for l in SMALL])
 def test_derived_layer_random_tolerance(O, lay, plan):
     x, w = syn.layer_inputs(lay, 200)
