@@ -392,6 +392,19 @@ def gpu_main(args):
                 x = sl.y
     torch.cuda.synchronize()
     kern = {}
+    layer_us = {}
+    nrec = {k: 0 for k in per}
+    for rep in range(reps):
+        for li, sl in enumerate(stack.layers):
+            t = 0.0
+            keys = (["eop_channel_pad"] if sl.pad_eop is not None else []) + (
+                ["merged_gemm", "selective_add" if sl.layer.transposed else "offset_add"] if sl.conv.ws_bytes
+                else ["fused_conv"])
+            for k in keys:
+                a0, b0, *_ = per[k][nrec[k]]
+                nrec[k] += 1
+                t += a0.elapsed_time(b0)
+            layer_us[sl.layer.name] = layer_us.get(sl.layer.name, 0.0) + 1e3 * t / reps
     for name, recs in per.items():
         tot_ms = sum(a.elapsed_time(b) for a, b, *_ in recs)
         byts = sum(r[2] for r in recs)
@@ -444,6 +457,9 @@ def gpu_main(args):
             "gpu_launches": stack.launches() * args.steps,
             "roofline": roof,
             "kernels": kern,
+            "layers_us": layer_us,
+            "plans": {sl.layer.name: O.plan_describe(sl.conv.shape, sl.conv.code, sl.conv.plan, sl.conv.transposed)
+                      for sl in stack.layers},
             "cudnn": cudnn,
             "cpu_baseline": cpu,
             "clocks": clocks,

@@ -127,6 +127,12 @@ ollie_status ollie_convtranspose2d_derived(const ollie_conv_shape *shape, ollie_
                                            const void *x_nhwc, const void *w_prep, void *y_nhwc,
                                            void *ws, size_t ws_bytes, int plan, ollie_stream_t stream);
 
+/* Introspection: writes a one-line description of the plan `plan` resolves to for this layer
+ * (kernel choice, tile geometry, f-slice, stages) into buf (NUL-terminated, truncated to len).
+ * Host-only; no launch. */
+ollie_status ollie_plan_describe(const ollie_conv_shape *shape, ollie_dtype dtype, int plan, int transposed,
+                                 char *buf, size_t len);
+
 /* a2 standalone (the merged Matmul of P:1342-1352 on tcgen05 tensor cores):
  *   T[m][n] = sum_k A[m][k] * B[n][k]      A [M][K], B [N][K] in `dtype` (BF16 / TF32),
  *   T fp32 with row stride ldT elements (ldT >= N, ldT % 4 == 0).  K % 8 (bf16) or

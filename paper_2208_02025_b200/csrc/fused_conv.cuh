@@ -38,8 +38,20 @@ struct FusedArgs {
     int32_t lbo;                   // planar chunk stride (bytes) = Yp*Xb*16
     int32_t b_stage_bytes;         // FS * 128
     int32_t na, nb;                // ring depths
+    int32_t MT;                    // M-tiles stacked vertically per work item (share patch + weights)
+    int32_t resident;              // 1: the CTA's whole weight slice stays in smem (loaded once)
+    int32_t nbuf;                  // TMEM accumulator sets (2 = epilogue overlaps the next item)
+    int32_t acc_cols;              // TMEM columns per M-tile accumulator (FS rounded up to 32)
     void *y;
+    long long *trace;              // debug only (nullptr in production): per-CTA timestamps
+    int32_t debug_flags;           // debug only: 1 = skip patch loads, 2 = skip weight loads
 };
+
+// Debug timeline: slot k of CTA b at trace[b * 32 + k] (clock64 relative to kernel entry).
+#define FC_TRACE(k)                                                              \
+    do {                                                                         \
+        if (a.trace) a.trace[blockIdx.x * 32 + (k)] = clock64() - t_entry;       \
+    } while (0)
 
 // K-major, no-swizzle ("interleaved") UMMA smem descriptor: core matrices of 8 rows x 16 B,
 // rows 16 B apart (SBO = 128 B between 8-row groups), K-chunks of 16 B `lbo` bytes apart.
@@ -80,7 +92,7 @@ __device__ __forceinline__ TileCoord fc_tile(const FusedArgs &a, int tile) {
     q /= a.tiles_x;
     const int ty = q % a.tiles_y;
     t.img = q / a.tiles_y;
-    t.y0 = ty * a.Yb;
+    t.y0 = ty * a.Yb * a.MT;
     t.x0 = tx * a.XB;
     t.f0 = fs * a.FS;
     return t;
@@ -95,12 +107,14 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int taps = a.R * a.S;
+    const int nbst = a.resident ? taps * a.kchunks : a.nb;   // B buffers (resident: one per (kc, tap))
     uint8_t *sA = smem;
     uint8_t *sB = sA + a.na * a.a_stage_bytes;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sB + a.nb * a.b_stage_bytes);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sB + nbst * a.b_stage_bytes);
     uint64_t *a_full = bars;
     uint64_t *a_empty = a_full + a.na;
-    uint64_t *b_full = a_empty + a.na;
+    uint64_t *b_full = a_empty + a.na;      // [nb]   (resident: b_full[0] = "all weights loaded")
     uint64_t *b_empty = b_full + a.nb;
     uint64_t *tfull = b_empty + a.nb;
     uint64_t *tempty = tfull + 2;
@@ -108,7 +122,15 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
-    const int taps = a.R * a.S;
+    const long long t_entry = clock64();
+    if (a.trace && threadIdx.x == 0) {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        a.trace[blockIdx.x * 32 + 30] = (long long)gt;
+        a.trace[blockIdx.x * 32 + 31] = smid;
+    }
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmX);
@@ -125,67 +147,189 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) FC_TRACE(0);
 
     if (warp == 0) {
         if (lane == 0) {
             // ===== TMA producer: per tile, per channel chunk: 1 patch + r*s weight tiles =====
             int as = 0, bs = 0;
             uint32_t ap = 0, bp = 0;
-            for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+            if (a.resident && blockIdx.x < a.num_tiles) {
+                // the CTA's f-slice is fixed (grid is a multiple of f_slices): load it once
+                const TileCoord tc0 = fc_tile(a, blockIdx.x);
+                mbar_arrive_expect_tx(&b_full[0], (uint32_t)(nbst * a.b_stage_bytes));
+                for (int kc = 0; kc < a.kchunks; ++kc)
+                    for (int t = 0; t < taps; ++t)
+                        tma_load_3d(sB + (kc * taps + t) * a.b_stage_bytes, &tmW, &b_full[0], kc * (128 / ES), tc0.f0, t);
+            }
+            for (int tile = blockIdx.x; tile < a.num_tiles && !(a.debug_flags & 8); tile += gridDim.x) {
                 const TileCoord tc = fc_tile(a, tile);
-                for (int kc = 0; kc < a.kchunks; ++kc) {
+                for (int kci = 0; kci < a.kchunks; ++kci) {
+                    // per-CTA rotation of the (chunk, tap) order: CTAs sharing an f-slice do not
+                    // request the same weight lines from the same L2 slices at the same time
+                    const int kc = (kci + (int)blockIdx.x / taps) % a.kchunks;
                     mbar_wait(&a_empty[as], ap ^ 1);
-                    mbar_arrive_expect_tx(&a_full[as], (uint32_t)a.a_box_bytes);
-                    tma_load_5d(sA + as * a.a_stage_bytes, &tmX, &a_full[as], 0, tc.x0 - a.pad, tc.y0 - a.pad, tc.img,
-                                kc * (a.BK / CI));
+                    if (a.debug_flags & 1) {
+                        mbar_arrive(&a_full[as]);
+                    } else {
+                        mbar_arrive_expect_tx(&a_full[as], (uint32_t)a.a_box_bytes);
+                        tma_load_5d(sA + as * a.a_stage_bytes, &tmX, &a_full[as], 0, tc.x0 - a.pad, tc.y0 - a.pad,
+                                    tc.img, kc * (a.BK / CI));
+                    }
                     if (++as == a.na) { as = 0; ap ^= 1; }
-                    for (int t = 0; t < taps; ++t) {
+                    if (a.resident || (a.debug_flags & 4)) continue;
+                    for (int ti = 0; ti < taps; ++ti) {
+                        const int t = (ti + (int)blockIdx.x) % taps;
                         mbar_wait(&b_empty[bs], bp ^ 1);
-                        mbar_arrive_expect_tx(&b_full[bs], (uint32_t)a.b_stage_bytes);
-                        tma_load_3d(sB + bs * a.b_stage_bytes, &tmW, &b_full[bs], kc * (128 / ES), tc.f0, t);
+                        if (tile == (int)blockIdx.x && kci * taps + ti <= 6) FC_TRACE(16 + kci * taps + ti);
+                        if (a.debug_flags & 2) {
+                            mbar_arrive(&b_full[bs]);
+                        } else {
+                            mbar_arrive_expect_tx(&b_full[bs], (uint32_t)a.b_stage_bytes);
+                            tma_load_3d(sB + bs * a.b_stage_bytes, &tmW, &b_full[bs], kc * (128 / ES), tc.f0, t);
+                        }
                         if (++bs == a.nb) { bs = 0; bp ^= 1; }
                     }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ===== MMA issuer: D[lane, f] += Patch[lane + off(i,j), c] * W'[(i,j), f, c] =====
+        // ===== MMA issuer: D[lane, f] += Patch[lane + off(i,j), c] * W'[(i,j), f, c] =====
+        // Lean single-thread issue: descriptors are templates + 16-byte-unit address adds, tap
+        // offsets come from a small smem table, no div/mod inside the loop.
+        uint32_t *s_off = reinterpret_cast<uint32_t *>(tmem_slot + 1);      // [taps] (<= 81 entries)
+        for (int t = lane; t < taps; t += 32) {
+            const int i = t / a.S, j = t - (t / a.S) * a.S;
+            s_off[t] = (uint32_t)((i * a.Xb + j) * a.dil);                  // rows of 16 B
+        }
+        __syncwarp();
+        {   // the whole warp runs the loop (warp-uniform values stay in uniform registers)
             const uint32_t idesc = make_idesc(kTF32, 128, (uint32_t)a.FS);
+            const uint64_t adesc_t = ((uint64_t)((a.lbo >> 4) & 0x3FFF) << 16) | ((uint64_t)(128 >> 4) << 32) |
+                                     ((uint64_t)1 << 46);
+            const uint64_t bdesc_t = ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
+                                     ((uint64_t)2 << 61);
+            const uint32_t lbo16 = (uint32_t)a.lbo >> 4;
+            const uint32_t mstride16 = (uint32_t)(a.Yb * a.Xb);             // rows between stacked M-tiles
+            const uint32_t sA16 = smem_u32(sA) >> 4, sB16 = smem_u32(sB) >> 4;
+            const uint32_t astage16 = (uint32_t)a.a_stage_bytes >> 4, bstage16 = (uint32_t)a.b_stage_bytes >> 4;
+            const int MT = a.MT, nb = a.nb, na = a.na, kchunks = a.kchunks, nbuf = a.nbuf, BK = a.BK, C = a.C;
+            const uint32_t acc_cols = (uint32_t)a.acc_cols;
+            const bool resident = a.resident != 0;
+            const bool skipb = (a.debug_flags & 4) != 0;   // debug: no per-tap B handshake
+            const bool tracing = a.trace != nullptr;
+            const int kc0 = ((int)blockIdx.x / taps) % kchunks, t0 = (int)blockIdx.x % taps;
             int as = 0, bs = 0;
             uint32_t ap = 0, bp = 0;
             int acc = 0;
             uint32_t accp = 0;
+            if (resident && blockIdx.x < a.num_tiles) {
+                mbar_wait(&b_full[0], 0);
+                tc_fence_after();
+            }
+            if (a.debug_flags & 8) {   // debug: the microbenchmark's issue loop, same MMA count, no waits
+                const int total = a.kchunks * taps * 4;
+                const uint64_t da0 = adesc_t | (uint64_t)(sA16 & 0x3FFF), db0 = bdesc_t | (uint64_t)(sB16 & 0x3FFF);
+                if (tracing && lane == 0) FC_TRACE(1);
+                const int v = a.debug_flags >> 4;
+                if (elect_one()) {
+                    if (v == 0) {
+                        for (int st = 0; st < total / 16; ++st) {
+#pragma unroll
+                            for (int k = 0; k < 16; ++k)
+                                umma<kTF32>(tmem_base, da0 + (uint64_t)((k & 3) * 2), db0 + (uint64_t)((k & 3) * 2), idesc, 1);
+                        }
+                    } else {
+                        int t = 0;
+                        for (int st = 0; st < total / 4; ++st) {
+                            const uint32_t stage16 = (v & 4) ? (uint32_t)((st / taps) % na) * astage16 : 0u;
+                            if ((v & 8) && st > 0 && st % taps == 0) umma_commit(&a_empty[0]);
+                            const uint64_t ad = (v & 1) ? (adesc_t | (uint64_t)((sA16 + stage16 + s_off[t]) & 0x3FFF)) : da0;
+                            const uint32_t acc0 = (v & 2) ? (uint32_t)st : 1u;
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                umma<kTF32>(tmem_base, ad + (uint64_t)((uint32_t)(2 * k) * lbo16), db0 + (uint64_t)(2 * k),
+                                            idesc, acc0 | (uint32_t)k);
+                            if (++t == taps) t = 0;
+                        }
+                    }
+                    umma_commit(&tfull[0]);
+                }
+                __syncwarp();
+                mbar_wait(&tfull[0], 0);
+                if (tracing && lane == 0) FC_TRACE(3);
+                if (elect_one()) mbar_arrive(&tempty[0]);
+            } else
             for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
                 mbar_wait(&tempty[acc], accp ^ 1);
                 tc_fence_after();
-                const uint32_t d_tmem = tmem_base + (uint32_t)(acc * 256);
-                for (int kc = 0; kc < a.kchunks; ++kc) {
-                    const int kvalid = min(a.BK, a.C - kc * a.BK);
+                const uint32_t d_tmem = tmem_base + (uint32_t)acc * (uint32_t)MT * acc_cols;
+                int kc = kc0;
+                for (int kci = 0; kci < kchunks; ++kci) {
+                    const int kvalid = min(BK, C - kc * BK);
                     const int ksteps = (kvalid + KI - 1) / KI;
                     mbar_wait(&a_full[as], ap);
                     tc_fence_after();
-                    const uint32_t a_base = smem_u32(sA + as * a.a_stage_bytes);
-                    for (int t = 0; t < taps; ++t) {
-                        const int i = t / a.S, j = t - i * a.S;
-                        const uint32_t off = (uint32_t)((i * a.Xb + j) * a.dil) * 16u;
-                        mbar_wait(&b_full[bs], bp);
-                        tc_fence_after();
-                        const uint32_t b_base = smem_u32(sB + bs * a.b_stage_bytes);
-                        for (int k = 0; k < ksteps; ++k) {
-                            umma<kTF32>(d_tmem, make_sdesc_k_interleave(a_base + (uint32_t)(2 * k) * a.lbo + off, a.lbo),
-                                        make_sdesc_k_sw128(b_base + k * 32), idesc, (kc | t | k) != 0);
+                    if (tracing && tile == (int)blockIdx.x && kci == 0 && lane == 0) FC_TRACE(1);
+                    if (tracing && tile == (int)blockIdx.x && lane == 0 && skipb && kci < 8) FC_TRACE(8 + kci);
+                    const uint32_t a16 = sA16 + (uint32_t)as * astage16;
+                    if (elect_one()) {
+                        // one elected thread issues the whole chunk: r*s taps x MT x ksteps MMAs
+                        int t = t0, lbs = bs;
+                        uint32_t lbp = bp;
+                        const bool full_k = ksteps == 4;
+                        for (int ti = 0; ti < taps; ++ti) {
+                            uint32_t b16;
+                            if (resident || skipb) {
+                                b16 = sB16 + (uint32_t)(skipb ? 0 : (kc * taps + t)) * bstage16;
+                            } else {
+                                mbar_wait(&b_full[lbs], lbp);
+                                tc_fence_after();
+                                b16 = sB16 + (uint32_t)lbs * bstage16;
+                            }
+                            const uint64_t ad = adesc_t | (uint64_t)((a16 + s_off[t]) & 0x3FFF);
+                            const uint64_t bd = bdesc_t | (uint64_t)(b16 & 0x3FFF);
+                            const uint32_t accum = (uint32_t)(kci | ti);
+                            if (full_k) {
+                                for (int m = 0; m < MT; ++m) {
+                                    const uint64_t adm = ad + (uint64_t)((uint32_t)m * mstride16);
+                                    const uint32_t dm = d_tmem + (uint32_t)m * acc_cols;
+#pragma unroll
+                                    for (int k = 0; k < 4; ++k)
+                                        umma<kTF32>(dm, adm + (uint64_t)((uint32_t)(2 * k) * lbo16), bd + (uint64_t)(2 * k),
+                                                    idesc, accum | (uint32_t)k);
+                                }
+                            } else {
+                                for (int m = 0; m < MT; ++m) {
+                                    const uint64_t adm = ad + (uint64_t)((uint32_t)m * mstride16);
+                                    const uint32_t dm = d_tmem + (uint32_t)m * acc_cols;
+                                    for (int k = 0; k < ksteps; ++k)
+                                        umma<kTF32>(dm, adm + (uint64_t)((uint32_t)(2 * k) * lbo16), bd + (uint64_t)(2 * k),
+                                                    idesc, accum | (uint32_t)k);
+                                }
+                            }
+                            if (!resident && !skipb) {
+                                umma_commit(&b_empty[lbs]);
+                                if (++lbs == nb) { lbs = 0; lbp ^= 1; }
+                            }
+                            if (++t == taps) t = 0;
                         }
-                        umma_commit(&b_empty[bs]);
-                        if (++bs == a.nb) { bs = 0; bp ^= 1; }
+                        umma_commit(&a_empty[as]);
                     }
-                    umma_commit(&a_empty[as]);
-                    if (++as == a.na) { as = 0; ap ^= 1; }
+                    __syncwarp();
+                    if (!resident && !skipb) {          // every lane replays the ring counters
+                        bs += taps;
+                        while (bs >= nb) { bs -= nb; bp ^= 1; }
+                    }
+                    if (++as == na) { as = 0; ap ^= 1; }
+                    if (++kc == kchunks) kc = 0;
                 }
-                umma_commit(&tfull[acc]);
-                acc ^= 1;
-                if (acc == 0) accp ^= 1;
+                if (elect_one()) umma_commit(&tfull[acc]);
+                __syncwarp();
+                if (tracing && tile == (int)blockIdx.x && lane == 0) FC_TRACE(3);
+                if (++acc == nbuf) { acc = 0; accp ^= 1; }
             }
+            if (lane == 0) FC_TRACE(4);
         }
     } else if (warp >= 4) {
         // ===== epilogue: TMEM -> registers -> Y (bf16 RNE or fp32), one output pixel per thread =====
@@ -199,12 +343,14 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             const TileCoord tc = fc_tile(a, tile);
             mbar_wait(&tfull[acc], accp);
             tc_fence_after();
-            const int oy = tc.y0 + ly, ox = tc.x0 + lx;
-            const bool valid = ly < a.Yb && lx < a.XB && oy < a.OH && ox < a.OW;
-            const int64_t pix = ((int64_t)tc.img * a.OH + oy) * a.OW + ox;
+            for (int m = 0; m < a.MT; ++m)
             for (int c = 0; c < a.FS; c += 32) {
+                const int oy = tc.y0 + m * a.Yb + ly, ox = tc.x0 + lx;
+                const bool valid = ly < a.Yb && lx < a.XB && oy < a.OH && ox < a.OW;
+                const int64_t pix = ((int64_t)tc.img * a.OH + oy) * a.OW + ox;
                 uint32_t v[32];
-                tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 256 + c), v);
+                tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) +
+                                       (uint32_t)((acc * a.MT + m) * a.acc_cols + c), v);
                 tmem_ld_wait();
                 const int f = tc.f0 + c;
                 if (valid && f < a.F) {
@@ -249,13 +395,15 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
-            acc ^= 1;
-            if (acc == 0) accp ^= 1;
+            if (threadIdx.x == 128 && tile == (int)blockIdx.x) FC_TRACE(5);
+            if (++acc == a.nbuf) { acc = 0; accp ^= 1; }
         }
+        if (threadIdx.x == 128) FC_TRACE(6);
     }
 
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) FC_TRACE(7);
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<FC_TMEM_COLS>(tmem_base);

@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -201,78 +202,150 @@ extern "C" ollie_status ollie_merged_gemm(int64_t M, int64_t N, int64_t K, ollie
 
 // ------------------------------------------------------------------------ fused plan (a8)
 // Tile geometry + f-slice choice for fused_conv_kernel; see fused_conv.cuh for the design.
-static bool plan_fused(const ollie_conv_shape *s, bool tf32, int transposed, FusedArgs *out, int64_t OH, int64_t OW) {
+static int g_force_mt = 0, g_force_fs = 0, g_force_res = -1;   // debug plan overrides (0 / -1 = auto)
+
+static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transposed, FusedArgs *out, int64_t OH, int64_t OW) {
     if (transposed || s->stride != 1) return false;
     const int es = tf32 ? 4 : 2;
     if ((s->c * es) % 16 != 0) return false;
     if (s->n > INT32_MAX || s->h > 32768 || s->w > 32768 || s->c > 65535 || s->f > 65535) return false;
     const int CI = 16 / es, KI = 32 / es, BKfull = 128 / es;
-    FusedArgs a{};
-    a.n = (int)s->n; a.H = (int)s->h; a.W = (int)s->w; a.C = (int)s->c; a.F = (int)s->f;
-    a.R = (int)s->r; a.S = (int)s->s; a.pad = s->pad; a.dil = s->dilation;
-    a.OH = (int)OH; a.OW = (int)OW;
-    a.BK = s->c >= BKfull ? BKfull : (int)((s->c + KI - 1) / KI * KI);
-    a.kchunks = (int)ceil_div(s->c, a.BK);
-    const int nchunk = a.BK / CI;
-    // geometry: minimise tiles per image (128 lanes each), tie-break the smaller patch
-    int best_tiles = INT32_MAX, best_bytes = INT32_MAX;
+    FusedArgs base{};
+    base.n = (int)s->n; base.H = (int)s->h; base.W = (int)s->w; base.C = (int)s->c; base.F = (int)s->f;
+    base.R = (int)s->r; base.S = (int)s->s; base.pad = s->pad; base.dil = s->dilation;
+    base.OH = (int)OH; base.OW = (int)OW;
+    base.BK = s->c >= BKfull ? BKfull : (int)((s->c + KI - 1) / KI * KI);
+    base.kchunks = (int)ceil_div(s->c, base.BK);
+    const int nchunk = base.BK / CI;
+    const int taps = base.R * base.S;
+    const int ksteps = base.BK / KI;
+    const int sms = num_sms();
+    const int64_t Fp = ceil_div(s->f, 16) * 16;
+    const int budget = FC_SMEM_BUDGET - 1024 - 1024;
+    // Cost model (SM cycles): per work item, MMA time = tcgen05 issue floor or the smem operand
+    // read (A 4 KB + B FS*32 B per instruction at ~128 B/clk), load time = TMA bytes at ~40 B/clk
+    // per SM, the larger wins; items are spread over the persistent grid.
+    double best = 1e300;
+    FusedArgs a_best{};
+    bool found = false;
     for (int XB = (int)std::min<int64_t>(OW, 128); XB >= 1; --XB) {
-        const int Xb = XB + (a.S - 1) * a.dil;
+        const int Xb = XB + (base.S - 1) * base.dil;
         if (Xb > 256) continue;
-        int Yb = std::min<int>((int)OH, (128 - XB) / Xb + 1);
+        const int Yb = std::min<int>((int)OH, (128 - XB) / Xb + 1);
         if (Yb < 1) continue;
-        const int Yp = Yb + (a.R - 1) * a.dil;
-        if (Yp > 256) continue;
-        const int max_off = ((a.R - 1) * Xb + (a.S - 1)) * a.dil;
-        const int box = 16 * Xb * Yp * nchunk;
-        const int need = (nchunk - 1) * 16 * Xb * Yp + (max_off + 128) * 16;
-        const int stage = (int)ceil_div(std::max(box, need), 1024) * 1024;
-        if (2 * stage + 2 * 16 * 128 > FC_SMEM_BUDGET) continue;
-        const int tiles = (int)(ceil_div(OW, XB) * ceil_div(OH, Yb));
-        if (tiles < best_tiles || (tiles == best_tiles && stage < best_bytes)) {
-            best_tiles = tiles;
-            best_bytes = stage;
-            a.XB = XB; a.Xb = Xb; a.Yb = Yb; a.Yp = Yp;
-            a.a_box_bytes = box;
-            a.a_stage_bytes = stage;
+        // skip XB that give the same column-block count as a wider XB (no benefit)
+        if (XB < std::min<int64_t>(OW, 128) && ceil_div(OW, XB) == ceil_div(OW, XB + 1) &&
+            (128 - (XB + 1)) / (Xb + 1) + 1 >= Yb)
+            continue;
+        for (int MT = 1; MT <= 4; ++MT) {
+            if (g_force_mt > 0 && MT != g_force_mt) continue;
+            if (MT > 1 && (int64_t)(MT - 1) * Yb >= OH) break;
+            const int Yp = MT * Yb + (base.R - 1) * base.dil;
+            if (Yp > 256) break;
+            const int max_off = ((base.R - 1) * Xb + (base.S - 1)) * base.dil + (MT - 1) * Yb * Xb;
+            const int box = 16 * Xb * Yp * nchunk;
+            const int need = (nchunk - 1) * 16 * Xb * Yp + (max_off + 128) * 16;
+            const int astage = (int)ceil_div(std::max(box, need), 1024) * 1024;
+            if (2 * astage > budget) break;
+            const int64_t items_sp = (int64_t)base.n * ceil_div(OW, XB) * ceil_div(OH, (int64_t)Yb * MT);
+            for (int FS : {(int)std::min<int64_t>(Fp, 256), 256, 192, 128, 96, 64, 48, 32, 16}) {
+                if (FS > Fp) continue;
+                if (g_force_fs > 0 && FS != g_force_fs) continue;
+                const int acc_cols = (FS + 31) / 32 * 32;
+                if (MT * acc_cols > 512) continue;
+                const int nbuf = 2 * MT * acc_cols <= 512 ? 2 : 1;
+                const int bstage = FS * 128;
+                const int64_t slices = ceil_div(s->f, FS);
+                const int64_t items = items_sp * slices;
+                if (items > INT32_MAX) continue;
+                const int64_t wbytes = (int64_t)taps * base.kchunks * bstage;
+                for (int resident = 0; resident <= 1; ++resident) {
+                    if (g_force_res >= 0 && resident != g_force_res) continue;
+                    int na, nb;
+                    if (resident) {
+                        if (wbytes + 2 * astage > budget) continue;
+                        na = (int)std::min<int64_t>(4, (budget - wbytes) / astage);
+                        nb = 1;
+                    } else {
+                        na = budget >= 3 * astage + 4 * bstage ? 3 : 2;
+                        nb = std::min(8, (budget - na * astage) / bstage);
+                        if (nb < 2) continue;
+                    }
+                    int grid = (int)std::min<int64_t>(items, sms);
+                    if (resident) grid = (int)std::max<int64_t>(slices, grid / slices * slices);
+                    // Calibrated on B200 with tools/sweep_plans.py: real-data tcgen05.mma with N <= 128
+                    // issues at ~80 cycles (N = 256: 128); streamed weight tiles cost more per byte than
+                    // the (larger, once-per-chunk) patch loads; single-buffered TMEM exposes the epilogue.
+                    const double per_cta = (double)ceil_div(items, grid);
+                    const double instr = (double)base.kchunks * taps * ksteps * MT;
+                    const double mma = instr * std::max(FS / 2.0, 40.0 + FS / 3.0) +
+                                       (resident ? 0.0 : 250.0 * base.kchunks * taps);   // per-tap B handshake
+                    const double ld = ((double)base.kchunks * box + (resident ? 0.0 : (double)wbytes)) / 40.0;
+                    const double epi = nbuf == 2 ? 0.0 : MT * (FS / 32.0) * 400.0;
+                    double t = per_cta * (std::max(mma, ld) + epi + 600.0);
+                    if (resident) t += (double)wbytes / 40.0;
+                    if (t < best * 0.995) {
+                        best = t;
+                        FusedArgs a = base;
+                        a.XB = XB; a.Xb = Xb; a.Yb = Yb; a.Yp = Yp; a.MT = MT;
+                        a.a_box_bytes = box; a.a_stage_bytes = astage;
+                        a.FS = FS; a.acc_cols = acc_cols; a.nbuf = nbuf; a.b_stage_bytes = bstage;
+                        a.resident = resident; a.na = na; a.nb = nb;
+                        a_best = a;
+                        found = true;
+                    }
+                }
+            }
         }
     }
-    if (best_tiles == INT32_MAX) return false;
+    if (!found) return false;
+    FusedArgs a = a_best;
     a.lbo = 16 * a.Xb * a.Yp;
     a.tiles_x = (int)ceil_div(OW, a.XB);
-    a.tiles_y = (int)ceil_div(OH, a.Yb);
-    // f-slice (UMMA N): estimated time = waves * taps * K-steps * max(FS/2, 32) cycles
-    const int64_t Fp = ceil_div(s->f, 16) * 16;
-    const int sms = num_sms();
-    double best_t = 1e30;
-    const int taps = a.R * a.S;
-    const int ksteps = a.kchunks * (a.BK / KI);
-    for (int FS : {(int)std::min<int64_t>(Fp, 256), 256, 192, 128, 96, 64, 48, 32, 16}) {
-        if (FS > Fp) continue;
-        const int64_t slices = ceil_div(s->f, FS);
-        const int64_t tiles = (int64_t)a.n * a.tiles_x * a.tiles_y * slices;
-        if (tiles > INT32_MAX) continue;
-        const double waves = (double)ceil_div(tiles, sms);
-        const double t = waves * ((double)taps * ksteps * std::max(FS / 2.0, 32.0) + 200.0);
-        if (t < best_t * 0.999) {
-            best_t = t;
-            a.FS = FS;
-        }
-    }
+    a.tiles_y = (int)ceil_div(OH, (int64_t)a.Yb * a.MT);
     a.f_slices = (int)ceil_div(s->f, a.FS);
     a.num_tiles = (int)((int64_t)a.n * a.tiles_x * a.tiles_y * a.f_slices);
-    a.b_stage_bytes = a.FS * 128;
-    int budget = FC_SMEM_BUDGET - 1024 - 512;
-    a.na = budget >= 3 * a.a_stage_bytes + 4 * a.b_stage_bytes ? 3 : 2;
-    budget -= a.na * a.a_stage_bytes;
-    a.nb = std::min(8, budget / a.b_stage_bytes);
-    if (a.nb < 2) return false;
     *out = a;
     return true;
 }
 
+// Plans are pure functions of (shape, dtype, SM count, overrides): cache them so the host cost of
+// a launch is a lookup (the search is O(10^4) cost-model evaluations).
+struct PlanKey {
+    int64_t v[12];
+    bool operator<(const PlanKey &o) const { return std::lexicographical_compare(v, v + 12, o.v, o.v + 12); }
+};
+static std::mutex g_plan_mu;
+static std::map<PlanKey, std::pair<bool, FusedArgs>> g_plan_cache;
+
+static bool plan_fused(const ollie_conv_shape *s, bool tf32, int transposed, FusedArgs *out, int64_t OH, int64_t OW) {
+    PlanKey k{{s->n, s->c, s->h, s->w, s->f, s->r * 65536 + s->s, s->pad, s->stride * 65536 + s->dilation,
+               (int64_t)tf32 * 2 + transposed, num_sms(), g_force_mt * 1000 + g_force_fs, g_force_res}};
+    {
+        std::lock_guard<std::mutex> g(g_plan_mu);
+        auto it = g_plan_cache.find(k);
+        if (it != g_plan_cache.end()) {
+            if (it->second.first) *out = it->second.second;
+            return it->second.first;
+        }
+    }
+    FusedArgs a{};
+    const bool okp = plan_fused_search(s, tf32, transposed, &a, OH, OW);
+    std::lock_guard<std::mutex> g(g_plan_mu);
+    g_plan_cache[k] = {okp, a};
+    if (okp) *out = a;
+    return okp;
+}
+
+static int fused_grid(const FusedArgs &a) {
+    int grid = (int)std::min<int64_t>(a.num_tiles, num_sms());
+    if (a.resident) grid = std::max(a.f_slices, grid / a.f_slices * a.f_slices);   // fixed f-slice per CTA
+    return grid;
+}
+
 static size_t fused_smem_bytes(const FusedArgs &a) {
-    return 1024 + (size_t)a.na * a.a_stage_bytes + (size_t)a.nb * a.b_stage_bytes + 512;
+    const size_t nbst = a.resident ? (size_t)a.R * a.S * a.kchunks : (size_t)a.nb;
+    return 1024 + (size_t)a.na * a.a_stage_bytes + nbst * a.b_stage_bytes + 1024;
 }
 
 static bool fused_supported(const ollie_conv_shape *s, bool tf32, int transposed) {
@@ -295,17 +368,21 @@ static ollie_status launch_fused_t(const CUtensorMap &tx, const CUtensorMap &tw,
         CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr_done[dev & 63] = true;
     }
-    const int grid = (int)std::min<int64_t>(a.num_tiles, num_sms());
-    kern<<<grid, FC_THREADS, fused_smem_bytes(a), stream>>>(tx, tw, a);
+    kern<<<fused_grid(a), FC_THREADS, fused_smem_bytes(a), stream>>>(tx, tw, a);
     CHECK_LAUNCH();
     return OLLIE_OK;
 }
+
+static long long *g_fc_trace = nullptr;   // debug timeline buffer (ollie_debug_set_trace), off by default
+static int g_fc_debug_flags = 0;          // debug: skip loads (ollie_debug_set_flags), 0 in production
 
 static ollie_status run_fused(const ollie_conv_shape *s, bool tf32, int transposed, const void *x, const void *wp,
                               void *y, int64_t OH, int64_t OW, cudaStream_t stream) {
     FusedArgs a;
     if (!plan_fused(s, tf32, transposed, &a, OH, OW)) return fail(OLLIE_E_UNSUPPORTED, "no fused plan for this shape");
     a.y = y;
+    a.trace = g_fc_trace;
+    a.debug_flags = g_fc_debug_flags;
     PFN_encodeTiled enc = get_encode();
     if (!enc) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
     const int es = tf32 ? 4 : 2, CI = 16 / es;
@@ -903,4 +980,41 @@ extern "C" ollie_status ollie_eop_eval(const ollie_eop *eop, const void *const *
     eop_eval_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(dv);
     CHECK_LAUNCH();
     return ok();
+}
+
+extern "C" ollie_status ollie_plan_describe(const ollie_conv_shape *s, ollie_dtype dtype, int plan, int transposed,
+                                            char *buf, size_t len) {
+    int64_t OH, OW;
+    ollie_status st = check_shape(s, transposed, &OH, &OW);
+    if (st != OLLIE_OK) return st;
+    if (!buf || len == 0) return fail(OLLIE_E_INVALID, "null buffer");
+    const bool tf32 = dtype == OLLIE_TF32;
+    const int rp = resolve_plan(s, dtype, plan, transposed);
+    if (rp == OLLIE_PLAN_FUSED) {
+        FusedArgs a;
+        if (!plan_fused(s, tf32, transposed, &a, OH, OW)) return fail(OLLIE_E_UNSUPPORTED, "no fused plan");
+        snprintf(buf, len,
+                 "fused XB=%d Yb=%d Xb=%d Yp=%d MT=%d FS=%d f_slices=%d resident=%d nbuf=%d na=%d nb=%d BK=%d "
+                 "kchunks=%d tiles=%d grid=%d smem=%zu",
+                 a.XB, a.Yb, a.Xb, a.Yp, a.MT, a.FS, a.f_slices, a.resident, a.nbuf, a.na, a.nb, a.BK, a.kchunks,
+                 a.num_tiles, fused_grid(a), fused_smem_bytes(a));
+    } else if (is_identity_offset_add(s, transposed)) {
+        snprintf(buf, len, "unfused-identity gemm BN=%d (OffsetAdd eliminated)", choose_bn(s->r * s->s * s->f));
+    } else {
+        snprintf(buf, len, "unfused gemm BN=%d ldT=%lld + %s", choose_bn(s->r * s->s * s->f), (long long)ldT_of(s),
+                 transposed ? "selective_add" : "offset_add");
+    }
+    return ok();
+}
+
+// Debug hook (not part of include/ollie.h): route the fused kernel's per-CTA timestamps into a
+// caller-owned device buffer of >= 16 * grid int64 (nullptr switches tracing off).
+extern "C" void ollie_debug_set_trace(void *dev_buf) { g_fc_trace = reinterpret_cast<long long *>(dev_buf); }
+extern "C" void ollie_debug_set_flags(int flags) { g_fc_debug_flags = flags; }
+// Debug hook (not part of include/ollie.h): force fused-plan parameters for sweeps
+// (mt / fs <= 0 and resident < 0 mean "auto").
+extern "C" void ollie_debug_force_plan(int mt, int fs, int resident) {
+    g_force_mt = mt;
+    g_force_fs = fs;
+    g_force_res = resident;
 }

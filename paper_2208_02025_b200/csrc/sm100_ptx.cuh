@@ -148,6 +148,14 @@ __host__ __device__ constexpr uint32_t make_idesc(bool tf32, uint32_t M, uint32_
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
+// One lane of a converged warp returns true (elect.sync); lets warp-uniform code issue
+// single-thread instructions (tcgen05.mma / commit) without divergence.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n}" : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ float bf16_bits_to_float(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
 
 // Round-to-nearest-even fp32 -> bf16 bits (finite inputs; NaN kept quiet).

@@ -88,6 +88,7 @@ _sig = {
                                      c_int, c_void_p]),
     "ollie_convtranspose2d_derived": (c_int, [_P(ConvShape), c_int, c_void_p, c_void_p, c_void_p, c_void_p,
                                               c_size_t, c_int, c_void_p]),
+    "ollie_plan_describe": (c_int, [_P(ConvShape), c_int, c_int, c_int, c_char_p, c_size_t]),
     "ollie_merged_gemm": (c_int, [c_int64, c_int64, c_int64, c_int, c_void_p, c_void_p, c_void_p, c_int64,
                                   c_void_p]),
     "ollie_offset_add": (c_int, [_P(ConvShape), c_int, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
@@ -187,6 +188,12 @@ def convtranspose2d_derived(shape: ConvShape, dtype: int, x, w_prep, y, ws=None,
     _check(_lib.ollie_convtranspose2d_derived(ctypes.byref(shape), dtype, _ptr(x), _ptr(w_prep), _ptr(y),
                                               _ptr(ws), ws_bytes, plan, _stream(stream)),
            "ollie_convtranspose2d_derived")
+
+
+def plan_describe(shape: ConvShape, dtype: int, plan: int = PLAN_AUTO, transposed: bool = False) -> str:
+    buf = ctypes.create_string_buffer(512)
+    _check(_lib.ollie_plan_describe(ctypes.byref(shape), dtype, plan, int(transposed), buf, 512), "ollie_plan_describe")
+    return buf.value.decode()
 
 
 def merged_gemm(M: int, N: int, K: int, dtype: int, A, B, T, ldT: int, stream=None):
