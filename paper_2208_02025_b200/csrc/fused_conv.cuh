@@ -1,4 +1,5 @@
-// fused_conv.cuh -- a8: the merged GEMM with the OffsetAdd fused in, T never materialised.
+// fused_conv.cuh -- a8: the merged GEMM with the OffsetAdd (Conv2d) or the selective addition
+// (ConvTranspose2d) fused in; the intermediate T is never materialised.
 //
 // Derivation: OffsetAdd o Matmul (E7 o E6, P:1049-1051,
 // P:1342-1352) is fused by the chain rule (expression fusion) and the inner
@@ -9,14 +10,21 @@
 // accumulator at its OffsetAdd offset.  On sm_100a the offset Delta_ij becomes a row
 // offset into a haloed input patch held in shared memory in the K-major "interleaved"
 // (no-swizzle) UMMA layout, where rows are 16 bytes apart, so ONE TMA load of the patch
-// per channel chunk feeds all r*s taps: tap (i,j) is the same smem tile read from row
-// i*dil*Xb + j*dil.  Zero padding is TMA out-of-bounds fill.
+// per channel chunk feeds every tap: tap (i,j) is the same smem tile read from another row.
+// Zero padding is TMA out-of-bounds fill.
 //
-// Tile: 128 TMEM lanes = output pixels (y, x) of a Yb x XB block, lane = y*Xb + x where
-// Xb = XB + (S-1)*dil is the patch width; N = FS output channels (<= 256); the fp32
-// accumulator lives in TMEM (two buffers), the epilogue converts and stores Y directly.
-// Persistent, warp-specialised (TMA producer / single-thread MMA issuer / TMEM allocator /
-// 4 epilogue warps), stride 1 only.
+// ConvTranspose2d: the selective addition is split by output residue class
+// (oh mod st, ow mod st) -- expression splitting, P:927-934 -- and every class is a stride-1
+// tap accumulation over the UNPADDED input with the class's tap subset (each output sums
+// only the Matmul outputs that land on it, no work on inserted zeros); the epilogue writes
+// the class interleaved into NHWC Y (the fused "selective add o interleave DLT" pair of
+// SURVEY 8(a) a5).
+//
+// Tile: 128 TMEM lanes = output pixels (y, x) of a Yb x XB block of one class grid, lane =
+// y*Xb + x (Xb = patch width); N = FS output channels (<= 256); MT blocks stacked vertically
+// share one patch and every weight tile; fp32 accumulators in TMEM (two buffers when they
+// fit), epilogue converts and stores Y directly.  Persistent, warp-specialised: warp 0 TMA
+// producer, warp 1 MMA issuer (one elected thread), warp 2 TMEM allocator, warps 4-7 epilogue.
 #pragma once
 #include "../../include/ollie.h"
 #include "sm100_ptx.cuh"
@@ -26,25 +34,37 @@ namespace ollie {
 constexpr int FC_THREADS = 256;
 constexpr uint32_t FC_TMEM_COLS = 512;
 constexpr int FC_SMEM_BUDGET = 225 * 1024;
+constexpr int FC_MAX_CLASSES = 4;
+constexpr int FC_MAX_TAPS = 32;
+
+struct FusedClass {
+    int32_t ntaps;
+    int32_t oy0, ox0;                 // output residue (ConvT) -- 0 for Conv2d
+    int32_t py, px;                   // patch origin relative to the tile origin (input pixels)
+    uint16_t tap_off[FC_MAX_TAPS];    // row offset of the tap inside the patch (16-byte rows)
+    uint8_t tap_w[FC_MAX_TAPS];       // weight tap index i*S + j in W'
+};
 
 struct FusedArgs {
     int32_t n, H, W, C, F, R, S, pad, dil;
     int32_t OH, OW;
-    int32_t XB, Yb, Xb, Yp;        // output cols / rows per tile, patch width / rows
+    int32_t ost;                      // output stride: 1 (Conv2d) or st (ConvTranspose2d classes)
+    int32_t nclass, max_taps;
+    int32_t XB, Yb, Xb, Yp;           // output cols / rows per tile, patch width / rows
     int32_t tiles_x, tiles_y, f_slices, FS, num_tiles;
-    int32_t kchunks, BK;           // channel chunks of BK elements
-    int32_t a_box_bytes;           // bytes TMA writes per patch load
-    int32_t a_stage_bytes;         // patch stage stride in smem (box + slack, 1024-aligned)
-    int32_t lbo;                   // planar chunk stride (bytes) = Yp*Xb*16
-    int32_t b_stage_bytes;         // FS * 128
-    int32_t na, nb;                // ring depths
-    int32_t MT;                    // M-tiles stacked vertically per work item (share patch + weights)
-    int32_t resident;              // 1: the CTA's whole weight slice stays in smem (loaded once)
-    int32_t nbuf;                  // TMEM accumulator sets (2 = epilogue overlaps the next item)
-    int32_t acc_cols;              // TMEM columns per M-tile accumulator (FS rounded up to 32)
+    int32_t kchunks, BK;              // channel chunks of BK elements
+    int32_t a_box_bytes;              // bytes TMA writes per patch load
+    int32_t a_stage_bytes;            // patch stage stride in smem (box + slack, 1024-aligned)
+    int32_t lbo;                      // planar chunk stride (bytes) = Yp*Xb*16
+    int32_t b_stage_bytes;            // FS * 128
+    int32_t na, nb;                   // ring depths
+    int32_t MT;                       // M-tiles stacked vertically per work item
+    int32_t resident;                 // 1: the CTA's whole weight slice stays in smem (loaded once)
+    int32_t nbuf;                     // TMEM accumulator sets (2 = epilogue overlaps the next item)
+    int32_t acc_cols;                 // TMEM columns per M-tile accumulator (FS rounded up to 32)
     void *y;
-    long long *trace;              // debug only (nullptr in production): per-CTA timestamps
-    int32_t debug_flags;           // debug only: 1 = skip patch loads, 2 = skip weight loads
+    long long *trace;                 // debug only (nullptr in production): per-CTA timestamps
+    FusedClass cls[FC_MAX_CLASSES];
 };
 
 // Debug timeline: slot k of CTA b at trace[b * 32 + k] (clock64 relative to kernel entry).
@@ -52,17 +72,6 @@ struct FusedArgs {
     do {                                                                         \
         if (a.trace) a.trace[blockIdx.x * 32 + (k)] = clock64() - t_entry;       \
     } while (0)
-
-// K-major, no-swizzle ("interleaved") UMMA smem descriptor: core matrices of 8 rows x 16 B,
-// rows 16 B apart (SBO = 128 B between 8-row groups), K-chunks of 16 B `lbo` bytes apart.
-__device__ __forceinline__ uint64_t make_sdesc_k_interleave(uint32_t smem_addr, uint32_t lbo) {
-    uint64_t d = 0;
-    d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
-    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-    d |= (uint64_t)(128 >> 4) << 32;
-    d |= (uint64_t)1 << 46;
-    return d;  // layout type 0 = SWIZZLE_NONE
-}
 
 __device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *m, uint64_t *bar, int32_t c0, int32_t c1,
                                             int32_t c2, int32_t c3, int32_t c4) {
@@ -82,8 +91,9 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *m, uin
 }
 
 struct TileCoord {
-    int img, y0, x0, f0;
+    int cls, img, y0, x0, f0;   // y0 / x0: first output row / col of the tile in class-grid units
 };
+// tile = (((cls * n + img) * tiles_y + ty) * tiles_x + tx) * f_slices + fs
 __device__ __forceinline__ TileCoord fc_tile(const FusedArgs &a, int tile) {
     TileCoord t;
     const int fs = tile % a.f_slices;
@@ -91,7 +101,9 @@ __device__ __forceinline__ TileCoord fc_tile(const FusedArgs &a, int tile) {
     const int tx = q % a.tiles_x;
     q /= a.tiles_x;
     const int ty = q % a.tiles_y;
-    t.img = q / a.tiles_y;
+    q /= a.tiles_y;
+    t.img = q % a.n;
+    t.cls = q / a.n;
     t.y0 = ty * a.Yb * a.MT;
     t.x0 = tx * a.XB;
     t.f0 = fs * a.FS;
@@ -100,15 +112,16 @@ __device__ __forceinline__ TileCoord fc_tile(const FusedArgs &a, int tile) {
 
 template <bool kTF32>
 __global__ void __launch_bounds__(FC_THREADS, 1)
-fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, FusedArgs a) {
+fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                  const __grid_constant__ FusedArgs a) {
     constexpr int ES = kTF32 ? 4 : 2;
     constexpr int CI = 16 / ES;                  // elements per 16-byte planar chunk
     constexpr int KI = 32 / ES;                  // K per tcgen05.mma (16 bf16 / 8 tf32)
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int taps = a.R * a.S;
-    const int nbst = a.resident ? taps * a.kchunks : a.nb;   // B buffers (resident: one per (kc, tap))
+    const int wtaps = a.R * a.S;                                    // weight taps (resident layout)
+    const int nbst = a.resident ? wtaps * a.kchunks : a.nb;         // B buffers
     uint8_t *sA = smem;
     uint8_t *sB = sA + a.na * a.a_stage_bytes;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sB + nbst * a.b_stage_bytes);
@@ -126,10 +139,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     if (a.trace && threadIdx.x == 0) {
         unsigned long long gt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        unsigned smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         a.trace[blockIdx.x * 32 + 30] = (long long)gt;
-        a.trace[blockIdx.x * 32 + 31] = smid;
     }
 
     if (warp == 0 && lane == 0) {
@@ -151,7 +161,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
 
     if (warp == 0) {
         if (lane == 0) {
-            // ===== TMA producer: per tile, per channel chunk: 1 patch + r*s weight tiles =====
+            // ===== TMA producer: per work item, per channel chunk: 1 patch + the class's weight tiles =====
             int as = 0, bs = 0;
             uint32_t ap = 0, bp = 0;
             if (a.resident && blockIdx.x < a.num_tiles) {
@@ -159,177 +169,126 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                 const TileCoord tc0 = fc_tile(a, blockIdx.x);
                 mbar_arrive_expect_tx(&b_full[0], (uint32_t)(nbst * a.b_stage_bytes));
                 for (int kc = 0; kc < a.kchunks; ++kc)
-                    for (int t = 0; t < taps; ++t)
-                        tma_load_3d(sB + (kc * taps + t) * a.b_stage_bytes, &tmW, &b_full[0], kc * (128 / ES), tc0.f0, t);
+                    for (int t = 0; t < wtaps; ++t)
+                        tma_load_3d(sB + (kc * wtaps + t) * a.b_stage_bytes, &tmW, &b_full[0], kc * (128 / ES), tc0.f0, t);
             }
-            for (int tile = blockIdx.x; tile < a.num_tiles && !(a.debug_flags & 8); tile += gridDim.x) {
+            for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
                 const TileCoord tc = fc_tile(a, tile);
+                const FusedClass &cl = a.cls[tc.cls];
+                const int ntaps = cl.ntaps;
+                // per-CTA rotation of the (chunk, tap) order spreads identical weight requests in time
+                int kc = ((int)blockIdx.x / ntaps) % a.kchunks;
                 for (int kci = 0; kci < a.kchunks; ++kci) {
-                    // per-CTA rotation of the (chunk, tap) order: CTAs sharing an f-slice do not
-                    // request the same weight lines from the same L2 slices at the same time
-                    const int kc = (kci + (int)blockIdx.x / taps) % a.kchunks;
                     mbar_wait(&a_empty[as], ap ^ 1);
-                    if (a.debug_flags & 1) {
-                        mbar_arrive(&a_full[as]);
-                    } else {
-                        mbar_arrive_expect_tx(&a_full[as], (uint32_t)a.a_box_bytes);
-                        tma_load_5d(sA + as * a.a_stage_bytes, &tmX, &a_full[as], 0, tc.x0 - a.pad, tc.y0 - a.pad,
-                                    tc.img, kc * (a.BK / CI));
-                    }
+                    mbar_arrive_expect_tx(&a_full[as], (uint32_t)a.a_box_bytes);
+                    tma_load_5d(sA + as * a.a_stage_bytes, &tmX, &a_full[as], 0, tc.x0 + cl.px, tc.y0 + cl.py,
+                                tc.img, kc * (a.BK / CI));
                     if (++as == a.na) { as = 0; ap ^= 1; }
-                    if (a.resident || (a.debug_flags & 4)) continue;
-                    for (int ti = 0; ti < taps; ++ti) {
-                        const int t = (ti + (int)blockIdx.x) % taps;
-                        mbar_wait(&b_empty[bs], bp ^ 1);
-                        if (tile == (int)blockIdx.x && kci * taps + ti <= 6) FC_TRACE(16 + kci * taps + ti);
-                        if (a.debug_flags & 2) {
-                            mbar_arrive(&b_full[bs]);
-                        } else {
+                    if (!a.resident) {
+                        int t = (int)blockIdx.x % ntaps;
+                        for (int ti = 0; ti < ntaps; ++ti) {
+                            mbar_wait(&b_empty[bs], bp ^ 1);
                             mbar_arrive_expect_tx(&b_full[bs], (uint32_t)a.b_stage_bytes);
-                            tma_load_3d(sB + bs * a.b_stage_bytes, &tmW, &b_full[bs], kc * (128 / ES), tc.f0, t);
+                            tma_load_3d(sB + bs * a.b_stage_bytes, &tmW, &b_full[bs], kc * (128 / ES), tc.f0, cl.tap_w[t]);
+                            if (++bs == a.nb) { bs = 0; bp ^= 1; }
+                            if (++t == ntaps) t = 0;
                         }
-                        if (++bs == a.nb) { bs = 0; bp ^= 1; }
                     }
+                    if (++kc == a.kchunks) kc = 0;
                 }
             }
         }
     } else if (warp == 1) {
-        // ===== MMA issuer: D[lane, f] += Patch[lane + off(i,j), c] * W'[(i,j), f, c] =====
-        // Lean single-thread issue: descriptors are templates + 16-byte-unit address adds, tap
-        // offsets come from a small smem table, no div/mod inside the loop.
-        uint32_t *s_off = reinterpret_cast<uint32_t *>(tmem_slot + 1);      // [taps] (<= 81 entries)
-        for (int t = lane; t < taps; t += 32) {
-            const int i = t / a.S, j = t - (t / a.S) * a.S;
-            s_off[t] = (uint32_t)((i * a.Xb + j) * a.dil);                  // rows of 16 B
+        // ===== MMA issuer: D[lane, f] += Patch[lane + off(tap), c] * W'[tap, f, c] =====
+        // The whole warp walks the schedule (warp-uniform values live in uniform registers); one
+        // elected thread issues a whole channel chunk: taps x MT x ksteps tcgen05.mma, with
+        // descriptors built as templates + 16-byte-unit address adds.
+        const uint32_t idesc = make_idesc(kTF32, 128, (uint32_t)a.FS);
+        const uint64_t adesc_t = ((uint64_t)((a.lbo >> 4) & 0x3FFF) << 16) | ((uint64_t)(128 >> 4) << 32) |
+                                 ((uint64_t)1 << 46);
+        const uint64_t bdesc_t = ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
+                                 ((uint64_t)2 << 61);
+        const uint32_t lbo16 = (uint32_t)a.lbo >> 4;
+        const uint32_t mstride16 = (uint32_t)(a.Yb * a.Xb);             // rows between stacked M-tiles
+        const uint32_t sA16 = smem_u32(sA) >> 4, sB16 = smem_u32(sB) >> 4;
+        const uint32_t astage16 = (uint32_t)a.a_stage_bytes >> 4, bstage16 = (uint32_t)a.b_stage_bytes >> 4;
+        const int MT = a.MT, nb = a.nb, na = a.na, kchunks = a.kchunks, nbuf = a.nbuf, BK = a.BK, C = a.C;
+        const uint32_t acc_cols = (uint32_t)a.acc_cols;
+        const bool resident = a.resident != 0;
+        int as = 0, bs = 0;
+        uint32_t ap = 0, bp = 0;
+        int acc = 0;
+        uint32_t accp = 0;
+        if (resident && blockIdx.x < a.num_tiles) {
+            mbar_wait(&b_full[0], 0);
+            tc_fence_after();
         }
-        __syncwarp();
-        {   // the whole warp runs the loop (warp-uniform values stay in uniform registers)
-            const uint32_t idesc = make_idesc(kTF32, 128, (uint32_t)a.FS);
-            const uint64_t adesc_t = ((uint64_t)((a.lbo >> 4) & 0x3FFF) << 16) | ((uint64_t)(128 >> 4) << 32) |
-                                     ((uint64_t)1 << 46);
-            const uint64_t bdesc_t = ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
-                                     ((uint64_t)2 << 61);
-            const uint32_t lbo16 = (uint32_t)a.lbo >> 4;
-            const uint32_t mstride16 = (uint32_t)(a.Yb * a.Xb);             // rows between stacked M-tiles
-            const uint32_t sA16 = smem_u32(sA) >> 4, sB16 = smem_u32(sB) >> 4;
-            const uint32_t astage16 = (uint32_t)a.a_stage_bytes >> 4, bstage16 = (uint32_t)a.b_stage_bytes >> 4;
-            const int MT = a.MT, nb = a.nb, na = a.na, kchunks = a.kchunks, nbuf = a.nbuf, BK = a.BK, C = a.C;
-            const uint32_t acc_cols = (uint32_t)a.acc_cols;
-            const bool resident = a.resident != 0;
-            const bool skipb = (a.debug_flags & 4) != 0;   // debug: no per-tap B handshake
-            const bool tracing = a.trace != nullptr;
-            const int kc0 = ((int)blockIdx.x / taps) % kchunks, t0 = (int)blockIdx.x % taps;
-            int as = 0, bs = 0;
-            uint32_t ap = 0, bp = 0;
-            int acc = 0;
-            uint32_t accp = 0;
-            if (resident && blockIdx.x < a.num_tiles) {
-                mbar_wait(&b_full[0], 0);
+        for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+            const TileCoord tc = fc_tile(a, tile);
+            const FusedClass &cl = a.cls[tc.cls];
+            const int ntaps = cl.ntaps;
+            mbar_wait(&tempty[acc], accp ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + (uint32_t)acc * (uint32_t)MT * acc_cols;
+            int kc = ((int)blockIdx.x / ntaps) % kchunks;
+            const int t0 = (int)blockIdx.x % ntaps;
+            for (int kci = 0; kci < kchunks; ++kci) {
+                const int kvalid = min(BK, C - kc * BK);
+                const int ksteps = (kvalid + KI - 1) / KI;
+                mbar_wait(&a_full[as], ap);
                 tc_fence_after();
-            }
-            if (a.debug_flags & 8) {   // debug: the microbenchmark's issue loop, same MMA count, no waits
-                const int total = a.kchunks * taps * 4;
-                const uint64_t da0 = adesc_t | (uint64_t)(sA16 & 0x3FFF), db0 = bdesc_t | (uint64_t)(sB16 & 0x3FFF);
-                if (tracing && lane == 0) FC_TRACE(1);
-                const int v = a.debug_flags >> 4;
+                if (tile == (int)blockIdx.x && kci == 0 && lane == 0) FC_TRACE(1);
+                const uint32_t a16 = sA16 + (uint32_t)as * astage16;
                 if (elect_one()) {
-                    if (v == 0) {
-                        for (int st = 0; st < total / 16; ++st) {
-#pragma unroll
-                            for (int k = 0; k < 16; ++k)
-                                umma<kTF32>(tmem_base, da0 + (uint64_t)((k & 3) * 2), db0 + (uint64_t)((k & 3) * 2), idesc, 1);
+                    int t = t0, lbs = bs;
+                    uint32_t lbp = bp;
+                    const bool full_k = ksteps == 4;
+                    for (int ti = 0; ti < ntaps; ++ti) {
+                        uint32_t b16;
+                        if (resident) {
+                            b16 = sB16 + (uint32_t)(kc * (a.R * a.S) + cl.tap_w[t]) * bstage16;
+                        } else {
+                            mbar_wait(&b_full[lbs], lbp);
+                            tc_fence_after();
+                            b16 = sB16 + (uint32_t)lbs * bstage16;
                         }
-                    } else {
-                        int t = 0;
-                        for (int st = 0; st < total / 4; ++st) {
-                            const uint32_t stage16 = (v & 4) ? (uint32_t)((st / taps) % na) * astage16 : 0u;
-                            if ((v & 8) && st > 0 && st % taps == 0) umma_commit(&a_empty[0]);
-                            const uint64_t ad = (v & 1) ? (adesc_t | (uint64_t)((sA16 + stage16 + s_off[t]) & 0x3FFF)) : da0;
-                            const uint32_t acc0 = (v & 2) ? (uint32_t)st : 1u;
-#pragma unroll
-                            for (int k = 0; k < 4; ++k)
-                                umma<kTF32>(tmem_base, ad + (uint64_t)((uint32_t)(2 * k) * lbo16), db0 + (uint64_t)(2 * k),
-                                            idesc, acc0 | (uint32_t)k);
-                            if (++t == taps) t = 0;
-                        }
-                    }
-                    umma_commit(&tfull[0]);
-                }
-                __syncwarp();
-                mbar_wait(&tfull[0], 0);
-                if (tracing && lane == 0) FC_TRACE(3);
-                if (elect_one()) mbar_arrive(&tempty[0]);
-            } else
-            for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
-                mbar_wait(&tempty[acc], accp ^ 1);
-                tc_fence_after();
-                const uint32_t d_tmem = tmem_base + (uint32_t)acc * (uint32_t)MT * acc_cols;
-                int kc = kc0;
-                for (int kci = 0; kci < kchunks; ++kci) {
-                    const int kvalid = min(BK, C - kc * BK);
-                    const int ksteps = (kvalid + KI - 1) / KI;
-                    mbar_wait(&a_full[as], ap);
-                    tc_fence_after();
-                    if (tracing && tile == (int)blockIdx.x && kci == 0 && lane == 0) FC_TRACE(1);
-                    if (tracing && tile == (int)blockIdx.x && lane == 0 && skipb && kci < 8) FC_TRACE(8 + kci);
-                    const uint32_t a16 = sA16 + (uint32_t)as * astage16;
-                    if (elect_one()) {
-                        // one elected thread issues the whole chunk: r*s taps x MT x ksteps MMAs
-                        int t = t0, lbs = bs;
-                        uint32_t lbp = bp;
-                        const bool full_k = ksteps == 4;
-                        for (int ti = 0; ti < taps; ++ti) {
-                            uint32_t b16;
-                            if (resident || skipb) {
-                                b16 = sB16 + (uint32_t)(skipb ? 0 : (kc * taps + t)) * bstage16;
-                            } else {
-                                mbar_wait(&b_full[lbs], lbp);
-                                tc_fence_after();
-                                b16 = sB16 + (uint32_t)lbs * bstage16;
-                            }
-                            const uint64_t ad = adesc_t | (uint64_t)((a16 + s_off[t]) & 0x3FFF);
-                            const uint64_t bd = bdesc_t | (uint64_t)(b16 & 0x3FFF);
-                            const uint32_t accum = (uint32_t)(kci | ti);
+                        const uint64_t ad = adesc_t | (uint64_t)((a16 + cl.tap_off[t]) & 0x3FFF);
+                        const uint64_t bd = bdesc_t | (uint64_t)(b16 & 0x3FFF);
+                        const uint32_t accum = (uint32_t)(kci | ti);
+                        for (int m = 0; m < MT; ++m) {
+                            const uint64_t adm = ad + (uint64_t)((uint32_t)m * mstride16);
+                            const uint32_t dm = d_tmem + (uint32_t)m * acc_cols;
                             if (full_k) {
-                                for (int m = 0; m < MT; ++m) {
-                                    const uint64_t adm = ad + (uint64_t)((uint32_t)m * mstride16);
-                                    const uint32_t dm = d_tmem + (uint32_t)m * acc_cols;
 #pragma unroll
-                                    for (int k = 0; k < 4; ++k)
-                                        umma<kTF32>(dm, adm + (uint64_t)((uint32_t)(2 * k) * lbo16), bd + (uint64_t)(2 * k),
-                                                    idesc, accum | (uint32_t)k);
-                                }
+                                for (int k = 0; k < 4; ++k)
+                                    umma<kTF32>(dm, adm + (uint64_t)((uint32_t)(2 * k) * lbo16), bd + (uint64_t)(2 * k),
+                                                idesc, accum | (uint32_t)k);
                             } else {
-                                for (int m = 0; m < MT; ++m) {
-                                    const uint64_t adm = ad + (uint64_t)((uint32_t)m * mstride16);
-                                    const uint32_t dm = d_tmem + (uint32_t)m * acc_cols;
-                                    for (int k = 0; k < ksteps; ++k)
-                                        umma<kTF32>(dm, adm + (uint64_t)((uint32_t)(2 * k) * lbo16), bd + (uint64_t)(2 * k),
-                                                    idesc, accum | (uint32_t)k);
-                                }
+                                for (int k = 0; k < ksteps; ++k)
+                                    umma<kTF32>(dm, adm + (uint64_t)((uint32_t)(2 * k) * lbo16), bd + (uint64_t)(2 * k),
+                                                idesc, accum | (uint32_t)k);
                             }
-                            if (!resident && !skipb) {
-                                umma_commit(&b_empty[lbs]);
-                                if (++lbs == nb) { lbs = 0; lbp ^= 1; }
-                            }
-                            if (++t == taps) t = 0;
                         }
-                        umma_commit(&a_empty[as]);
+                        if (!resident) {
+                            umma_commit(&b_empty[lbs]);
+                            if (++lbs == nb) { lbs = 0; lbp ^= 1; }
+                        }
+                        if (++t == ntaps) t = 0;
                     }
-                    __syncwarp();
-                    if (!resident && !skipb) {          // every lane replays the ring counters
-                        bs += taps;
-                        while (bs >= nb) { bs -= nb; bp ^= 1; }
-                    }
-                    if (++as == na) { as = 0; ap ^= 1; }
-                    if (++kc == kchunks) kc = 0;
+                    umma_commit(&a_empty[as]);
                 }
-                if (elect_one()) umma_commit(&tfull[acc]);
                 __syncwarp();
-                if (tracing && tile == (int)blockIdx.x && lane == 0) FC_TRACE(3);
-                if (++acc == nbuf) { acc = 0; accp ^= 1; }
+                if (!resident) {          // every lane replays the ring counters
+                    bs += ntaps;
+                    while (bs >= nb) { bs -= nb; bp ^= 1; }
+                }
+                if (++as == na) { as = 0; ap ^= 1; }
+                if (++kc == kchunks) kc = 0;
             }
-            if (lane == 0) FC_TRACE(4);
+            if (elect_one()) umma_commit(&tfull[acc]);
+            __syncwarp();
+            if (tile == (int)blockIdx.x && lane == 0) FC_TRACE(3);
+            if (++acc == nbuf) { acc = 0; accp ^= 1; }
         }
     } else if (warp >= 4) {
         // ===== epilogue: TMEM -> registers -> Y (bf16 RNE or fp32), one output pixel per thread =====
@@ -341,57 +300,59 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         const bool vec = (a.F % (kTF32 ? 4 : 8)) == 0;
         for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
             const TileCoord tc = fc_tile(a, tile);
+            const FusedClass &cl = a.cls[tc.cls];
             mbar_wait(&tfull[acc], accp);
             tc_fence_after();
             for (int m = 0; m < a.MT; ++m)
-            for (int c = 0; c < a.FS; c += 32) {
-                const int oy = tc.y0 + m * a.Yb + ly, ox = tc.x0 + lx;
-                const bool valid = ly < a.Yb && lx < a.XB && oy < a.OH && ox < a.OW;
-                const int64_t pix = ((int64_t)tc.img * a.OH + oy) * a.OW + ox;
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) +
-                                       (uint32_t)((acc * a.MT + m) * a.acc_cols + c), v);
-                tmem_ld_wait();
-                const int f = tc.f0 + c;
-                if (valid && f < a.F) {
-                    const int nf = min(min(32, a.FS - c), a.F - f);
-                    if constexpr (kTF32) {
-                        float *yp = reinterpret_cast<float *>(a.y) + pix * a.F + f;
-                        if (vec && nf == 32) {
+                for (int c = 0; c < a.FS; c += 32) {
+                    const int oy = (tc.y0 + m * a.Yb + ly) * a.ost + cl.oy0, ox = (tc.x0 + lx) * a.ost + cl.ox0;
+                    const bool valid = ly < a.Yb && lx < a.XB && oy < a.OH && ox < a.OW;
+                    const int64_t pix = ((int64_t)tc.img * a.OH + oy) * a.OW + ox;
+                    uint32_t v[32];
+                    tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) +
+                                           (uint32_t)((acc * a.MT + m) * a.acc_cols + c),
+                                       v);
+                    tmem_ld_wait();
+                    const int f = tc.f0 + c;
+                    if (valid && f < a.F) {
+                        const int nf = min(min(32, a.FS - c), a.F - f);
+                        if constexpr (kTF32) {
+                            float *yp = reinterpret_cast<float *>(a.y) + pix * a.F + f;
+                            if (vec && nf == 32) {
 #pragma unroll
-                            for (int e = 0; e < 32; e += 4)
-                                *reinterpret_cast<float4 *>(yp + e) =
-                                    make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]),
-                                                __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
-                        } else {
+                                for (int e = 0; e < 32; e += 4)
+                                    *reinterpret_cast<float4 *>(yp + e) =
+                                        make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]),
+                                                    __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
+                            } else {
 #pragma unroll
-                            for (int e = 0; e < 32; ++e)
-                                if (e < nf) yp[e] = __uint_as_float(v[e]);
-                        }
-                    } else {
-                        uint16_t *yp = reinterpret_cast<uint16_t *>(a.y) + pix * a.F + f;
-                        if (vec && nf == 32) {
-#pragma unroll
-                            for (int e = 0; e < 32; e += 8) {
-                                uint4 pk;
-                                pk.x = (uint32_t)float_to_bf16_rne(__uint_as_float(v[e])) |
-                                       ((uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 1])) << 16);
-                                pk.y = (uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 2])) |
-                                       ((uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 3])) << 16);
-                                pk.z = (uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 4])) |
-                                       ((uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 5])) << 16);
-                                pk.w = (uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 6])) |
-                                       ((uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 7])) << 16);
-                                *reinterpret_cast<uint4 *>(yp + e) = pk;
+                                for (int e = 0; e < 32; ++e)
+                                    if (e < nf) yp[e] = __uint_as_float(v[e]);
                             }
                         } else {
+                            uint16_t *yp = reinterpret_cast<uint16_t *>(a.y) + pix * a.F + f;
+                            if (vec && nf == 32) {
 #pragma unroll
-                            for (int e = 0; e < 32; ++e)
-                                if (e < nf) yp[e] = float_to_bf16_rne(__uint_as_float(v[e]));
+                                for (int e = 0; e < 32; e += 8) {
+                                    uint4 pk;
+                                    pk.x = (uint32_t)float_to_bf16_rne(__uint_as_float(v[e])) |
+                                           ((uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 1])) << 16);
+                                    pk.y = (uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 2])) |
+                                           ((uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 3])) << 16);
+                                    pk.z = (uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 4])) |
+                                           ((uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 5])) << 16);
+                                    pk.w = (uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 6])) |
+                                           ((uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 7])) << 16);
+                                    *reinterpret_cast<uint4 *>(yp + e) = pk;
+                                }
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < 32; ++e)
+                                    if (e < nf) yp[e] = float_to_bf16_rne(__uint_as_float(v[e]));
+                            }
                         }
                     }
                 }
-            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);

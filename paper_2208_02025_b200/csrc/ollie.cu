@@ -203,51 +203,100 @@ extern "C" ollie_status ollie_merged_gemm(int64_t M, int64_t N, int64_t K, ollie
 // ------------------------------------------------------------------------ fused plan (a8)
 // Tile geometry + f-slice choice for fused_conv_kernel; see fused_conv.cuh for the design.
 static int g_force_mt = 0, g_force_fs = 0, g_force_res = -1;   // debug plan overrides (0 / -1 = auto)
+static thread_local double g_last_fused_cost = 0, g_last_unfused_cost = 0;
 
-static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transposed, FusedArgs *out, int64_t OH, int64_t OW) {
-    if (transposed || s->stride != 1) return false;
+// Per-class tap tables (see fused_conv.cuh).  Conv2d: one class, every tap (i, j) at patch row
+// offset i*dil*Xb + j*dil.  ConvTranspose2d (dilation 1): class (a, b) = output residue; kernel
+// rows i = i0 + st*k with i0 = (a + pad) mod st read input row u + c_a - k, c_a = (a+pad-i0)/st.
+struct ClassGeom {
+    int ntaps_r, ntaps_s, i0, j0, ca, cb;
+};
+static void class_geom(const ollie_conv_shape *s, int a, int b, ClassGeom *g) {
+    const int st = s->stride;
+    g->i0 = (a + s->pad) % st;
+    g->j0 = (b + s->pad) % st;
+    g->ntaps_r = g->i0 < s->r ? (int)((s->r - g->i0 + st - 1) / st) : 0;
+    g->ntaps_s = g->j0 < s->s ? (int)((s->s - g->j0 + st - 1) / st) : 0;
+    g->ca = (a + s->pad - g->i0) / st;
+    g->cb = (b + s->pad - g->j0) / st;
+}
+
+static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transposed, FusedArgs *out, int64_t OH,
+                              int64_t OW) {
     const int es = tf32 ? 4 : 2;
     if ((s->c * es) % 16 != 0) return false;
     if (s->n > INT32_MAX || s->h > 32768 || s->w > 32768 || s->c > 65535 || s->f > 65535) return false;
-    const int CI = 16 / es, KI = 32 / es, BKfull = 128 / es;
     FusedArgs base{};
+    int span_y, span_x, max_taps, nclass;
+    int64_t GH, GW;                               // class-grid (tile space) extent
+    if (!transposed) {
+        if (s->stride != 1 || s->r * s->s > FC_MAX_TAPS) return false;
+        span_y = (int)((s->r - 1) * s->dilation);
+        span_x = (int)((s->s - 1) * s->dilation);
+        max_taps = (int)(s->r * s->s);
+        nclass = 1;
+        GH = OH; GW = OW;
+        base.ost = 1;
+    } else {
+        const int st = s->stride;
+        if (s->dilation != 1 || st * st > FC_MAX_CLASSES) return false;
+        int kr = 0, ks = 0;
+        max_taps = 0;
+        for (int a = 0; a < st; ++a)
+            for (int b = 0; b < st; ++b) {
+                ClassGeom g;
+                class_geom(s, a, b, &g);
+                if (g.ntaps_r == 0 || g.ntaps_s == 0) return false;      // class of pure zeros: not fused
+                kr = std::max(kr, g.ntaps_r);
+                ks = std::max(ks, g.ntaps_s);
+                max_taps = std::max(max_taps, g.ntaps_r * g.ntaps_s);
+            }
+        if (max_taps > FC_MAX_TAPS) return false;
+        span_y = kr - 1;
+        span_x = ks - 1;
+        nclass = st * st;
+        GH = ceil_div(OH, st); GW = ceil_div(OW, st);
+        base.ost = st;
+    }
+    const int CI = 16 / es, KI = 32 / es, BKfull = 128 / es;
     base.n = (int)s->n; base.H = (int)s->h; base.W = (int)s->w; base.C = (int)s->c; base.F = (int)s->f;
     base.R = (int)s->r; base.S = (int)s->s; base.pad = s->pad; base.dil = s->dilation;
     base.OH = (int)OH; base.OW = (int)OW;
+    base.nclass = nclass; base.max_taps = max_taps;
     base.BK = s->c >= BKfull ? BKfull : (int)((s->c + KI - 1) / KI * KI);
     base.kchunks = (int)ceil_div(s->c, base.BK);
     const int nchunk = base.BK / CI;
-    const int taps = base.R * base.S;
+    const int wtaps = (int)(s->r * s->s);
     const int ksteps = base.BK / KI;
     const int sms = num_sms();
     const int64_t Fp = ceil_div(s->f, 16) * 16;
     const int budget = FC_SMEM_BUDGET - 1024 - 1024;
-    // Cost model (SM cycles): per work item, MMA time = tcgen05 issue floor or the smem operand
-    // read (A 4 KB + B FS*32 B per instruction at ~128 B/clk), load time = TMA bytes at ~40 B/clk
-    // per SM, the larger wins; items are spread over the persistent grid.
+    // Cost model (SM cycles), calibrated on B200 with tools/sweep_plans.py: real-data tcgen05.mma
+    // issues at ~max(N/2, 40 + N/3) cycles; a streamed weight tile costs a ~250-cycle handshake;
+    // TMA streams ~40 B/clk per SM; single-buffered TMEM exposes the epilogue.
     double best = 1e300;
     FusedArgs a_best{};
     bool found = false;
-    for (int XB = (int)std::min<int64_t>(OW, 128); XB >= 1; --XB) {
-        const int Xb = XB + (base.S - 1) * base.dil;
+    for (int XB = (int)std::min<int64_t>(GW, 128); XB >= 1; --XB) {
+        const int Xb = XB + span_x;
         if (Xb > 256) continue;
-        const int Yb = std::min<int>((int)OH, (128 - XB) / Xb + 1);
+        const int Yb = (int)std::min<int64_t>(GH, (128 - XB) / Xb + 1);
         if (Yb < 1) continue;
-        // skip XB that give the same column-block count as a wider XB (no benefit)
-        if (XB < std::min<int64_t>(OW, 128) && ceil_div(OW, XB) == ceil_div(OW, XB + 1) &&
+        if (XB < std::min<int64_t>(GW, 128) && ceil_div(GW, XB) == ceil_div(GW, XB + 1) &&
             (128 - (XB + 1)) / (Xb + 1) + 1 >= Yb)
             continue;
         for (int MT = 1; MT <= 4; ++MT) {
             if (g_force_mt > 0 && MT != g_force_mt) continue;
-            if (MT > 1 && (int64_t)(MT - 1) * Yb >= OH) break;
-            const int Yp = MT * Yb + (base.R - 1) * base.dil;
+            if (MT > 1 && (int64_t)(MT - 1) * Yb >= GH) break;
+            const int Yp = MT * Yb + span_y;
             if (Yp > 256) break;
-            const int max_off = ((base.R - 1) * Xb + (base.S - 1)) * base.dil + (MT - 1) * Yb * Xb;
+            const int max_off = span_y * Xb + span_x + (MT - 1) * Yb * Xb;
+            if (max_off >= 65536) break;
             const int box = 16 * Xb * Yp * nchunk;
             const int need = (nchunk - 1) * 16 * Xb * Yp + (max_off + 128) * 16;
             const int astage = (int)ceil_div(std::max(box, need), 1024) * 1024;
             if (2 * astage > budget) break;
-            const int64_t items_sp = (int64_t)base.n * ceil_div(OW, XB) * ceil_div(OH, (int64_t)Yb * MT);
+            const int64_t items_sp = (int64_t)nclass * base.n * ceil_div(GW, XB) * ceil_div(GH, (int64_t)Yb * MT);
             for (int FS : {(int)std::min<int64_t>(Fp, 256), 256, 192, 128, 96, 64, 48, 32, 16}) {
                 if (FS > Fp) continue;
                 if (g_force_fs > 0 && FS != g_force_fs) continue;
@@ -258,7 +307,8 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                 const int64_t slices = ceil_div(s->f, FS);
                 const int64_t items = items_sp * slices;
                 if (items > INT32_MAX) continue;
-                const int64_t wbytes = (int64_t)taps * base.kchunks * bstage;
+                const int64_t wbytes = (int64_t)wtaps * base.kchunks * bstage;          // whole slice
+                const int64_t tbytes = (int64_t)max_taps * base.kchunks * bstage;       // per item
                 for (int resident = 0; resident <= 1; ++resident) {
                     if (g_force_res >= 0 && resident != g_force_res) continue;
                     int na, nb;
@@ -273,14 +323,11 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                     }
                     int grid = (int)std::min<int64_t>(items, sms);
                     if (resident) grid = (int)std::max<int64_t>(slices, grid / slices * slices);
-                    // Calibrated on B200 with tools/sweep_plans.py: real-data tcgen05.mma with N <= 128
-                    // issues at ~80 cycles (N = 256: 128); streamed weight tiles cost more per byte than
-                    // the (larger, once-per-chunk) patch loads; single-buffered TMEM exposes the epilogue.
                     const double per_cta = (double)ceil_div(items, grid);
-                    const double instr = (double)base.kchunks * taps * ksteps * MT;
+                    const double instr = (double)base.kchunks * max_taps * ksteps * MT;
                     const double mma = instr * std::max(FS / 2.0, 40.0 + FS / 3.0) +
-                                       (resident ? 0.0 : 250.0 * base.kchunks * taps);   // per-tap B handshake
-                    const double ld = ((double)base.kchunks * box + (resident ? 0.0 : (double)wbytes)) / 40.0;
+                                       (resident ? 0.0 : 250.0 * base.kchunks * max_taps);
+                    const double ld = ((double)base.kchunks * box + (resident ? 0.0 : (double)tbytes)) / 40.0;
                     const double epi = nbuf == 2 ? 0.0 : MT * (FS / 32.0) * 400.0;
                     double t = per_cta * (std::max(mma, ld) + epi + 600.0);
                     if (resident) t += (double)wbytes / 40.0;
@@ -301,11 +348,51 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
     if (!found) return false;
     FusedArgs a = a_best;
     a.lbo = 16 * a.Xb * a.Yp;
-    a.tiles_x = (int)ceil_div(OW, a.XB);
-    a.tiles_y = (int)ceil_div(OH, (int64_t)a.Yb * a.MT);
+    a.tiles_x = (int)ceil_div(GW, a.XB);
+    a.tiles_y = (int)ceil_div(GH, (int64_t)a.Yb * a.MT);
     a.f_slices = (int)ceil_div(s->f, a.FS);
-    a.num_tiles = (int)((int64_t)a.n * a.tiles_x * a.tiles_y * a.f_slices);
+    a.num_tiles = (int)((int64_t)nclass * a.n * a.tiles_x * a.tiles_y * a.f_slices);
+    // class tables
+    if (!transposed) {
+        FusedClass &c = a.cls[0];
+        c.ntaps = max_taps;
+        c.oy0 = c.ox0 = 0;
+        c.py = -s->pad;
+        c.px = -s->pad;
+        for (int i = 0; i < s->r; ++i)
+            for (int j = 0; j < s->s; ++j) {
+                const int t = (int)(i * s->s + j);
+                c.tap_off[t] = (uint16_t)((i * a.Xb + j) * s->dilation);
+                c.tap_w[t] = (uint8_t)t;
+            }
+    } else {
+        const int st = s->stride;
+        for (int ca = 0; ca < st; ++ca)
+            for (int cb = 0; cb < st; ++cb) {
+                ClassGeom g;
+                class_geom(s, ca, cb, &g);
+                FusedClass &c = a.cls[ca * st + cb];
+                c.ntaps = g.ntaps_r * g.ntaps_s;
+                c.oy0 = ca;
+                c.ox0 = cb;
+                c.py = g.ca - (g.ntaps_r - 1);
+                c.px = g.cb - (g.ntaps_s - 1);
+                for (int k = 0; k < g.ntaps_r; ++k)
+                    for (int l = 0; l < g.ntaps_s; ++l) {
+                        const int t = k * g.ntaps_s + l;
+                        c.tap_off[t] = (uint16_t)((g.ntaps_r - 1 - k) * a.Xb + (g.ntaps_s - 1 - l));
+                        c.tap_w[t] = (uint8_t)((g.i0 + st * k) * s->s + (g.j0 + st * l));
+                    }
+            }
+    }
     *out = a;
+    // the cost of the same layer unfused (GEMM writes T, OffsetAdd reads it back): AUTO only fuses
+    // when the fused estimate is lower
+    const double tbytes_unf = (double)(s->n * s->h * s->w) * (double)(s->r * s->s * s->f) * 4.0;
+    const double unf = (2.0 * tbytes_unf + (double)(s->n * s->h * s->w * s->c) * es +
+                        (double)(s->n * OH * OW * s->f) * es) / (23.0 * sms) + 8000.0;
+    g_last_fused_cost = best;
+    g_last_unfused_cost = unf;
     return true;
 }
 
@@ -315,26 +402,35 @@ struct PlanKey {
     int64_t v[12];
     bool operator<(const PlanKey &o) const { return std::lexicographical_compare(v, v + 12, o.v, o.v + 12); }
 };
+struct PlanEntry {
+    bool ok;
+    FusedArgs args;
+    double fused_cost, unfused_cost;
+};
 static std::mutex g_plan_mu;
-static std::map<PlanKey, std::pair<bool, FusedArgs>> g_plan_cache;
+static std::map<PlanKey, PlanEntry> g_plan_cache;
 
-static bool plan_fused(const ollie_conv_shape *s, bool tf32, int transposed, FusedArgs *out, int64_t OH, int64_t OW) {
+static const PlanEntry &plan_entry(const ollie_conv_shape *s, bool tf32, int transposed, int64_t OH, int64_t OW) {
     PlanKey k{{s->n, s->c, s->h, s->w, s->f, s->r * 65536 + s->s, s->pad, s->stride * 65536 + s->dilation,
-               (int64_t)tf32 * 2 + transposed, num_sms(), g_force_mt * 1000 + g_force_fs, g_force_res}};
+               (int64_t)tf32 * 2 + transposed + 4 * (int64_t)s->output_padding, num_sms(),
+               g_force_mt * 1000 + g_force_fs, g_force_res}};
     {
         std::lock_guard<std::mutex> g(g_plan_mu);
         auto it = g_plan_cache.find(k);
-        if (it != g_plan_cache.end()) {
-            if (it->second.first) *out = it->second.second;
-            return it->second.first;
-        }
+        if (it != g_plan_cache.end()) return it->second;
     }
-    FusedArgs a{};
-    const bool okp = plan_fused_search(s, tf32, transposed, &a, OH, OW);
+    PlanEntry e{};
+    e.ok = plan_fused_search(s, tf32, transposed, &e.args, OH, OW);
+    e.fused_cost = g_last_fused_cost;
+    e.unfused_cost = g_last_unfused_cost;
     std::lock_guard<std::mutex> g(g_plan_mu);
-    g_plan_cache[k] = {okp, a};
-    if (okp) *out = a;
-    return okp;
+    return g_plan_cache.emplace(k, e).first->second;   // std::map references stay valid
+}
+
+static bool plan_fused(const ollie_conv_shape *s, bool tf32, int transposed, FusedArgs *out, int64_t OH, int64_t OW) {
+    const PlanEntry &e = plan_entry(s, tf32, transposed, OH, OW);
+    if (e.ok) *out = e.args;
+    return e.ok;
 }
 
 static int fused_grid(const FusedArgs &a) {
@@ -348,14 +444,32 @@ static size_t fused_smem_bytes(const FusedArgs &a) {
     return 1024 + (size_t)a.na * a.a_stage_bytes + nbst * a.b_stage_bytes + 1024;
 }
 
+static bool out_hw(const ollie_conv_shape *s, int transposed, int64_t *OH, int64_t *OW) {
+    if (!transposed) {
+        *OH = (s->h + 2 * s->pad - (int64_t)s->dilation * (s->r - 1) - 1) / s->stride + 1;
+        *OW = (s->w + 2 * s->pad - (int64_t)s->dilation * (s->s - 1) - 1) / s->stride + 1;
+    } else {
+        *OH = (s->h - 1) * s->stride - 2 * (int64_t)s->pad + (int64_t)s->dilation * (s->r - 1) + s->output_padding + 1;
+        *OW = (s->w - 1) * s->stride - 2 * (int64_t)s->pad + (int64_t)s->dilation * (s->s - 1) + s->output_padding + 1;
+    }
+    return *OH > 0 && *OW > 0;
+}
+
+// Fused kernel can run this layer (explicit OLLIE_PLAN_FUSED).
 static bool fused_supported(const ollie_conv_shape *s, bool tf32, int transposed) {
     int64_t OH, OW;
-    if (transposed || s->stride != 1) return false;
-    OH = (s->h + 2 * s->pad - (int64_t)s->dilation * (s->r - 1) - 1) / s->stride + 1;
-    OW = (s->w + 2 * s->pad - (int64_t)s->dilation * (s->s - 1) - 1) / s->stride + 1;
-    if (OH <= 0 || OW <= 0) return false;
-    FusedArgs a;
-    return plan_fused(s, tf32, transposed, &a, OH, OW);
+    if (!out_hw(s, transposed, &OH, &OW)) return false;
+    return plan_entry(s, tf32, transposed, OH, OW).ok;
+}
+
+// OLLIE_PLAN_AUTO picks the fused kernel when it can run the layer and its cost estimate beats
+// the unfused GEMM + OffsetAdd estimate (small-F, many-tap layers such as FSRCNN's 9x9 deconv
+// keep the literal merged-GEMM form, where N = r*s*f stays wide).
+static bool fused_preferred(const ollie_conv_shape *s, bool tf32, int transposed) {
+    int64_t OH, OW;
+    if (!out_hw(s, transposed, &OH, &OW)) return false;
+    const PlanEntry &e = plan_entry(s, tf32, transposed, OH, OW);
+    return e.ok && e.fused_cost <= e.unfused_cost;
 }
 
 template <bool TF32>
@@ -374,7 +488,6 @@ static ollie_status launch_fused_t(const CUtensorMap &tx, const CUtensorMap &tw,
 }
 
 static long long *g_fc_trace = nullptr;   // debug timeline buffer (ollie_debug_set_trace), off by default
-static int g_fc_debug_flags = 0;          // debug: skip loads (ollie_debug_set_flags), 0 in production
 
 static ollie_status run_fused(const ollie_conv_shape *s, bool tf32, int transposed, const void *x, const void *wp,
                               void *y, int64_t OH, int64_t OW, cudaStream_t stream) {
@@ -382,7 +495,6 @@ static ollie_status run_fused(const ollie_conv_shape *s, bool tf32, int transpos
     if (!plan_fused(s, tf32, transposed, &a, OH, OW)) return fail(OLLIE_E_UNSUPPORTED, "no fused plan for this shape");
     a.y = y;
     a.trace = g_fc_trace;
-    a.debug_flags = g_fc_debug_flags;
     PFN_encodeTiled enc = get_encode();
     if (!enc) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
     const int es = tf32 ? 4 : 2, CI = 16 / es;
@@ -538,7 +650,7 @@ static bool is_identity_offset_add(const ollie_conv_shape *s, int transposed) {
 static int resolve_plan(const ollie_conv_shape *s, ollie_dtype dtype, int plan, int transposed) {
     if (plan == OLLIE_PLAN_FUSED || plan == OLLIE_PLAN_UNFUSED) return plan;
     if (is_identity_offset_add(s, transposed)) return OLLIE_PLAN_UNFUSED;
-    return fused_supported(s, dtype == OLLIE_TF32, transposed) ? OLLIE_PLAN_FUSED : OLLIE_PLAN_UNFUSED;
+    return fused_preferred(s, dtype == OLLIE_TF32, transposed) ? OLLIE_PLAN_FUSED : OLLIE_PLAN_UNFUSED;
 }
 
 extern "C" size_t ollie_workspace_bytes(const ollie_conv_shape *s, ollie_dtype dtype, int plan, int transposed) {
@@ -995,9 +1107,9 @@ extern "C" ollie_status ollie_plan_describe(const ollie_conv_shape *s, ollie_dty
         if (!plan_fused(s, tf32, transposed, &a, OH, OW)) return fail(OLLIE_E_UNSUPPORTED, "no fused plan");
         snprintf(buf, len,
                  "fused XB=%d Yb=%d Xb=%d Yp=%d MT=%d FS=%d f_slices=%d resident=%d nbuf=%d na=%d nb=%d BK=%d "
-                 "kchunks=%d tiles=%d grid=%d smem=%zu",
+                 "kchunks=%d tiles=%d grid=%d smem=%zu classes=%d taps=%d",
                  a.XB, a.Yb, a.Xb, a.Yp, a.MT, a.FS, a.f_slices, a.resident, a.nbuf, a.na, a.nb, a.BK, a.kchunks,
-                 a.num_tiles, fused_grid(a), fused_smem_bytes(a));
+                 a.num_tiles, fused_grid(a), fused_smem_bytes(a), a.nclass, a.max_taps);
     } else if (is_identity_offset_add(s, transposed)) {
         snprintf(buf, len, "unfused-identity gemm BN=%d (OffsetAdd eliminated)", choose_bn(s->r * s->s * s->f));
     } else {
@@ -1010,7 +1122,6 @@ extern "C" ollie_status ollie_plan_describe(const ollie_conv_shape *s, ollie_dty
 // Debug hook (not part of include/ollie.h): route the fused kernel's per-CTA timestamps into a
 // caller-owned device buffer of >= 16 * grid int64 (nullptr switches tracing off).
 extern "C" void ollie_debug_set_trace(void *dev_buf) { g_fc_trace = reinterpret_cast<long long *>(dev_buf); }
-extern "C" void ollie_debug_set_flags(int flags) { g_fc_debug_flags = flags; }
 // Debug hook (not part of include/ollie.h): force fused-plan parameters for sweeps
 // (mt / fs <= 0 and resident < 0 mean "auto").
 extern "C" void ollie_debug_force_plan(int mt, int fs, int resident) {

@@ -6,9 +6,9 @@ import ollie_synth as syn
 from paper_2208_02025_b200 import ollie as O
 from paper_2208_02025_b200.layers import DerivedConv
 cfg = sys.argv[1]
-flags = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+flags = 0
 plan = int(sys.argv[3]) if len(sys.argv) > 3 else 0
-O._lib.ollie_debug_set_flags(flags)
+
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for li, lay in enumerate(syn.CONFIGS[cfg]):
     x, w = syn.layer_inputs(lay, 1)

@@ -13,7 +13,7 @@ from paper_2208_02025_b200.layers import DerivedConv
 cfg, li = sys.argv[1], int(sys.argv[2])
 noflush = "noflush" in sys.argv[3:]
 dbg = int([a for a in sys.argv[3:] if a.startswith("flags=")][0][6:]) if any(a.startswith("flags=") for a in sys.argv[3:]) else 0
-O._lib.ollie_debug_set_flags(dbg)
+
 lay = syn.CONFIGS[cfg][li]
 x, w = syn.layer_inputs(lay, 1)
 conv = DerivedConv.from_layer(lay).prepare(w.cuda())
