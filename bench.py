@@ -11,7 +11,8 @@ batch 16 and at batch 1, bf16.  Metric: useful TFLOP/s
 (2*n*OH*OW*f*c*r*s per layer) of the whole step; higher is better.
 
 Timing: W untimed warm-up steps; then exactly K steps, each preceded by an
-L2 flush (a 2x L2-size write, outside the per-step events), each captured as one CUDA
+L2 flush (a 2x L2-size write, then a read of it that retires the dirty lines; both outside
+the per-step events), each captured as one CUDA
 graph replay bracketed by CUDA events on the launching stream; a barrier +
 synchronize on both sides of the K steps; max over ranks.  N > 1 (torchrun, NCCL):
 every rank runs its own batch (weak scaling); `--allgather` adds the a9 output
@@ -259,15 +260,24 @@ def gpu_main(args):
     flops = sum(l.useful_flops for l in layers)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(max(2 * l2, 64 << 20), dtype=torch.uint8, device=dev)
+    flush_sink = torch.empty((), dtype=torch.int64, device=dev)
+
+    def l2_flush(k):
+        # write a buffer larger than L2 (evicts everything), then read it back so the dirty lines
+        # are written back to HBM here -- outside the timed events -- and not inside the next kernel
+        flush.fill_(k & 0xFF)
+        torch.sum(flush.view(torch.int64), dim=0, out=flush_sink)
     stream = torch.cuda.Stream(device=dev)
 
     def step():
         stack(inputs, stream=stream.cuda_stream)
 
+    from paper_2208_02025_b200 import parallel as par
+
     def gather():
         if gather_bufs is not None:
-            for o, g in zip(out_dev, gather_bufs):
-                dist.all_gather_into_tensor(g, o)
+            for o in out_dev:
+                par.gather_batch(o, world * o.shape[0])
 
     # warm-up + graph capture of one step (the per-layer launches of the derived program)
     with torch.cuda.stream(stream):
@@ -304,7 +314,7 @@ def gpu_main(args):
         t_wall0 = time.perf_counter()
         with torch.cuda.stream(stream):
             for k in range(args.steps):
-                flush.fill_(k & 0xFF)
+                l2_flush(k)
                 starts[k].record(stream)
                 replay()
                 gather()
@@ -356,7 +366,7 @@ def gpu_main(args):
                 src = x if chained else inputs[li]
                 lay = sl.padded
                 if sl.pad_eop is not None:
-                    flush.fill_(rep & 0xFF)
+                    l2_flush(rep)
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
                     O.eop_eval(sl.pad_eop, [src], sl.x_pad, stream.cuda_stream)
@@ -365,7 +375,7 @@ def gpu_main(args):
                     per.setdefault("eop_channel_pad", []).append((e0, e1, b, 0, "hbm"))
                     src = sl.x_pad
                 conv = sl.conv
-                flush.fill_(rep & 0xFF)
+                l2_flush(rep)
                 if conv.ws_bytes:      # unfused: time the two kernels of the derived program separately
                     M, N, K = lay.gemm_mnk
                     ldT = -(-N // 4) * 4
@@ -428,7 +438,7 @@ def gpu_main(args):
     # ---------------- cuDNN on the same box, same inputs, same flush + event method
     cudnn = None
     if not args.no_cudnn and rank == 0:
-        cudnn = _time_cudnn(layers, chained, xs_host, ws_dev, dev, flush, args.steps, stream)
+        cudnn = _time_cudnn(layers, chained, xs_host, ws_dev, dev, l2_flush, args.steps, stream)
 
     result = None
     if rank == 0:
@@ -448,7 +458,7 @@ def gpu_main(args):
             "dtype": layers[0].dtype, "data": "synthetic (seeded, ollie_synth)",
             "config": {"workload": CONFIG_TEXT.get(cfg, cfg), "name": cfg,
                        "layers": [l.name for l in layers], "plan": args.plan,
-                       "l2": "flushed before every step (2x L2 write outside the per-step events)",
+                       "l2": "flushed before every step: 2x-L2 write, then read back (retires dirty lines), both outside the per-step events",
                        "timing": "CUDA graph replay per step, CUDA events on the launching stream, max over ranks",
                        "allgather": bool(gather_bufs is not None),
                        "parallelism": f"batch-sharded x{world}" if world > 1 else "1 GPU"},
@@ -483,7 +493,7 @@ def _traffic_from_profiles(cfg, kernel):
         return None
 
 
-def _time_cudnn(layers, chained, xs_host, ws_dev, dev, flush, steps, stream):
+def _time_cudnn(layers, chained, xs_host, ws_dev, dev, l2_flush, steps, stream):
     import torch
     import torch.nn.functional as F
     torch.backends.cudnn.benchmark = True
@@ -514,7 +524,7 @@ def _time_cudnn(layers, chained, xs_host, ws_dev, dev, flush, steps, stream):
     tot = []
     with torch.cuda.stream(stream):
         for k in range(steps):
-            flush.fill_(k & 0xFF)
+            l2_flush(k)
             evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(layers) + 1)]
             evs[0].record(stream)
             x = xs[0]

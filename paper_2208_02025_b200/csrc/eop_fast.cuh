@@ -1,0 +1,169 @@
+// eop_fast.cuh -- fast paths of the eOperator evaluator for PURE-INDEXING AFFINE eOperators
+// (one input, no summation, body = the access, every index term a plain iterator):
+// layout transforms (DLT), channel pads, reshapes.  Such an eOp is
+//     out[o] = in[B + sum_d s_d * o_d]   if every input index b_k + sum_d a_kd * o_d is inside
+//                                         the tensor, else 0 (pad band)
+// over the dense output coordinates o.  HBM-bound: bytes = |in| + |out|.
+//  - gather kernel: one thread per 8 consecutive elements of an output row (innermost output
+//    dimension), 32-bit index math after collapsing output dims that merge linearly, bounds tests
+//    only on input dims that have a pad band, 16-byte stores; reads are coalesced across the warp
+//    when the innermost output dimension has input stride 1 (pads, reshapes).
+//  - transpose kernel: when the innermost output dimension is strided in the input, a 32x32 tile
+//    of (input-contiguous dim, output-contiguous dim) goes through shared memory so both the
+//    reads and the writes are coalesced (NCHW <-> NHWC).
+#pragma once
+#include <type_traits>
+#include "sm100_ptx.cuh"
+
+namespace ollie {
+
+constexpr int FAST_MAX_D = 6;
+
+struct AffineEop {
+    const void *in;
+    void *out;
+    int32_t in_bf16, out_bf16;
+    int32_t nd_out, nd_in;
+    int32_t w[FAST_MAX_D];                  // output widths (dense, traversal order)
+    int32_t s[FAST_MAX_D];                  // input element stride per output dim
+    int32_t a[FAST_MAX_D][FAST_MAX_D];      // a[k][d]: coefficient of output dim d in input index k
+    int32_t b[FAST_MAX_D];                  // input index k at o = 0
+    int32_t shape[FAST_MAX_D];              // input extents
+    int32_t base;                           // input linear offset at o = 0 (may be negative: pad band)
+    int32_t rows;                           // product of all output widths but the last
+    int32_t inner;                          // last output width
+    // transpose kernel: output dim dt (input stride 1) and the innermost output dim
+    int32_t dt;
+    int32_t chk;                            // bit k: input dim k has a pad band (needs a bounds test)
+};
+
+__device__ __forceinline__ float fast_ld(const AffineEop &e, int32_t off) {
+    if (e.in_bf16) return bf16_bits_to_float(__ldg(reinterpret_cast<const uint16_t *>(e.in) + off));
+    return __ldg(reinterpret_cast<const float *>(e.in) + off);
+}
+__device__ __forceinline__ void fast_st(const AffineEop &e, int64_t off, float v) {
+    if (e.out_bf16) reinterpret_cast<uint16_t *>(e.out)[off] = float_to_bf16_rne(v);
+    else reinterpret_cast<float *>(e.out)[off] = v;
+}
+
+__device__ __forceinline__ int32_t fdiv32(int32_t a, int32_t b) {   // floor(a / b), b != 0
+    int32_t q = a / b;
+    return (q * b != a && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+__device__ __forceinline__ int32_t cdiv32(int32_t a, int32_t b) { return -fdiv32(-a, b); }   // ceil(a / b)
+
+// Raw element move (dtypes equal): bits are copied, zero is the all-zero pattern.
+template <typename E>
+__device__ __forceinline__ E raw_ld(const void *p, int32_t off) { return __ldg(reinterpret_cast<const E *>(p) + off); }
+
+// VEC consecutive inner elements per thread, 32-bit index math (the host guarantees every
+// extent and offset fits), outer coordinates decoded once per thread.  Input dims with a pad
+// band (bit k of `chk`) are affine in the inner coordinate j, so each thread turns them into one
+// valid interval [jlo, jhi) before touching memory.  E = element type when in/out dtypes match
+// (raw bit copy); E = void converts through fp32.
+template <int VEC, typename E>
+__global__ void __launch_bounds__(256) eop_affine_gather_kernel(const __grid_constant__ AffineEop e) {
+    const int32_t vec_per_row = (e.inner + VEC - 1) / VEC;
+    const int32_t total = e.rows * vec_per_row;
+    const int dl = e.nd_out - 1;
+    for (int32_t it = blockIdx.x * blockDim.x + threadIdx.x; it < total; it += gridDim.x * blockDim.x) {
+        const int32_t row0 = it / vec_per_row;
+        const int32_t j0 = (it - row0 * vec_per_row) * VEC;
+        int32_t row = row0;
+        int32_t off = e.base;
+        int32_t idx[FAST_MAX_D];
+#pragma unroll
+        for (int k = 0; k < FAST_MAX_D; ++k) idx[k] = e.b[k];
+        for (int d = e.nd_out - 2; d >= 0; --d) {
+            const int32_t q = row / e.w[d];
+            const int32_t od = row - q * e.w[d];
+            row = q;
+            off += e.s[d] * od;
+#pragma unroll
+            for (int k = 0; k < FAST_MAX_D; ++k) idx[k] += e.a[k][d] * od;
+        }
+        int32_t jlo = 0, jhi = e.inner;
+        if (e.chk) {
+#pragma unroll
+            for (int k = 0; k < FAST_MAX_D; ++k)
+                if (e.chk & (1 << k)) {
+                    const int32_t c = e.a[k][dl], b = idx[k], n = e.shape[k];
+                    if (c == 0) {
+                        if (b < 0 || b >= n) jhi = 0;
+                    } else if (c > 0) {
+                        jlo = max(jlo, cdiv32(-b, c));
+                        jhi = min(jhi, fdiv32(n - 1 - b, c) + 1);
+                    } else {
+                        jlo = max(jlo, cdiv32(n - 1 - b, c));
+                        jhi = min(jhi, fdiv32(-b, c) + 1);
+                    }
+                }
+        }
+        const int32_t sl = e.s[dl];
+        const int64_t obase = (int64_t)row0 * e.inner + j0;
+        if constexpr (!std::is_void<E>::value) {
+            E v[VEC];
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) {
+                const int32_t j = j0 + q;
+                v[q] = (j >= jlo && j < jhi) ? raw_ld<E>(e.in, off + sl * j) : E(0);
+            }
+            E *o = reinterpret_cast<E *>(e.out) + obase;
+            if (j0 + VEC <= e.inner && ((obase * (int64_t)sizeof(E)) & 15) == 0 && VEC * sizeof(E) == 16) {
+                uint4 pk;
+                memcpy(&pk, v, 16);
+                *reinterpret_cast<uint4 *>(o) = pk;
+            } else {
+#pragma unroll
+                for (int q = 0; q < VEC; ++q)
+                    if (j0 + q < e.inner) o[q] = v[q];
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) {
+                const int32_t j = j0 + q;
+                if (j < e.inner) fast_st(e, obase + q, (j >= jlo && j < jhi) ? fast_ld(e, off + sl * j) : 0.f);
+            }
+        }
+    }
+}
+
+// Tiled transpose: the output's innermost dim (dl) is strided in the input and dim dt has input
+// stride 1.  Block = one 32 x 32 tile of (dt, dl) for one combination of the other dims.  No pad
+// band (checked on the host).  grid.x = tiles over (dt, dl), grid.y = other-dims combinations.
+__global__ void __launch_bounds__(256) eop_affine_transpose_kernel(const __grid_constant__ AffineEop e) {
+    __shared__ float tile[32][33];
+    const int dl = e.nd_out - 1, dt = e.dt;
+    const int32_t nt_l = (e.w[dl] + 31) / 32;
+    const int32_t tl = (int32_t)(blockIdx.x % nt_l), tt = (int32_t)(blockIdx.x / nt_l);
+    // decode the other output dims from blockIdx.y (row-major over dims != dt, dl)
+    int32_t rest = (int32_t)blockIdx.y;
+    int32_t off = e.base;
+    int64_t obase = 0, ostride = 1;
+    int32_t ostr[FAST_MAX_D];
+    for (int d = e.nd_out - 1; d >= 0; --d) {
+        ostr[d] = (int32_t)ostride;
+        ostride *= e.w[d];
+    }
+    for (int d = e.nd_out - 1; d >= 0; --d) {
+        if (d == dl || d == dt) continue;
+        const int32_t od = rest % e.w[d];
+        rest /= e.w[d];
+        off += e.s[d] * od;
+        obase += (int64_t)ostr[d] * od;
+    }
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    // read: coalesced along dt (input stride 1)
+    for (int r = ty; r < 32; r += 8) {
+        const int32_t ol = tl * 32 + r, ot = tt * 32 + tx;
+        if (ol < e.w[dl] && ot < e.w[dt]) tile[r][tx] = fast_ld(e, off + e.s[dl] * ol + ot);
+    }
+    __syncthreads();
+    // write: coalesced along dl (output stride 1)
+    for (int r = ty; r < 32; r += 8) {
+        const int32_t ot = tt * 32 + r, ol = tl * 32 + tx;
+        if (ol < e.w[dl] && ot < e.w[dt]) fast_st(e, obase + (int64_t)ostr[dt] * ot + ol, tile[tx][r]);
+    }
+}
+
+}  // namespace ollie

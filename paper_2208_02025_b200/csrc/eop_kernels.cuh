@@ -76,25 +76,45 @@ __device__ __forceinline__ void accum_tap(float (&acc)[VEC], const float *src) {
     }
 }
 
-// a3: OffsetAdd.  Taps are issued in (i, j) order; out-of-image taps are skipped.
-template <int VEC, bool kOutBF16>
+// a3: OffsetAdd.  Taps are issued in (i, j) order; out-of-image taps are skipped.  Index
+// decoding is 32-bit (IDX = int32_t) whenever the host proves every index fits.
+template <int VEC, bool kOutBF16, typename IDX>
 __global__ void __launch_bounds__(256) offset_add_kernel(OffsetAddArgs a) {
-    const int64_t fv_per_px = a.f / VEC;
-    const int64_t nt_rsf = a.r * a.s * a.f;
-    (void)nt_rsf;
-    for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < a.items;
-         it += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t fv = it % fv_per_px;
-        const int64_t px = it / fv_per_px;
-        const int64_t ow = px % a.ow;
-        const int64_t t = px / a.ow;
-        const int64_t oh = t % a.oh;
-        const int64_t b = t / a.oh;
+    const IDX fv_per_px = (IDX)(a.f / VEC);
+    const IDX OW = (IDX)a.ow, OHh = (IDX)a.oh;
+    for (IDX it = (IDX)(blockIdx.x * blockDim.x + threadIdx.x); it < (IDX)a.items; it += (IDX)(gridDim.x * blockDim.x)) {
+        const IDX px = it / fv_per_px;
+        const int64_t fv = it - px * fv_per_px;
+        const IDX t = px / OW;
+        const int64_t ow = px - t * OW;
+        const IDX b_ = t / OHh;
+        const int64_t oh = t - b_ * OHh;
+        const int64_t b = b_;
         float acc[VEC];
 #pragma unroll
         for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
         const int64_t h0 = oh * a.stride - a.pad, w0 = ow * a.stride - a.pad;
         const float *Tb = a.T + (b * a.h) * a.w * a.ldT + fv * VEC;
+        if (VEC == 4 && a.r == 3 && a.s == 3) {
+            // 3x3: issue all nine (predicated) 16-byte loads before summing, in (i, j) order
+            float4 tv[9];
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    const int64_t t1 = h0 + i * a.dil, t2 = w0 + j * a.dil;
+                    const bool in = t1 >= 0 && t1 < a.h && t2 >= 0 && t2 < a.w;
+                    tv[i * 3 + j] = in ? ld_stream_f4(Tb + (t1 * a.w + t2) * a.ldT + (i * 3 + j) * a.f)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+            for (int q = 0; q < 9; ++q) {
+                acc[0] += tv[q].x;
+                if constexpr (VEC == 4) { acc[1] += tv[q].y; acc[2] += tv[q].z; acc[3] += tv[q].w; }
+            }
+            store_y<VEC, kOutBF16>(a.y, px * a.f + fv * VEC, acc);
+            continue;
+        }
         for (int64_t i = 0; i < a.r; ++i) {
             const int64_t t1 = h0 + i * a.dil;
             if (t1 < 0 || t1 >= a.h) continue;
@@ -112,18 +132,19 @@ __global__ void __launch_bounds__(256) offset_add_kernel(OffsetAddArgs a) {
 
 // a4: ConvTranspose selective addition (dilation 1).  Only the taps i == (oh+p) mod st
 // (mod st) are visited: each output reads exactly the Matmul outputs that land on it.
-template <int VEC, bool kOutBF16>
+template <int VEC, bool kOutBF16, typename IDX>
 __global__ void __launch_bounds__(256) selective_add_kernel(OffsetAddArgs a) {
-    const int64_t fv_per_px = a.f / VEC;
+    const IDX fv_per_px = (IDX)(a.f / VEC);
+    const IDX OW = (IDX)a.ow, OHh = (IDX)a.oh;
     const int64_t st = a.stride;
-    for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < a.items;
-         it += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t fv = it % fv_per_px;
-        const int64_t px = it / fv_per_px;
-        const int64_t ow = px % a.ow;
-        const int64_t t = px / a.ow;
-        const int64_t oh = t % a.oh;
-        const int64_t b = t / a.oh;
+    for (IDX it = (IDX)(blockIdx.x * blockDim.x + threadIdx.x); it < (IDX)a.items; it += (IDX)(gridDim.x * blockDim.x)) {
+        const IDX px = it / fv_per_px;
+        const int64_t fv = it - px * fv_per_px;
+        const IDX t = px / OW;
+        const int64_t ow = px - t * OW;
+        const IDX b_ = t / OHh;
+        const int64_t oh = t - b_ * OHh;
+        const int64_t b = b_;
         float acc[VEC];
 #pragma unroll
         for (int v = 0; v < VEC; ++v) acc[v] = 0.f;

@@ -17,6 +17,7 @@
 
 #include "../../include/ollie.h"
 #include "eop_eval.cuh"
+#include "eop_fast.cuh"
 #include "eop_kernels.cuh"
 #include "fused_conv.cuh"
 #include "merged_gemm.cuh"
@@ -606,23 +607,21 @@ static ollie_status run_offset_add(const ollie_conv_shape *s, int transposed, co
     a.items = s->n * OH * OW * (s->f / VEC);
     const int64_t blocks = std::min<int64_t>(ceil_div(a.items, 256), (int64_t)num_sms() * 16);
     const unsigned g = (unsigned)std::max<int64_t>(blocks, 1);
+    // 32-bit index decoding when the item count and the grid stride fit comfortably
+    const bool i32 = a.items + (int64_t)g * 256 < (1ll << 31);
+#define OA_LAUNCH(K, V, B)                                                                 \
+    do {                                                                                   \
+        if (i32) K<V, B, int32_t><<<g, 256, 0, stream>>>(a);                               \
+        else K<V, B, int64_t><<<g, 256, 0, stream>>>(a);                                   \
+    } while (0)
     if (!transposed) {
-        if (vec4) {
-            if (out_bf16) offset_add_kernel<4, true><<<g, 256, 0, stream>>>(a);
-            else offset_add_kernel<4, false><<<g, 256, 0, stream>>>(a);
-        } else {
-            if (out_bf16) offset_add_kernel<1, true><<<g, 256, 0, stream>>>(a);
-            else offset_add_kernel<1, false><<<g, 256, 0, stream>>>(a);
-        }
+        if (vec4) { if (out_bf16) OA_LAUNCH(offset_add_kernel, 4, true); else OA_LAUNCH(offset_add_kernel, 4, false); }
+        else { if (out_bf16) OA_LAUNCH(offset_add_kernel, 1, true); else OA_LAUNCH(offset_add_kernel, 1, false); }
     } else {
-        if (vec4) {
-            if (out_bf16) selective_add_kernel<4, true><<<g, 256, 0, stream>>>(a);
-            else selective_add_kernel<4, false><<<g, 256, 0, stream>>>(a);
-        } else {
-            if (out_bf16) selective_add_kernel<1, true><<<g, 256, 0, stream>>>(a);
-            else selective_add_kernel<1, false><<<g, 256, 0, stream>>>(a);
-        }
+        if (vec4) { if (out_bf16) OA_LAUNCH(selective_add_kernel, 4, true); else OA_LAUNCH(selective_add_kernel, 4, false); }
+        else { if (out_bf16) OA_LAUNCH(selective_add_kernel, 1, true); else OA_LAUNCH(selective_add_kernel, 1, false); }
     }
+#undef OA_LAUNCH
     CHECK_LAUNCH();
     return OLLIE_OK;
 }
@@ -1057,6 +1056,94 @@ int64_t tensor_bytes(const ollie_tensor &t) {
 
 }  // namespace
 
+// Fast-path selection for pure-indexing affine eOperators (eop_fast.cuh).  Returns 0 (generic
+// evaluator), 1 (affine gather) or 2 (tiled transpose).
+static int affine_fast_plan(const ollie_eop *e, const void *in, void *out, AffineEop *fe) {
+    if (!is_pure_indexing(e) || e->n_in != 1) return 0;
+    const ollie_scope &s = e->scope[0];
+    const ollie_access &ac = s.acc[0];
+    const ollie_tensor &t = e->in[ac.tensor];
+    if (s.n_trav > FAST_MAX_D || t.ndim > FAST_MAX_D || s.n_trav < 1) return 0;
+    memset(fe, 0, sizeof *fe);
+    fe->in = in;
+    fe->out = out;
+    fe->in_bf16 = t.dtype == OLLIE_BF16;
+    fe->out_bf16 = e->out_dtype == OLLIE_BF16;
+    fe->nd_out = s.n_trav;
+    fe->nd_in = t.ndim;
+    int64_t in_elems = 1, out_elems = 1;
+    for (int k = 0; k < t.ndim; ++k) in_elems *= t.shape[k];
+    for (int d = 0; d < s.n_trav; ++d) out_elems *= s.trav_hi[d] - s.trav_lo[d];
+    if (in_elems >= (1ll << 31) || out_elems >= (1ll << 31)) return 0;
+    int64_t stride[FAST_MAX_D];
+    stride[t.ndim - 1] = 1;
+    for (int k = t.ndim - 2; k >= 0; --k) stride[k] = stride[k + 1] * t.shape[k + 1];
+    int64_t base = 0, sd[FAST_MAX_D] = {0};
+    for (int k = 0; k < t.ndim; ++k) {
+        const ollie_index &ix = ac.idx[k];
+        int64_t b = ix.c0;
+        for (int q = 0; q < ix.nterms; ++q) {
+            const ollie_term &tm = ix.term[q];
+            if (tm.kind != OLLIE_ATOM_ITER || tm.iter >= s.n_trav) return 0;
+            fe->a[k][tm.iter] += (int32_t)tm.coef;
+            b += tm.coef * s.trav_lo[tm.iter];
+        }
+        if (b > INT32_MAX || b < INT32_MIN) return 0;
+        fe->b[k] = (int32_t)b;
+        fe->shape[k] = (int32_t)t.shape[k];
+        base += stride[k] * b;
+    }
+    for (int d = 0; d < s.n_trav; ++d) {
+        fe->w[d] = (int32_t)(s.trav_hi[d] - s.trav_lo[d]);
+        for (int k = 0; k < t.ndim; ++k) sd[d] += stride[k] * fe->a[k][d];
+        if (sd[d] > INT32_MAX || sd[d] < INT32_MIN) return 0;
+        fe->s[d] = (int32_t)sd[d];
+    }
+    if (base > INT32_MAX || base < INT32_MIN) return 0;
+    fe->base = (int32_t)base;
+    {   // input dims with a pad band need a bounds test; every other read is proven in range
+        int64_t lo[EOPD_MAX_ITERS], hi[EOPD_MAX_ITERS];
+        for (int d = 0; d < s.n_trav; ++d) { lo[d] = s.trav_lo[d]; hi[d] = s.trav_hi[d]; }
+        for (int k = 0; k < t.ndim; ++k) {
+            Interval iv = index_interval(ac.idx[k], lo, hi);
+            if (iv.lo < 0 || iv.hi >= t.shape[k]) fe->chk |= 1 << k;
+        }
+    }
+    // collapse adjacent output dims (d, d+1) that merge linearly: o' = o_d * w_{d+1} + o_{d+1}
+    // keeps both the input offset and every CHECKED input index affine
+    int nd = s.n_trav;
+    for (int d = nd - 3; d >= 0; --d) {       // never merge into the innermost dim
+        bool ok = (int64_t)fe->s[d] == (int64_t)fe->s[d + 1] * fe->w[d + 1];
+        for (int k = 0; k < t.ndim && ok; ++k)
+            if (fe->chk & (1 << k)) ok = (int64_t)fe->a[k][d] == (int64_t)fe->a[k][d + 1] * fe->w[d + 1];
+        if (!ok) continue;
+        fe->w[d] *= fe->w[d + 1];
+        fe->s[d] = fe->s[d + 1];
+        for (int k = 0; k < t.ndim; ++k) fe->a[k][d] = fe->a[k][d + 1];
+        for (int e2 = d + 1; e2 < nd - 1; ++e2) {
+            fe->w[e2] = fe->w[e2 + 1];
+            fe->s[e2] = fe->s[e2 + 1];
+            for (int k = 0; k < t.ndim; ++k) fe->a[k][e2] = fe->a[k][e2 + 1];
+        }
+        --nd;
+    }
+    fe->nd_out = nd;
+    fe->inner = fe->w[nd - 1];
+    fe->rows = (int32_t)(out_elems / fe->inner);
+    if ((int64_t)fe->rows * ((fe->inner + 7) / 8) >= (1ll << 31)) return 0;
+    // transpose path: innermost output dim strided in the input, another output dim with input
+    // stride 1, and no pad-band reads (every index interval inside the tensor)
+    if (fe->s[nd - 1] != 1 && fe->s[nd - 1] != 0 && nd >= 2) {
+        const bool inside = fe->chk == 0;
+        for (int d = 0; d < nd - 1 && inside; ++d)
+            if (fe->s[d] == 1 && out_elems / ((int64_t)fe->w[d] * fe->inner) < 65536) {
+                fe->dt = d;
+                return 2;
+            }
+    }
+    return 1;
+}
+
 extern "C" ollie_status ollie_eop_analyze(const ollie_eop *eop, ollie_eop_info *info) {
     ollie_status st = validate_eop(eop);
     if (st != OLLIE_OK) return st;
@@ -1084,6 +1171,33 @@ extern "C" ollie_status ollie_eop_eval(const ollie_eop *eop, const void *const *
         if (inputs[0] == output) return ok();
         CUDA_TRY(cudaMemcpyAsync(output, inputs[0], (size_t)tensor_bytes(eop->in[0]), cudaMemcpyDeviceToDevice, s));
         return ok();
+    }
+    {
+        AffineEop fe;
+        int kind = affine_fast_plan(eop, inputs[0], output, &fe);
+        if (kind == 1) {
+            const int64_t vec_per_row = (fe.inner + 7) / 8;
+            const int64_t blocks = std::min<int64_t>(ceil_div((int64_t)fe.rows * vec_per_row, 256), (int64_t)num_sms() * 32);
+            const unsigned gb = (unsigned)std::max<int64_t>(blocks, 1);
+            if (fe.in_bf16 == fe.out_bf16) {
+                if (fe.in_bf16) eop_affine_gather_kernel<8, uint16_t><<<gb, 256, 0, s>>>(fe);
+                else eop_affine_gather_kernel<4, uint32_t><<<gb, 256, 0, s>>>(fe);
+            } else {
+                eop_affine_gather_kernel<8, void><<<gb, 256, 0, s>>>(fe);
+            }
+            CHECK_LAUNCH();
+            return ok();
+        }
+        if (kind == 2) {
+            int64_t others = 1;
+            for (int d = 0; d < fe.nd_out; ++d)
+                if (d != fe.dt && d != fe.nd_out - 1) others *= fe.w[d];
+            const int64_t tiles = ceil_div(fe.w[fe.nd_out - 1], 32) * ceil_div(fe.w[fe.dt], 32);
+            dim3 grid((unsigned)tiles, (unsigned)others);
+            eop_affine_transpose_kernel<<<grid, 256, 0, s>>>(fe);
+            CHECK_LAUNCH();
+            return ok();
+        }
     }
     EopDev dv;
     st = compile_eop(eop, inputs, output, &dv);

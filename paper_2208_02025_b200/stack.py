@@ -1,10 +1,17 @@
-"""A sequence of derived layers run through the C ABI, with the layout eOperators the
-path needs inserted automatically: when an activation row (c * sizeof(elem))
-is not a multiple of 16 bytes, a channel-pad eOperator widens it and the layer's weight
-is zero-padded along c at prepare time (a compile-time, weight-only expression,
-P:1445-1447) -- both through libollie kernels.  Chained stacks (FSRCNN, DCGAN) feed each
-output to the next layer; independent stacks (ResNet-18 stages) give every layer its
-own input."""
+"""A sequence of derived layers run through the C ABI, with the layout eOperators the path needs
+(TMA wants 16-byte activation rows).
+
+ - The network input, if its rows are narrower than 16 bytes (FSRCNN's c=1), goes through a
+   channel-pad layout eOperator (`eops.channel_pad`).
+ - Inside a chained stack, a layer whose output rows would be misaligned for the next layer
+   (FSRCNN's f=12) writes its output with zero-padded channels instead: its weight is padded
+   with zero output channels at prepare time, so the "channel-pad o OffsetAdd" eOperator pair
+   is evaluated inside the layer (fused pair) and no pad launch is needed.
+ - Weight padding is a weight-only expression, evaluated once at prepare ("compile") time
+    by the libollie eOperator kernel.
+Chained stacks (FSRCNN, DCGAN) feed each output to the next layer; independent stacks
+(ResNet-18 stages) give every layer its own input.
+"""
 from __future__ import annotations
 
 from dataclasses import replace
@@ -25,40 +32,48 @@ def padded_channels(c: int, dtype: str) -> int:
     return -(-c // q) * q
 
 
+def _pad_spec_3d(d0, d1, d2, p0, p1):
+    """[d0, d1, d2] -> [d0 + p0, d1 + p1, d2], zero in the new rows (pad band on dims 0, 1)."""
+    ix = lambda it: {"terms": [[1, it, "id", 1]], "const": 0}  # noqa: E731
+    return {"inputs": [{"shape": [d0, d1, d2], "pad": [[0, p0], [0, p1], [0, 0]]}],
+            "scopes": [{"trav": [[0, d0 + p0], [0, d1 + p1], [0, d2]], "sum": [],
+                        "access": [{"tensor": 0, "index": [ix(0), ix(1), ix(2)]}],
+                        "body": [["acc", 0]]}]}
+
+
 class StackLayer:
-    def __init__(self, layer, plan, device):
+    """One derived layer computing `fout` output channels from `cin` input channels, where
+    cin >= layer.c and fout >= layer.f carry zero padding."""
+
+    def __init__(self, layer, cin, fout, pad_input, plan, device):
         self.layer = layer
-        self.cp = padded_channels(layer.c, layer.dtype)
-        self.padded = replace(layer, c=self.cp)
+        self.cin, self.fout = cin, fout
+        self.padded = replace(layer, c=cin, f=fout)
         self.conv = DerivedConv.from_layer(self.padded, plan=plan, device=device)
         self.pad_eop = None
-        if self.cp != layer.c:
-            self.pad_eop = _o.make_eop(eops.channel_pad(layer.n, layer.h, layer.w, layer.c, self.cp),
+        if pad_input:
+            self.pad_eop = _o.make_eop(eops.channel_pad(layer.n, layer.h, layer.w, layer.c, cin),
                                        [_CODE[layer.dtype]], _CODE[layer.dtype])
-            self.x_pad = torch.empty(layer.n, layer.h, layer.w, self.cp, dtype=_TORCH[layer.dtype], device=device)
+            self.x_pad = torch.empty(layer.n, layer.h, layer.w, cin, dtype=_TORCH[layer.dtype], device=device)
         self.y = self.conv.new_output()
+
+    @property
+    def y_logical(self):
+        """The layer's output without the zero padding channels (a view)."""
+        return self.y[..., : self.layer.f]
 
     def prepare(self, w: torch.Tensor):
         """w in PyTorch layout ([f,c,r,s] conv, [c,f,r,s] convT), on the device."""
         lay = self.layer
-        if self.cp != lay.c:
+        if self.cin != lay.c or self.fout != lay.f:
             code = _CODE[lay.dtype]
-            if lay.transposed:     # [c, f, r, s] -> [cp, f, r, s]
-                spec = {"inputs": [{"shape": [lay.c, lay.f * lay.r * lay.s], "pad": [[0, self.cp - lay.c], [0, 0]]}],
-                        "scopes": [{"trav": [[0, self.cp], [0, lay.f * lay.r * lay.s]], "sum": [],
-                                    "access": [{"tensor": 0, "index": [{"terms": [[1, 0, "id", 1]], "const": 0},
-                                                                       {"terms": [[1, 1, "id", 1]], "const": 0}]}],
-                                    "body": [["acc", 0]]}]}
-                wp = torch.empty(self.cp, lay.f, lay.r, lay.s, dtype=w.dtype, device=w.device)
-            else:                  # [f, c, r, s] -> [f, cp, r, s]
-                spec = {"inputs": [{"shape": [lay.f, lay.c, lay.r * lay.s],
-                                    "pad": [[0, 0], [0, self.cp - lay.c], [0, 0]]}],
-                        "scopes": [{"trav": [[0, lay.f], [0, self.cp], [0, lay.r * lay.s]], "sum": [],
-                                    "access": [{"tensor": 0, "index": [{"terms": [[1, 0, "id", 1]], "const": 0},
-                                                                       {"terms": [[1, 1, "id", 1]], "const": 0},
-                                                                       {"terms": [[1, 2, "id", 1]], "const": 0}]}],
-                                    "body": [["acc", 0]]}]}
-                wp = torch.empty(lay.f, self.cp, lay.r, lay.s, dtype=w.dtype, device=w.device)
+            rs = lay.r * lay.s
+            if lay.transposed:     # [c, f, r, s] -> [cin, fout, r, s]
+                spec = _pad_spec_3d(lay.c, lay.f, rs, self.cin - lay.c, self.fout - lay.f)
+                wp = torch.empty(self.cin, self.fout, lay.r, lay.s, dtype=w.dtype, device=w.device)
+            else:                  # [f, c, r, s] -> [fout, cin, r, s]
+                spec = _pad_spec_3d(lay.f, lay.c, rs, self.fout - lay.f, self.cin - lay.c)
+                wp = torch.empty(self.fout, self.cin, lay.r, lay.s, dtype=w.dtype, device=w.device)
             _o.eop_eval(_o.make_eop(spec, [code], code), [w.contiguous()], wp)
             w = wp
         self.conv.prepare(w)
@@ -78,11 +93,22 @@ class StackLayer:
 
 class DerivedStack:
     def __init__(self, layers, chained: bool, plan=_o.PLAN_AUTO, device="cuda"):
-        self.layers = [StackLayer(l, plan, device) for l in layers]
         self.chained = chained
+        self.layers = []
         if chained:
             for a, b in zip(layers, layers[1:]):
                 assert (a.n, a.oh, a.ow, a.f) == (b.n, b.h, b.w, b.c), f"{a.name} -> {b.name} does not chain"
+        prev_fout = None
+        for k, l in enumerate(layers):
+            if chained and k > 0:
+                cin, pad_in = prev_fout, False
+            else:
+                cin = padded_channels(l.c, l.dtype)
+                pad_in = cin != l.c
+            last = (not chained) or k == len(layers) - 1
+            fout = l.f if last else padded_channels(l.f, l.dtype)
+            self.layers.append(StackLayer(l, cin, fout, pad_in, plan, device))
+            prev_fout = fout
 
     def prepare(self, weights):
         for sl, w in zip(self.layers, weights):
@@ -90,14 +116,15 @@ class DerivedStack:
         return self
 
     def __call__(self, inputs, stream=None):
-        """inputs: one tensor (chained) or one per layer (independent).  Returns outputs."""
+        """inputs: one tensor (chained) or one per layer (independent).  Returns the layers'
+        logical outputs (views without padding channels)."""
         outs = []
         x = inputs if self.chained else None
         for k, sl in enumerate(self.layers):
             src = x if self.chained else inputs[k]
-            y = sl(src, stream)
-            outs.append(y)
-            x = y
+            sl(src, stream)
+            outs.append(sl.y_logical)
+            x = sl.y
         return outs
 
     def launches(self) -> int:

@@ -200,6 +200,14 @@ EOPS = {
     "selective_add_9x9": lambda: (ec.selective_add(1, 4, 3, 1, 9, 9, 4, 2, 1), [(1, 4, 3, 9, 9, 1)]),
     "fused_pair": lambda: (ec.fused_pad_then_offset_add(1, 5, 6, 2, 3, 3, 1, 3), [(1, 5, 6, 18)]),
     "affine_mix": lambda: (ec.affine_mix(2, 3, 5, 6), [(2, 3, 5, 6), (5, 6)]),
+    # fast paths: tiled transpose (inner output dim strided in the input) and affine gather
+    "transpose_big": lambda: (ec.transpose_nchw_to_nhwc(2, 70, 33, 45), [(2, 70, 33, 45)]),
+    "channel_pad_big": lambda: (ec.channel_pad(3, 17, 40, 12, 16), [(3, 17, 40, 12)]),
+    "flip_pad": lambda: ({"inputs": [{"shape": [5, 37], "pad": [[2, 1], [0, 3]]}],
+                          "scopes": [{"trav": [[0, 8], [0, 40]], "sum": [],
+                                      "access": [{"tensor": 0, "index": [ec.idx(ec.I(0, -1), const=5),
+                                                                         ec.idx(ec.I(1))]}],
+                                      "body": [["acc", 0]]}]}, [(5, 37)]),
 }
 
 
