@@ -90,6 +90,12 @@ __global__ void __launch_bounds__(256) eop_affine_gather_kernel(const __grid_con
                     const int32_t c = e.a[k][dl], b = idx[k], n = e.shape[k];
                     if (c == 0) {
                         if (b < 0 || b >= n) jhi = 0;
+                    } else if (c == 1) {                 // the common cases, division-free
+                        jlo = max(jlo, -b);
+                        jhi = min(jhi, n - b);
+                    } else if (c == -1) {
+                        jlo = max(jlo, b - n + 1);
+                        jhi = min(jhi, b + 1);
                     } else if (c > 0) {
                         jlo = max(jlo, cdiv32(-b, c));
                         jhi = min(jhi, fdiv32(n - 1 - b, c) + 1);
@@ -129,40 +135,47 @@ __global__ void __launch_bounds__(256) eop_affine_gather_kernel(const __grid_con
 }
 
 // Tiled transpose: the output's innermost dim (dl) is strided in the input and dim dt has input
-// stride 1.  Block = one 32 x 32 tile of (dt, dl) for one combination of the other dims.  No pad
-// band (checked on the host).  grid.x = tiles over (dt, dl), grid.y = other-dims combinations.
+// stride 1.  A block moves a 32 (dt) x 128 (dl) strip as four 32 x 32 tiles through shared
+// memory, so both the reads (along dt) and the writes (along dl) are coalesced; same-dtype moves
+// copy raw bits.  No pad band (checked on the host).  grid.x = strips, grid.y = other dims.
+template <typename E>
 __global__ void __launch_bounds__(256) eop_affine_transpose_kernel(const __grid_constant__ AffineEop e) {
-    __shared__ float tile[32][33];
+    __shared__ E tile[32][33];
     const int dl = e.nd_out - 1, dt = e.dt;
-    const int32_t nt_l = (e.w[dl] + 31) / 32;
-    const int32_t tl = (int32_t)(blockIdx.x % nt_l), tt = (int32_t)(blockIdx.x / nt_l);
-    // decode the other output dims from blockIdx.y (row-major over dims != dt, dl)
+    const int32_t ns_l = (e.w[dl] + 127) / 128;
+    const int32_t sl = (int32_t)(blockIdx.x % ns_l), tt = (int32_t)(blockIdx.x / ns_l);
     int32_t rest = (int32_t)blockIdx.y;
     int32_t off = e.base;
     int64_t obase = 0, ostride = 1;
-    int32_t ostr[FAST_MAX_D];
+    int64_t ostr[FAST_MAX_D];
     for (int d = e.nd_out - 1; d >= 0; --d) {
-        ostr[d] = (int32_t)ostride;
+        ostr[d] = ostride;
         ostride *= e.w[d];
     }
     for (int d = e.nd_out - 1; d >= 0; --d) {
         if (d == dl || d == dt) continue;
-        const int32_t od = rest % e.w[d];
-        rest /= e.w[d];
+        const int32_t q = rest / e.w[d];
+        const int32_t od = rest - q * e.w[d];
+        rest = q;
         off += e.s[d] * od;
-        obase += (int64_t)ostr[d] * od;
+        obase += ostr[d] * od;
     }
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    // read: coalesced along dt (input stride 1)
-    for (int r = ty; r < 32; r += 8) {
-        const int32_t ol = tl * 32 + r, ot = tt * 32 + tx;
-        if (ol < e.w[dl] && ot < e.w[dt]) tile[r][tx] = fast_ld(e, off + e.s[dl] * ol + ot);
-    }
-    __syncthreads();
-    // write: coalesced along dl (output stride 1)
-    for (int r = ty; r < 32; r += 8) {
-        const int32_t ot = tt * 32 + r, ol = tl * 32 + tx;
-        if (ol < e.w[dl] && ot < e.w[dt]) fast_st(e, obase + (int64_t)ostr[dt] * ot + ol, tile[tx][r]);
+    const E *in = reinterpret_cast<const E *>(e.in);
+    E *out = reinterpret_cast<E *>(e.out);
+    for (int sub = 0; sub < 4; ++sub) {
+        const int32_t l0 = sl * 128 + sub * 32;
+        if (l0 >= e.w[dl]) break;
+        for (int r = ty; r < 32; r += 8) {           // read: coalesced along dt (input stride 1)
+            const int32_t ol = l0 + r, ot = tt * 32 + tx;
+            if (ol < e.w[dl] && ot < e.w[dt]) tile[r][tx] = __ldg(in + off + e.s[dl] * ol + ot);
+        }
+        __syncthreads();
+        for (int r = ty; r < 32; r += 8) {           // write: coalesced along dl (output stride 1)
+            const int32_t ot = tt * 32 + r, ol = l0 + tx;
+            if (ol < e.w[dl] && ot < e.w[dt]) out[obase + ostr[dt] * ot + ol] = tile[tx][r];
+        }
+        __syncthreads();
     }
 }
 

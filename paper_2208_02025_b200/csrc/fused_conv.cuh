@@ -11,7 +11,11 @@
 // offset into a haloed input patch held in shared memory in the K-major "interleaved"
 // (no-swizzle) UMMA layout, where rows are 16 bytes apart, so ONE TMA load of the patch
 // per channel chunk feeds every tap: tap (i,j) is the same smem tile read from another row.
-// Zero padding is TMA out-of-bounds fill.
+// Zero padding is TMA out-of-bounds fill.  When a channel chunk is a full 128 bytes
+// the patch is instead loaded as 128-byte pixel rows with SWIZZLE_128B (one TMA row per pixel,
+// 8x fewer than 16-byte planar rows); a tap's row shift then starts the descriptor inside a
+// 1024-byte swizzle atom, which is consistent because both TMA and the tensor core apply the
+// swizzle to absolute shared-memory address bits (base offset 0).
 //
 // ConvTranspose2d: the selective addition is split by output residue class
 // (oh mod st, ow mod st) -- expression splitting, P:927-934 -- and every class is a stride-1
@@ -62,6 +66,7 @@ struct FusedArgs {
     int32_t resident;                 // 1: the CTA's whole weight slice stays in smem (loaded once)
     int32_t nbuf;                     // TMEM accumulator sets (2 = epilogue overlaps the next item)
     int32_t acc_cols;                 // TMEM columns per M-tile accumulator (FS rounded up to 32)
+    int32_t sw128;                    // 1: patch rows are 128-byte pixel rows, SWIZZLE_128B (BK*es == 128)
     void *y;
     long long *trace;                 // debug only (nullptr in production): per-CTA timestamps
     FusedClass cls[FC_MAX_CLASSES];
@@ -181,8 +186,12 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                 for (int kci = 0; kci < a.kchunks; ++kci) {
                     mbar_wait(&a_empty[as], ap ^ 1);
                     mbar_arrive_expect_tx(&a_full[as], (uint32_t)a.a_box_bytes);
-                    tma_load_5d(sA + as * a.a_stage_bytes, &tmX, &a_full[as], 0, tc.x0 + cl.px, tc.y0 + cl.py,
-                                tc.img, kc * (a.BK / CI));
+                    if (a.sw128)
+                        tma_load_4d(sA + as * a.a_stage_bytes, &tmX, &a_full[as], kc * a.BK, tc.x0 + cl.px,
+                                    tc.y0 + cl.py, tc.img);
+                    else
+                        tma_load_5d(sA + as * a.a_stage_bytes, &tmX, &a_full[as], 0, tc.x0 + cl.px, tc.y0 + cl.py,
+                                    tc.img, kc * (a.BK / CI));
                     if (++as == a.na) { as = 0; ap ^= 1; }
                     if (!a.resident) {
                         int t = (int)blockIdx.x % ntaps;
@@ -204,12 +213,18 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         // elected thread issues a whole channel chunk: taps x MT x ksteps tcgen05.mma, with
         // descriptors built as templates + 16-byte-unit address adds.
         const uint32_t idesc = make_idesc(kTF32, 128, (uint32_t)a.FS);
-        const uint64_t adesc_t = ((uint64_t)((a.lbo >> 4) & 0x3FFF) << 16) | ((uint64_t)(128 >> 4) << 32) |
-                                 ((uint64_t)1 << 46);
+        const bool sw = a.sw128 != 0;
+        // A: interleaved (LBO = planar chunk stride, SBO = 128 B) or SWIZZLE_128B (SBO = 1024 B)
+        const uint64_t adesc_t = sw ? (((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
+                                       ((uint64_t)2 << 61))
+                                    : (((uint64_t)((a.lbo >> 4) & 0x3FFF) << 16) | ((uint64_t)(128 >> 4) << 32) |
+                                       ((uint64_t)1 << 46));
+        const uint32_t rowb16 = sw ? 8u : 1u;                           // one patch row, 16-byte units
         const uint64_t bdesc_t = ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
                                  ((uint64_t)2 << 61);
         const uint32_t lbo16 = (uint32_t)a.lbo >> 4;
-        const uint32_t mstride16 = (uint32_t)(a.Yb * a.Xb);             // rows between stacked M-tiles
+        const uint32_t mstride16 = (uint32_t)(a.Yb * a.Xb) * rowb16;    // stacked M-tiles, 16-byte units
+        const uint32_t kstep16 = sw ? 2u : 2u * lbo16;                  // one K=16|8 step, 16-byte units
         const uint32_t sA16 = smem_u32(sA) >> 4, sB16 = smem_u32(sB) >> 4;
         const uint32_t astage16 = (uint32_t)a.a_stage_bytes >> 4, bstage16 = (uint32_t)a.b_stage_bytes >> 4;
         const int MT = a.MT, nb = a.nb, na = a.na, kchunks = a.kchunks, nbuf = a.nbuf, BK = a.BK, C = a.C;
@@ -252,21 +267,25 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                             tc_fence_after();
                             b16 = sB16 + (uint32_t)lbs * bstage16;
                         }
-                        const uint64_t ad = adesc_t | (uint64_t)((a16 + cl.tap_off[t]) & 0x3FFF);
+                        const uint32_t at16 = a16 + (uint32_t)cl.tap_off[t] * rowb16;
                         const uint64_t bd = bdesc_t | (uint64_t)(b16 & 0x3FFF);
                         const uint32_t accum = (uint32_t)(kci | ti);
                         for (int m = 0; m < MT; ++m) {
-                            const uint64_t adm = ad + (uint64_t)((uint32_t)m * mstride16);
+                            const uint32_t am16 = at16 + (uint32_t)m * mstride16;
+                            // SWIZZLE_128B rows may start anywhere inside a 1024-byte atom: the tensor
+                            // core XORs with absolute smem address bits, exactly as TMA wrote them, so
+                            // the descriptor's base-offset field stays 0 (verified on B200 by parity)
+                            const uint64_t adm = adesc_t | (uint64_t)(am16 & 0x3FFF);
                             const uint32_t dm = d_tmem + (uint32_t)m * acc_cols;
                             if (full_k) {
 #pragma unroll
                                 for (int k = 0; k < 4; ++k)
-                                    umma<kTF32>(dm, adm + (uint64_t)((uint32_t)(2 * k) * lbo16), bd + (uint64_t)(2 * k),
-                                                idesc, accum | (uint32_t)k);
+                                    umma<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16), bd + (uint64_t)(2 * k), idesc,
+                                                accum | (uint32_t)k);
                             } else {
                                 for (int k = 0; k < ksteps; ++k)
-                                    umma<kTF32>(dm, adm + (uint64_t)((uint32_t)(2 * k) * lbo16), bd + (uint64_t)(2 * k),
-                                                idesc, accum | (uint32_t)k);
+                                    umma<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16), bd + (uint64_t)(2 * k), idesc,
+                                                accum | (uint32_t)k);
                             }
                         }
                         if (!resident) {
@@ -303,56 +322,56 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             const FusedClass &cl = a.cls[tc.cls];
             mbar_wait(&tfull[acc], accp);
             tc_fence_after();
-            for (int m = 0; m < a.MT; ++m)
-                for (int c = 0; c < a.FS; c += 32) {
-                    const int oy = (tc.y0 + m * a.Yb + ly) * a.ost + cl.oy0, ox = (tc.x0 + lx) * a.ost + cl.ox0;
-                    const bool valid = ly < a.Yb && lx < a.XB && oy < a.OH && ox < a.OW;
-                    const int64_t pix = ((int64_t)tc.img * a.OH + oy) * a.OW + ox;
-                    uint32_t v[32];
-                    tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) +
-                                           (uint32_t)((acc * a.MT + m) * a.acc_cols + c),
-                                       v);
+            for (int m = 0; m < a.MT; ++m) {
+                const int oy = (tc.y0 + m * a.Yb + ly) * a.ost + cl.oy0, ox = (tc.x0 + lx) * a.ost + cl.ox0;
+                const bool valid = ly < a.Yb && lx < a.XB && oy < a.OH && ox < a.OW;
+                const int64_t pix = ((int64_t)tc.img * a.OH + oy) * a.OW + ox;
+                const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((acc * a.MT + m) * a.acc_cols);
+                // up to 64 columns per round: both TMEM loads in flight before one wait
+                for (int c0 = 0; c0 < a.FS; c0 += 64) {
+                    uint32_t v[64];
+                    tmem_ld_32x32b_x32(tbase + (uint32_t)c0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+                    const bool two = c0 + 32 < a.FS;
+                    if (two) tmem_ld_32x32b_x32(tbase + (uint32_t)(c0 + 32), *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
                     tmem_ld_wait();
-                    const int f = tc.f0 + c;
-                    if (valid && f < a.F) {
-                        const int nf = min(min(32, a.FS - c), a.F - f);
-                        if constexpr (kTF32) {
-                            float *yp = reinterpret_cast<float *>(a.y) + pix * a.F + f;
-                            if (vec && nf == 32) {
+                    const int f = tc.f0 + c0;
+                    if (!valid || f >= a.F) continue;
+                    const int nf = min(min(64, a.FS - c0), a.F - f);
+                    if constexpr (kTF32) {
+                        float *yp = reinterpret_cast<float *>(a.y) + pix * a.F + f;
+                        if (vec && (nf & 3) == 0) {
 #pragma unroll
-                                for (int e = 0; e < 32; e += 4)
+                            for (int e = 0; e < 64; e += 4)
+                                if (e < nf)
                                     *reinterpret_cast<float4 *>(yp + e) =
                                         make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]),
                                                     __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
-                            } else {
-#pragma unroll
-                                for (int e = 0; e < 32; ++e)
-                                    if (e < nf) yp[e] = __uint_as_float(v[e]);
-                            }
                         } else {
-                            uint16_t *yp = reinterpret_cast<uint16_t *>(a.y) + pix * a.F + f;
-                            if (vec && nf == 32) {
 #pragma unroll
-                                for (int e = 0; e < 32; e += 8) {
+                            for (int e = 0; e < 64; ++e)
+                                if (e < nf) yp[e] = __uint_as_float(v[e]);
+                        }
+                    } else {
+                        uint16_t *yp = reinterpret_cast<uint16_t *>(a.y) + pix * a.F + f;
+                        if (vec && (nf & 7) == 0) {
+#pragma unroll
+                            for (int e = 0; e < 64; e += 8)
+                                if (e < nf) {
                                     uint4 pk;
-                                    pk.x = (uint32_t)float_to_bf16_rne(__uint_as_float(v[e])) |
-                                           ((uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 1])) << 16);
-                                    pk.y = (uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 2])) |
-                                           ((uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 3])) << 16);
-                                    pk.z = (uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 4])) |
-                                           ((uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 5])) << 16);
-                                    pk.w = (uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 6])) |
-                                           ((uint32_t)float_to_bf16_rne(__uint_as_float(v[e + 7])) << 16);
+                                    pk.x = pack_bf16x2_rn(__uint_as_float(v[e]), __uint_as_float(v[e + 1]));
+                                    pk.y = pack_bf16x2_rn(__uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
+                                    pk.z = pack_bf16x2_rn(__uint_as_float(v[e + 4]), __uint_as_float(v[e + 5]));
+                                    pk.w = pack_bf16x2_rn(__uint_as_float(v[e + 6]), __uint_as_float(v[e + 7]));
                                     *reinterpret_cast<uint4 *>(yp + e) = pk;
                                 }
-                            } else {
+                        } else {
 #pragma unroll
-                                for (int e = 0; e < 32; ++e)
-                                    if (e < nf) yp[e] = float_to_bf16_rne(__uint_as_float(v[e]));
-                            }
+                            for (int e = 0; e < 64; ++e)
+                                if (e < nf) yp[e] = float_to_bf16_rne(__uint_as_float(v[e]));
                         }
                     }
                 }
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);

@@ -267,6 +267,8 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
     base.BK = s->c >= BKfull ? BKfull : (int)((s->c + KI - 1) / KI * KI);
     base.kchunks = (int)ceil_div(s->c, base.BK);
     const int nchunk = base.BK / CI;
+    const bool sw128 = base.BK * es == 128;      // full 128-byte channel chunks: SWIZZLE_128B pixel rows
+    const int rowbytes = sw128 ? 128 : 16;
     const int wtaps = (int)(s->r * s->s);
     const int ksteps = base.BK / KI;
     const int sms = num_sms();
@@ -293,8 +295,8 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
             if (Yp > 256) break;
             const int max_off = span_y * Xb + span_x + (MT - 1) * Yb * Xb;
             if (max_off >= 65536) break;
-            const int box = 16 * Xb * Yp * nchunk;
-            const int need = (nchunk - 1) * 16 * Xb * Yp + (max_off + 128) * 16;
+            const int box = 16 * Xb * Yp * nchunk;   // same bytes in both layouts
+            const int need = sw128 ? (max_off + 128) * 128 : (nchunk - 1) * 16 * Xb * Yp + (max_off + 128) * 16;
             const int astage = (int)ceil_div(std::max(box, need), 1024) * 1024;
             if (2 * astage > budget) break;
             const int64_t items_sp = (int64_t)nclass * base.n * ceil_div(GW, XB) * ceil_div(GH, (int64_t)Yb * MT);
@@ -328,7 +330,10 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                     const double instr = (double)base.kchunks * max_taps * ksteps * MT;
                     const double mma = instr * std::max(FS / 2.0, 40.0 + FS / 3.0) +
                                        (resident ? 0.0 : 250.0 * base.kchunks * max_taps);
-                    const double ld = ((double)base.kchunks * box + (resident ? 0.0 : (double)tbytes)) / 40.0;
+                    // TMA issues one request per box row: 16-byte planar rows stream at ~8 B/clk,
+                    // 128-byte pixel rows at ~40 B/clk (tools/trace_fused.py)
+                    const double ld = (double)base.kchunks * box / (sw128 ? 40.0 : 8.0) +
+                                      (resident ? 0.0 : (double)tbytes / 40.0);
                     const double epi = nbuf == 2 ? 0.0 : MT * (FS / 32.0) * 400.0;
                     double t = per_cta * (std::max(mma, ld) + epi + 600.0);
                     if (resident) t += (double)wbytes / 40.0;
@@ -349,6 +354,8 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
     if (!found) return false;
     FusedArgs a = a_best;
     a.lbo = 16 * a.Xb * a.Yp;
+    a.sw128 = sw128 ? 1 : 0;
+    (void)rowbytes;
     a.tiles_x = (int)ceil_div(GW, a.XB);
     a.tiles_y = (int)ceil_div(GH, (int64_t)a.Yb * a.MT);
     a.f_slices = (int)ceil_div(s->f, a.FS);
@@ -501,7 +508,11 @@ static ollie_status run_fused(const ollie_conv_shape *s, bool tf32, int transpos
     const int es = tf32 ? 4 : 2, CI = 16 / es;
     const CUtensorMapDataType dt = tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     CUtensorMap tx, tw;
-    {   // X as 5-D planar view {c_in (16 B), w, h, n, c_out}
+    if (a.sw128) {   // X as 4-D NHWC {c, w, h, n}, box = 128-byte pixel rows, SWIZZLE_128B
+        ollie_status st4 = make_tmap_nhwc(&tx, x, tf32, s->n, s->h, s->w, s->c, (uint32_t)a.BK, (uint32_t)a.Xb,
+                                          (uint32_t)a.Yp, 1);
+        if (st4 != OLLIE_OK) return st4;
+    } else {   // X as 5-D planar view {c_in (16 B), w, h, n, c_out}
         cuuint64_t dims[5] = {(cuuint64_t)CI, (cuuint64_t)s->w, (cuuint64_t)s->h, (cuuint64_t)s->n,
                               (cuuint64_t)(s->c / CI)};
         cuuint64_t strides[4] = {(cuuint64_t)(s->c * es), (cuuint64_t)(s->w * s->c * es),
@@ -1133,7 +1144,7 @@ static int affine_fast_plan(const ollie_eop *e, const void *in, void *out, Affin
     if ((int64_t)fe->rows * ((fe->inner + 7) / 8) >= (1ll << 31)) return 0;
     // transpose path: innermost output dim strided in the input, another output dim with input
     // stride 1, and no pad-band reads (every index interval inside the tensor)
-    if (fe->s[nd - 1] != 1 && fe->s[nd - 1] != 0 && nd >= 2) {
+    if (fe->s[nd - 1] != 1 && fe->s[nd - 1] != 0 && nd >= 2 && fe->in_bf16 == fe->out_bf16) {
         const bool inside = fe->chk == 0;
         for (int d = 0; d < nd - 1 && inside; ++d)
             if (fe->s[d] == 1 && out_elems / ((int64_t)fe->w[d] * fe->inner) < 65536) {
@@ -1192,9 +1203,11 @@ extern "C" ollie_status ollie_eop_eval(const ollie_eop *eop, const void *const *
             int64_t others = 1;
             for (int d = 0; d < fe.nd_out; ++d)
                 if (d != fe.dt && d != fe.nd_out - 1) others *= fe.w[d];
-            const int64_t tiles = ceil_div(fe.w[fe.nd_out - 1], 32) * ceil_div(fe.w[fe.dt], 32);
-            dim3 grid((unsigned)tiles, (unsigned)others);
-            eop_affine_transpose_kernel<<<grid, 256, 0, s>>>(fe);
+            const int64_t strips = ceil_div(fe.w[fe.nd_out - 1], 128) * ceil_div(fe.w[fe.dt], 32);
+            dim3 grid((unsigned)strips, (unsigned)others);
+            if (fe.in_bf16 && fe.out_bf16) eop_affine_transpose_kernel<uint16_t><<<grid, 256, 0, s>>>(fe);
+            else if (!fe.in_bf16 && !fe.out_bf16) eop_affine_transpose_kernel<uint32_t><<<grid, 256, 0, s>>>(fe);
+            else return fail(OLLIE_E_UNSUPPORTED, "internal: converting transpose");
             CHECK_LAUNCH();
             return ok();
         }
@@ -1221,9 +1234,9 @@ extern "C" ollie_status ollie_plan_describe(const ollie_conv_shape *s, ollie_dty
         if (!plan_fused(s, tf32, transposed, &a, OH, OW)) return fail(OLLIE_E_UNSUPPORTED, "no fused plan");
         snprintf(buf, len,
                  "fused XB=%d Yb=%d Xb=%d Yp=%d MT=%d FS=%d f_slices=%d resident=%d nbuf=%d na=%d nb=%d BK=%d "
-                 "kchunks=%d tiles=%d grid=%d smem=%zu classes=%d taps=%d",
+                 "kchunks=%d tiles=%d grid=%d smem=%zu classes=%d taps=%d sw128=%d",
                  a.XB, a.Yb, a.Xb, a.Yp, a.MT, a.FS, a.f_slices, a.resident, a.nbuf, a.na, a.nb, a.BK, a.kchunks,
-                 a.num_tiles, fused_grid(a), fused_smem_bytes(a), a.nclass, a.max_taps);
+                 a.num_tiles, fused_grid(a), fused_smem_bytes(a), a.nclass, a.max_taps, a.sw128);
     } else if (is_identity_offset_add(s, transposed)) {
         snprintf(buf, len, "unfused-identity gemm BN=%d (OffsetAdd eliminated)", choose_bn(s->r * s->s * s->f));
     } else {

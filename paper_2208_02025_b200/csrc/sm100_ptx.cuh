@@ -158,6 +158,13 @@ __device__ __forceinline__ bool elect_one() {
 
 __device__ __forceinline__ float bf16_bits_to_float(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
 
+// Two fp32 -> packed bf16x2 with the hardware RNE conversion (lo in the low half).
+__device__ __forceinline__ uint32_t pack_bf16x2_rn(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
 // Round-to-nearest-even fp32 -> bf16 bits (finite inputs; NaN kept quiet).
 __device__ __forceinline__ uint16_t float_to_bf16_rne(float f) {
     uint32_t u = __float_as_uint(f);

@@ -1,0 +1,19 @@
+#!/bin/bash
+# Run ON THE GPU BOX (via gpurun).  Produces, under gpurun_out/:
+#   <tag>_launches_<cfg>.csv : ncu launch list (gpu__time_duration.sum, --clock-control none) of the
+#                              bench command itself (cold-cache, serialised: compare SHARES)
+#   <tag>_full_<cfg>.ncu-rep : ncu --set full of every libollie kernel of one step of <cfg>
+set -u
+TAG=${TAG:-r01}
+mkdir -p gpurun_out
+for cfg in ${CFGS:-resnet18 csrnet fsrcnn}; do
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file gpurun_out/${TAG}_launches_${cfg}.csv \
+      python bench.py --config $cfg --steps 2 --warmup 3 --no-cpu-baseline --no-cudnn --no-graph \
+      > gpurun_out/${TAG}_launches_${cfg}.log 2>&1
+  timeout 1500 ncu --set full --clock-control none --import-source on \
+      -k regex:"fused_conv|merged_gemm|offset_add|selective_add|eop_" -s ${SKIP:-0} -c ${COUNT:-12} \
+      -o gpurun_out/${TAG}_full_${cfg} python tools/run_layer.py --config $cfg --iters 1 \
+      > gpurun_out/${TAG}_full_${cfg}.log 2>&1
+  echo "$cfg done"
+done

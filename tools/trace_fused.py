@@ -16,7 +16,7 @@ dbg = int([a for a in sys.argv[3:] if a.startswith("flags=")][0][6:]) if any(a.s
 
 lay = syn.CONFIGS[cfg][li]
 x, w = syn.layer_inputs(lay, 1)
-conv = DerivedConv.from_layer(lay).prepare(w.cuda())
+conv = DerivedConv.from_layer(lay, plan=1).prepare(w.cuda())
 xd = x.cuda()
 tr = torch.zeros(148 * 32 * 4, dtype=torch.int64, device="cuda")
 O._lib.ollie_debug_set_trace.argtypes = [ctypes.c_void_p]
@@ -38,7 +38,7 @@ print(lay.name, O.plan_describe(conv.shape, conv.code))
 t = tr.view(-1, 32).cpu()
 t = t[t[:, 30] != 0]
 g0 = t[:, 30].min()
-names = ["setup", "A0", "B0", "tile0_mma", "mma_end", "epi0", "epi_end", "end", "B1", "B2", "B3", "B4", "B5", "B6", "-", "-"] + [f"issueB{k}" for k in range(7)] + [f"reachB{k}" for k in range(1,7)]
+names = ["setup", "A0", "-", "tile0_mma", "-", "epi0", "epi_end", "end"]
 print("CTAs", t.shape[0], "start spread (ns):", int((t[:, 30] - g0).max()))
 for k, nm in enumerate(names):
     if nm == '-': continue
