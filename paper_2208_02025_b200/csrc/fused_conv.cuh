@@ -339,24 +339,23 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                     const int nf = min(min(64, a.FS - c0), a.F - f);
                     if constexpr (kTF32) {
                         float *yp = reinterpret_cast<float *>(a.y) + pix * a.F + f;
-                        if (vec && (nf & 3) == 0) {
+                        const int nv = vec ? (nf & ~3) : 0;      // whole 16-byte groups, then a scalar tail
 #pragma unroll
-                            for (int e = 0; e < 64; e += 4)
-                                if (e < nf)
-                                    *reinterpret_cast<float4 *>(yp + e) =
-                                        make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]),
-                                                    __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
-                        } else {
+                        for (int e = 0; e < 64; e += 4)
+                            if (e < nv)
+                                *reinterpret_cast<float4 *>(yp + e) =
+                                    make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]),
+                                                __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
 #pragma unroll
-                            for (int e = 0; e < 64; ++e)
-                                if (e < nf) yp[e] = __uint_as_float(v[e]);
-                        }
+                        for (int e = 0; e < 64; ++e)
+                            if (e >= nv && e < nf) yp[e] = __uint_as_float(v[e]);
                     } else {
                         uint16_t *yp = reinterpret_cast<uint16_t *>(a.y) + pix * a.F + f;
-                        if (vec && (nf & 7) == 0) {
+                        const int nv = vec ? (nf & ~7) : 0;      // whole 16-byte groups, then a scalar tail
+                        {
 #pragma unroll
                             for (int e = 0; e < 64; e += 8)
-                                if (e < nf) {
+                                if (e < nv) {
                                     uint4 pk;
                                     pk.x = pack_bf16x2_rn(__uint_as_float(v[e]), __uint_as_float(v[e + 1]));
                                     pk.y = pack_bf16x2_rn(__uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
@@ -364,10 +363,9 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                                     pk.w = pack_bf16x2_rn(__uint_as_float(v[e + 6]), __uint_as_float(v[e + 7]));
                                     *reinterpret_cast<uint4 *>(yp + e) = pk;
                                 }
-                        } else {
 #pragma unroll
                             for (int e = 0; e < 64; ++e)
-                                if (e < nf) yp[e] = float_to_bf16_rne(__uint_as_float(v[e]));
+                                if (e >= nv && e < nf) yp[e] = float_to_bf16_rne(__uint_as_float(v[e]));
                         }
                     }
                 }

@@ -9,7 +9,7 @@
 //   warp 0     TMA producer: A / B tiles (K-major, SWIZZLE_128B) into a STAGES-deep smem ring
 //   warp 1     MMA issuer:   one thread issues tcgen05.mma (128 x BN x 16|8) into TMEM
 //   warp 2     TMEM allocator (512 columns = two BN<=256 fp32 accumulators, double-buffered)
-//   warps 4-7  epilogue:     tcgen05.ld -> registers -> padded smem -> coalesced st.global
+//   warps 4-7  epilogue:     tcgen05.ld -> registers -> 16-byte row stores (one row per thread)
 // BN (the UMMA N) is a runtime parameter (multiple of 16, <= 256) chosen on the host to
 // minimise N-tail waste.  M / N / K tails are handled by TMA zero fill and store guards.
 #pragma once
@@ -137,41 +137,64 @@ merged_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
             }
         }
     } else if (warp >= 4) {
-        // ===== epilogue: TMEM -> registers -> smem (padded) -> coalesced global stores =====
+        // ===== epilogue: TMEM -> registers -> global, one output row (pixel) per thread =====
+        // Two 32-column TMEM loads in flight per wait; each thread writes its row's contiguous
+        // columns with 16-byte stores (hardware bf16x2 packing for bf16 output).  Rows of
+        // consecutive lanes are adjacent in memory, and each thread fills whole 32-byte sectors.
         const int ew = warp - 4;                 // == warp % 4: TMEM lane quadrant of this warp
-        float *st = stg + ew * GEMM_STG_FLOATS;
         int acc = 0;
         uint32_t acc_phase = 0;
+        const bool vec = kOutBF16 ? (args.ldo % 8 == 0) : (args.ldo % 4 == 0);
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             const int m_blk = tile / num_n, n_blk = tile % num_n;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const int64_t row0 = (int64_t)m_blk * GEMM_BM + ew * 32;
+            const int64_t row = (int64_t)m_blk * GEMM_BM + ew * 32 + lane;
             const int64_t col_base = (int64_t)n_blk * BN;
             const int64_t col_end = col_base + BN < N ? col_base + BN : N;   // this tile's columns only
-            for (int c = 0; c < BN; c += 32) {
-                if (col_base + c >= col_end) break;
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * GEMM_MAX_BN + c), v);
+            const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * GEMM_MAX_BN);
+            for (int c0 = 0; c0 < BN; c0 += 64) {
+                if (col_base + c0 >= col_end) break;
+                uint32_t v[64];
+                tmem_ld_32x32b_x32(tbase + (uint32_t)c0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+                const bool two = c0 + 32 < BN && col_base + c0 + 32 < col_end;
+                if (two) tmem_ld_32x32b_x32(tbase + (uint32_t)(c0 + 32), *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
                 tmem_ld_wait();
+                if (row >= M) continue;
+                const int nc = (int)min((int64_t)64, col_end - (col_base + c0));
+                if constexpr (kOutBF16) {
+                    uint16_t *o = reinterpret_cast<uint16_t *>(args.out) + row * args.ldo + col_base + c0;
+                    {
+                        const int nv = vec ? (nc & ~7) : 0;      // whole 16-byte groups, then a scalar tail
 #pragma unroll
-                for (int j = 0; j < 32; ++j) st[lane * 33 + j] = __uint_as_float(v[j]);
-                __syncwarp();
-                const int64_t col = col_base + c + lane;
-                if (col < col_end) {
-#pragma unroll 4
-                    for (int r = 0; r < 32; ++r) {
-                        const int64_t row = row0 + r;
-                        if (row < M) {
-                            const float val = st[r * 33 + lane];
-                            if constexpr (kOutBF16)
-                                reinterpret_cast<uint16_t *>(args.out)[row * args.ldo + col] = float_to_bf16_rne(val);
-                            else
-                                reinterpret_cast<float *>(args.out)[row * args.ldo + col] = val;
-                        }
+                        for (int e = 0; e < 64; e += 8)
+                            if (e < nv) {
+                                uint4 pk;
+                                pk.x = pack_bf16x2_rn(__uint_as_float(v[e]), __uint_as_float(v[e + 1]));
+                                pk.y = pack_bf16x2_rn(__uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
+                                pk.z = pack_bf16x2_rn(__uint_as_float(v[e + 4]), __uint_as_float(v[e + 5]));
+                                pk.w = pack_bf16x2_rn(__uint_as_float(v[e + 6]), __uint_as_float(v[e + 7]));
+                                *reinterpret_cast<uint4 *>(o + e) = pk;
+                            }
+#pragma unroll
+                        for (int e = 0; e < 64; ++e)
+                            if (e >= nv && e < nc) o[e] = float_to_bf16_rne(__uint_as_float(v[e]));
+                    }
+                } else {
+                    float *o = reinterpret_cast<float *>(args.out) + row * args.ldo + col_base + c0;
+                    {
+                        const int nv = vec ? (nc & ~3) : 0;      // whole 16-byte groups, then a scalar tail
+#pragma unroll
+                        for (int e = 0; e < 64; e += 4)
+                            if (e < nv)
+                                *reinterpret_cast<float4 *>(o + e) =
+                                    make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]),
+                                                __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
+#pragma unroll
+                        for (int e = 0; e < 64; ++e)
+                            if (e >= nv && e < nc) o[e] = __uint_as_float(v[e]);
                     }
                 }
-                __syncwarp();
             }
             tc_fence_before();
             __syncwarp();

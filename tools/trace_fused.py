@@ -15,6 +15,9 @@ noflush = "noflush" in sys.argv[3:]
 dbg = int([a for a in sys.argv[3:] if a.startswith("flags=")][0][6:]) if any(a.startswith("flags=") for a in sys.argv[3:]) else 0
 
 lay = syn.CONFIGS[cfg][li]
+from dataclasses import replace as _rep
+from paper_2208_02025_b200.stack import padded_channels
+lay = _rep(lay, c=padded_channels(lay.c, lay.dtype), f=padded_channels(lay.f, lay.dtype) if cfg == 'fsrcnn' and li < 7 else lay.f)
 x, w = syn.layer_inputs(lay, 1)
 conv = DerivedConv.from_layer(lay, plan=1).prepare(w.cuda())
 xd = x.cuda()
