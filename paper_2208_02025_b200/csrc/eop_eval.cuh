@@ -156,6 +156,8 @@ __device__ float scope_value(const EopDev &e, int64_t *it) {
 }
 
 __global__ void __launch_bounds__(256) eop_eval_kernel(const __grid_constant__ EopDev e) {
+    pdl_launch_dependents();
+    pdl_wait();
     const DScope &s = e.sc[0];
     for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < e.out_elems;
          o += (int64_t)gridDim.x * blockDim.x) {

@@ -63,6 +63,8 @@ __device__ __forceinline__ E raw_ld(const void *p, int32_t off) { return __ldg(r
 // (raw bit copy); E = void converts through fp32.
 template <int VEC, typename E>
 __global__ void __launch_bounds__(256) eop_affine_gather_kernel(const __grid_constant__ AffineEop e) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int32_t vec_per_row = (e.inner + VEC - 1) / VEC;
     const int32_t total = e.rows * vec_per_row;
     const int dl = e.nd_out - 1;
@@ -140,6 +142,8 @@ __global__ void __launch_bounds__(256) eop_affine_gather_kernel(const __grid_con
 // copy raw bits.  No pad band (checked on the host).  grid.x = strips, grid.y = other dims.
 template <typename E>
 __global__ void __launch_bounds__(256) eop_affine_transpose_kernel(const __grid_constant__ AffineEop e) {
+    pdl_launch_dependents();
+    pdl_wait();
     __shared__ E tile[32][33];
     const int dl = e.nd_out - 1, dt = e.dt;
     const int32_t ns_l = (e.w[dl] + 127) / 128;

@@ -80,6 +80,8 @@ __device__ __forceinline__ void accum_tap(float (&acc)[VEC], const float *src) {
 // decoding is 32-bit (IDX = int32_t) whenever the host proves every index fits.
 template <int VEC, bool kOutBF16, typename IDX>
 __global__ void __launch_bounds__(256) offset_add_kernel(OffsetAddArgs a) {
+    pdl_launch_dependents();
+    pdl_wait();
     const IDX fv_per_px = (IDX)(a.f / VEC);
     const IDX OW = (IDX)a.ow, OHh = (IDX)a.oh;
     for (IDX it = (IDX)(blockIdx.x * blockDim.x + threadIdx.x); it < (IDX)a.items; it += (IDX)(gridDim.x * blockDim.x)) {
@@ -134,6 +136,8 @@ __global__ void __launch_bounds__(256) offset_add_kernel(OffsetAddArgs a) {
 // (mod st) are visited: each output reads exactly the Matmul outputs that land on it.
 template <int VEC, bool kOutBF16, typename IDX>
 __global__ void __launch_bounds__(256) selective_add_kernel(OffsetAddArgs a) {
+    pdl_launch_dependents();
+    pdl_wait();
     const IDX fv_per_px = (IDX)(a.f / VEC);
     const IDX OW = (IDX)a.ow, OHh = (IDX)a.oh;
     const int64_t st = a.stride;
@@ -172,6 +176,8 @@ __global__ void __launch_bounds__(256) selective_add_kernel(OffsetAddArgs a) {
 template <typename E>
 __global__ void __launch_bounds__(256) weight_dlt_kernel(const E *__restrict__ src, E *__restrict__ dst, int64_t F,
                                                          int64_t C, int64_t RS, int64_t sz, int64_t sc) {
+    pdl_launch_dependents();
+    pdl_wait();
     __shared__ E tile[32][33];
     const int64_t f = blockIdx.z;
     const int64_t c0 = (int64_t)blockIdx.y * 32, ij0 = (int64_t)blockIdx.x * 32;

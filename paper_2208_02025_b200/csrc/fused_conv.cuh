@@ -163,12 +163,24 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) FC_TRACE(0);
+    if (threadIdx.x == 0) pdl_launch_dependents();   // the next layer may start its prologue
 
     if (warp == 0) {
         if (lane == 0) {
             // ===== TMA producer: per work item, per channel chunk: 1 patch + the class's weight tiles =====
             int as = 0, bs = 0;
             uint32_t ap = 0, bp = 0;
+            if (blockIdx.x < a.num_tiles) {
+                // weights are read-only: warm L2 with this CTA's first tiles while the previous
+                // layer (which produces X) may still be running, then wait for it
+                const TileCoord tc0 = fc_tile(a, blockIdx.x);
+                const int npre = a.resident ? a.kchunks * wtaps : min(a.nb, a.cls[tc0.cls].ntaps);
+                for (int q = 0; q < npre; ++q) {
+                    const int kc = a.resident ? q / wtaps : 0, t = a.resident ? q % wtaps : a.cls[tc0.cls].tap_w[q];
+                    tma_prefetch_3d(&tmW, kc * (128 / ES), tc0.f0, t);
+                }
+            }
+            pdl_wait();
             if (a.resident && blockIdx.x < a.num_tiles) {
                 // the CTA's f-slice is fixed (grid is a multiple of f_slices): load it once
                 const TileCoord tc0 = fc_tile(a, blockIdx.x);
@@ -317,6 +329,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         int acc = 0;
         uint32_t accp = 0;
         const bool vec = (a.F % (kTF32 ? 4 : 8)) == 0;
+        pdl_wait();   // Y may still be read by the previous kernel: order our stores after it
         for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
             const TileCoord tc = fc_tile(a, tile);
             const FusedClass &cl = a.cls[tc.cls];

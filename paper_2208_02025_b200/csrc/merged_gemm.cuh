@@ -88,6 +88,7 @@ merged_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_base_slot;
+    if (threadIdx.x == 0) pdl_launch_dependents();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -95,6 +96,11 @@ merged_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
             const uint32_t stage_bytes = GEMM_A_STAGE_BYTES + (uint32_t)BN * GEMM_BK_BYTES;
             int stage = 0;
             uint32_t phase = 0;
+            if ((int)blockIdx.x < num_tiles) {   // read-only weights: warm L2 before waiting on the producer of A
+                const int n_blk0 = blockIdx.x % num_n;
+                for (int kb = 0; kb < num_k && kb < GEMM_STAGES; ++kb) tma_prefetch_2d(&tmB, kb * BK, n_blk0 * BN);
+            }
+            pdl_wait();
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
                 const int m_blk = tile / num_n, n_blk = tile % num_n;
                 for (int kb = 0; kb < num_k; ++kb) {
@@ -145,6 +151,7 @@ merged_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         int acc = 0;
         uint32_t acc_phase = 0;
         const bool vec = kOutBF16 ? (args.ldo % 8 == 0) : (args.ldo % 4 == 0);
+        pdl_wait();
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             const int m_blk = tile / num_n, n_blk = tile % num_n;
             mbar_wait(&tfull[acc], acc_phase);

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <utility>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -84,6 +86,34 @@ static int num_sms() {
 static size_t elem_size(ollie_dtype d) { return d == OLLIE_BF16 ? 2 : 4; }
 static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------------------ launches
+// Every libollie kernel is launched with programmatic stream serialization (PDL): it may start
+// while the previous kernel on the stream finishes; kernels call griddepcontrol.wait before
+// touching data another kernel produces (sm100_ptx.cuh).  OLLIE_PDL=0 disables it (A/B tests).
+static bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("OLLIE_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+template <typename... KArgs, typename... Args>
+static cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                          Args &&...args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ------------------------------------------------------------------------ TMA
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -164,8 +194,7 @@ static ollie_status launch_gemm_t(const CUtensorMap &ta, const CUtensorMap &tb, 
     }
     const int64_t tiles = ceil_div(ga.M, GEMM_BM) * ceil_div(ga.N, ga.BN);
     const int grid = (int)std::min<int64_t>(tiles, num_sms());
-    kern<<<grid, GEMM_THREADS, gemm_smem_bytes(), stream>>>(ta, tb, ga);
-    CHECK_LAUNCH();
+    CUDA_TRY(launch(kern, dim3(grid), dim3(GEMM_THREADS), gemm_smem_bytes(), stream, ta, tb, ga));
     return OLLIE_OK;
 }
 
@@ -490,8 +519,7 @@ static ollie_status launch_fused_t(const CUtensorMap &tx, const CUtensorMap &tw,
         CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr_done[dev & 63] = true;
     }
-    kern<<<fused_grid(a), FC_THREADS, fused_smem_bytes(a), stream>>>(tx, tw, a);
-    CHECK_LAUNCH();
+    CUDA_TRY(launch(kern, dim3(fused_grid(a)), dim3(FC_THREADS), fused_smem_bytes(a), stream, tx, tw, a));
     return OLLIE_OK;
 }
 
@@ -587,9 +615,11 @@ static ollie_status prepare_weight(const ollie_conv_shape *s, ollie_dtype dtype,
     const int64_t sc = transposed ? F * RS : RS;
     dim3 grid((unsigned)ceil_div(RS, 32), (unsigned)ceil_div(C, 32), (unsigned)F);
     if (dtype == OLLIE_BF16)
-        weight_dlt_kernel<uint16_t><<<grid, 256, 0, stream>>>((const uint16_t *)w, (uint16_t *)wp, F, C, RS, sz, sc);
+        CUDA_TRY(launch(weight_dlt_kernel<uint16_t>, grid, dim3(256), 0, stream, (const uint16_t *)w, (uint16_t *)wp, F, C,
+                        RS, sz, sc));
     else
-        weight_dlt_kernel<float><<<grid, 256, 0, stream>>>((const float *)w, (float *)wp, F, C, RS, sz, sc);
+        CUDA_TRY(launch(weight_dlt_kernel<float>, grid, dim3(256), 0, stream, (const float *)w, (float *)wp, F, C, RS, sz,
+                        sc));
     CHECK_LAUNCH();
     return ok();
 }
@@ -622,8 +652,8 @@ static ollie_status run_offset_add(const ollie_conv_shape *s, int transposed, co
     const bool i32 = a.items + (int64_t)g * 256 < (1ll << 31);
 #define OA_LAUNCH(K, V, B)                                                                 \
     do {                                                                                   \
-        if (i32) K<V, B, int32_t><<<g, 256, 0, stream>>>(a);                               \
-        else K<V, B, int64_t><<<g, 256, 0, stream>>>(a);                                   \
+        if (i32) CUDA_TRY(launch(K<V, B, int32_t>, dim3(g), dim3(256), 0, stream, a));        \
+        else CUDA_TRY(launch(K<V, B, int64_t>, dim3(g), dim3(256), 0, stream, a));            \
     } while (0)
     if (!transposed) {
         if (vec4) { if (out_bf16) OA_LAUNCH(offset_add_kernel, 4, true); else OA_LAUNCH(offset_add_kernel, 4, false); }
@@ -1191,10 +1221,10 @@ extern "C" ollie_status ollie_eop_eval(const ollie_eop *eop, const void *const *
             const int64_t blocks = std::min<int64_t>(ceil_div((int64_t)fe.rows * vec_per_row, 256), (int64_t)num_sms() * 32);
             const unsigned gb = (unsigned)std::max<int64_t>(blocks, 1);
             if (fe.in_bf16 == fe.out_bf16) {
-                if (fe.in_bf16) eop_affine_gather_kernel<8, uint16_t><<<gb, 256, 0, s>>>(fe);
-                else eop_affine_gather_kernel<4, uint32_t><<<gb, 256, 0, s>>>(fe);
+                if (fe.in_bf16) CUDA_TRY(launch(eop_affine_gather_kernel<8, uint16_t>, dim3(gb), dim3(256), 0, s, fe));
+                else CUDA_TRY(launch(eop_affine_gather_kernel<4, uint32_t>, dim3(gb), dim3(256), 0, s, fe));
             } else {
-                eop_affine_gather_kernel<8, void><<<gb, 256, 0, s>>>(fe);
+                CUDA_TRY(launch(eop_affine_gather_kernel<8, void>, dim3(gb), dim3(256), 0, s, fe));
             }
             CHECK_LAUNCH();
             return ok();
@@ -1205,8 +1235,8 @@ extern "C" ollie_status ollie_eop_eval(const ollie_eop *eop, const void *const *
                 if (d != fe.dt && d != fe.nd_out - 1) others *= fe.w[d];
             const int64_t strips = ceil_div(fe.w[fe.nd_out - 1], 128) * ceil_div(fe.w[fe.dt], 32);
             dim3 grid((unsigned)strips, (unsigned)others);
-            if (fe.in_bf16 && fe.out_bf16) eop_affine_transpose_kernel<uint16_t><<<grid, 256, 0, s>>>(fe);
-            else if (!fe.in_bf16 && !fe.out_bf16) eop_affine_transpose_kernel<uint32_t><<<grid, 256, 0, s>>>(fe);
+            if (fe.in_bf16 && fe.out_bf16) CUDA_TRY(launch(eop_affine_transpose_kernel<uint16_t>, grid, dim3(256), 0, s, fe));
+            else if (!fe.in_bf16 && !fe.out_bf16) CUDA_TRY(launch(eop_affine_transpose_kernel<uint32_t>, grid, dim3(256), 0, s, fe));
             else return fail(OLLIE_E_UNSUPPORTED, "internal: converting transpose");
             CHECK_LAUNCH();
             return ok();
@@ -1216,7 +1246,7 @@ extern "C" ollie_status ollie_eop_eval(const ollie_eop *eop, const void *const *
     st = compile_eop(eop, inputs, output, &dv);
     if (st != OLLIE_OK) return st;
     const int64_t blocks = std::min<int64_t>(ceil_div(dv.out_elems, 256), (int64_t)num_sms() * 32);
-    eop_eval_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(dv);
+    CUDA_TRY(launch(eop_eval_kernel, dim3((unsigned)std::max<int64_t>(blocks, 1)), dim3(256), 0, s, dv));
     CHECK_LAUNCH();
     return ok();
 }

@@ -148,6 +148,25 @@ __host__ __device__ constexpr uint32_t make_idesc(bool tf32, uint32_t M, uint32_
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
+// Programmatic dependent launch (PDL): a kernel launched with the programmatic-serialization
+// attribute may start while its predecessor on the stream is still running; pdl_wait() blocks
+// until the predecessor grid has completed and its memory is visible, pdl_launch_dependents()
+// lets the NEXT kernel start its prologue early.  Both are no-ops without PDL.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// L2 prefetch of a TMA tile (no smem write, no barrier): warms read-only operands before pdl_wait.
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap *m, int32_t c0, int32_t c1, int32_t c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(reinterpret_cast<uint64_t>(m)),
+                 "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *m, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
+
 // One lane of a converged warp returns true (elect.sync); lets warp-uniform code issue
 // single-thread instructions (tcgen05.mma / commit) without divergence.
 __device__ __forceinline__ bool elect_one() {
