@@ -376,7 +376,7 @@ def gpu_main(args):
                     src = sl.x_pad
                 conv = sl.conv
                 l2_flush(rep)
-                if conv.ws_bytes:      # unfused: time the two kernels of the derived program separately
+                if conv.resolved_plan() == "unfused":   # time the two kernels of the program separately
                     M, N, K = lay.gemm_mnk
                     ldT = -(-N // 4) * 4
                     e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
@@ -408,8 +408,8 @@ def gpu_main(args):
         for li, sl in enumerate(stack.layers):
             t = 0.0
             keys = (["eop_channel_pad"] if sl.pad_eop is not None else []) + (
-                ["merged_gemm", "selective_add" if sl.layer.transposed else "offset_add"] if sl.conv.ws_bytes
-                else ["fused_conv"])
+                ["merged_gemm", "selective_add" if sl.layer.transposed else "offset_add"]
+                if sl.conv.resolved_plan() == "unfused" else ["fused_conv"])
             for k in keys:
                 a0, b0, *_ = per[k][nrec[k]]
                 nrec[k] += 1

@@ -133,6 +133,17 @@ ollie_status ollie_convtranspose2d_derived(const ollie_conv_shape *shape, ollie_
 ollie_status ollie_plan_describe(const ollie_conv_shape *shape, ollie_dtype dtype, int plan, int transposed,
                                  char *buf, size_t len);
 
+/* Plan selection by measurement (the paper keeps the candidate with the best measured
+ * performance): times the planner's fused candidates (best few by its cost model) and,
+ * when ws can hold T, the unfused plan, on `stream` (synchronizing it), and makes
+ * OLLIE_PLAN_AUTO use the fastest for this (shape, dtype, direction) from then on, process-wide.
+ * x / w_prep / y / ws as for ollie_conv2d_derived; y ends up holding the layer's result.
+ * best_us (may be NULL) receives the winner's time in microseconds.  Not for capture into a
+ * CUDA graph. */
+ollie_status ollie_autotune_derived(const ollie_conv_shape *shape, ollie_dtype dtype, int transposed,
+                                    const void *x_nhwc, const void *w_prep, void *y_nhwc, void *ws,
+                                    size_t ws_bytes, ollie_stream_t stream, float *best_us);
+
 /* a2 standalone (the merged Matmul of P:1342-1352 on tcgen05 tensor cores):
  *   T[m][n] = sum_k A[m][k] * B[n][k]      A [M][K], B [N][K] in `dtype` (BF16 / TF32),
  *   T fp32 with row stride ldT elements (ldT >= N, ldT % 4 == 0).  K % 8 (bf16) or

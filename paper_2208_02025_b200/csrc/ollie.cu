@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <utility>
+#include <vector>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -234,6 +235,7 @@ extern "C" ollie_status ollie_merged_gemm(int64_t M, int64_t N, int64_t K, ollie
 // Tile geometry + f-slice choice for fused_conv_kernel; see fused_conv.cuh for the design.
 static int g_force_mt = 0, g_force_fs = 0, g_force_res = -1;   // debug plan overrides (0 / -1 = auto)
 static thread_local double g_last_fused_cost = 0, g_last_unfused_cost = 0;
+static thread_local std::vector<FusedArgs> g_last_cands;
 
 // Per-class tap tables (see fused_conv.cuh).  Conv2d: one class, every tap (i, j) at patch row
 // offset i*dil*Xb + j*dil.  ConvTranspose2d (dilation 1): class (a, b) = output residue; kernel
@@ -309,6 +311,7 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
     double best = 1e300;
     FusedArgs a_best{};
     bool found = false;
+    std::vector<std::pair<double, FusedArgs>> all;   // every evaluated plan (autotune candidates)
     for (int XB = (int)std::min<int64_t>(GW, 128); XB >= 1; --XB) {
         const int Xb = XB + span_x;
         if (Xb > 256) continue;
@@ -366,22 +369,25 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                     const double epi = nbuf == 2 ? 0.0 : MT * (FS / 32.0) * 400.0;
                     double t = per_cta * (std::max(mma, ld) + epi + 600.0);
                     if (resident) t += (double)wbytes / 40.0;
-                    if (t < best * 0.995) {
-                        best = t;
+                    {
                         FusedArgs a = base;
                         a.XB = XB; a.Xb = Xb; a.Yb = Yb; a.Yp = Yp; a.MT = MT;
                         a.a_box_bytes = box; a.a_stage_bytes = astage;
                         a.FS = FS; a.acc_cols = acc_cols; a.nbuf = nbuf; a.b_stage_bytes = bstage;
                         a.resident = resident; a.na = na; a.nb = nb;
-                        a_best = a;
-                        found = true;
+                        all.emplace_back(t, a);
+                        if (t < best * 0.995) {
+                            best = t;
+                            a_best = a;
+                            found = true;
+                        }
                     }
                 }
             }
         }
     }
     if (!found) return false;
-    FusedArgs a = a_best;
+    auto finalize = [&](FusedArgs a) -> FusedArgs {
     a.lbo = 16 * a.Xb * a.Yp;
     a.sw128 = sw128 ? 1 : 0;
     (void)rowbytes;
@@ -422,7 +428,21 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                     }
             }
     }
-    *out = a;
+    return a;
+    };
+    *out = finalize(a_best);
+    // autotune candidates: the model's best few, distinct in (geometry, MT, FS, residency)
+    std::sort(all.begin(), all.end(), [](const auto &x, const auto &y) { return x.first < y.first; });
+    g_last_cands.clear();
+    g_last_cands.push_back(*out);
+    for (auto &c : all) {
+        if ((int)g_last_cands.size() >= 8) break;
+        bool dup = false;
+        for (auto &d : g_last_cands)
+            dup |= d.XB == c.second.XB && d.Yb == c.second.Yb && d.MT == c.second.MT && d.FS == c.second.FS &&
+                   d.resident == c.second.resident;
+        if (!dup && c.first < 3.0 * best) g_last_cands.push_back(finalize(c.second));
+    }
     // the cost of the same layer unfused (GEMM writes T, OffsetAdd reads it back): AUTO only fuses
     // when the fused estimate is lower
     const double tbytes_unf = (double)(s->n * s->h * s->w) * (double)(s->r * s->s * s->f) * 4.0;
@@ -441,31 +461,38 @@ struct PlanKey {
 };
 struct PlanEntry {
     bool ok;
-    FusedArgs args;
+    FusedArgs args;                 // the plan in use (model's best, or the autotuned winner)
+    std::vector<FusedArgs> cands;   // autotune candidates (cands[0] = model's best)
     double fused_cost, unfused_cost;
+    int tuned;                      // 0: model decides; 1: autotuned fused; 2: autotuned unfused
 };
 static std::mutex g_plan_mu;
 static std::map<PlanKey, PlanEntry> g_plan_cache;
 
-static const PlanEntry &plan_entry(const ollie_conv_shape *s, bool tf32, int transposed, int64_t OH, int64_t OW) {
+static PlanEntry *plan_entry_mut(const ollie_conv_shape *s, bool tf32, int transposed, int64_t OH, int64_t OW) {
     PlanKey k{{s->n, s->c, s->h, s->w, s->f, s->r * 65536 + s->s, s->pad, s->stride * 65536 + s->dilation,
                (int64_t)tf32 * 2 + transposed + 4 * (int64_t)s->output_padding, num_sms(),
                g_force_mt * 1000 + g_force_fs, g_force_res}};
     {
         std::lock_guard<std::mutex> g(g_plan_mu);
         auto it = g_plan_cache.find(k);
-        if (it != g_plan_cache.end()) return it->second;
+        if (it != g_plan_cache.end()) return &it->second;
     }
     PlanEntry e{};
     e.ok = plan_fused_search(s, tf32, transposed, &e.args, OH, OW);
     e.fused_cost = g_last_fused_cost;
     e.unfused_cost = g_last_unfused_cost;
+    if (e.ok) e.cands = g_last_cands;
     std::lock_guard<std::mutex> g(g_plan_mu);
-    return g_plan_cache.emplace(k, e).first->second;   // std::map references stay valid
+    return &g_plan_cache.emplace(k, e).first->second;   // std::map nodes are stable
+}
+static const PlanEntry &plan_entry(const ollie_conv_shape *s, bool tf32, int transposed, int64_t OH, int64_t OW) {
+    return *plan_entry_mut(s, tf32, transposed, OH, OW);
 }
 
 static bool plan_fused(const ollie_conv_shape *s, bool tf32, int transposed, FusedArgs *out, int64_t OH, int64_t OW) {
     const PlanEntry &e = plan_entry(s, tf32, transposed, OH, OW);
+    std::lock_guard<std::mutex> g(g_plan_mu);
     if (e.ok) *out = e.args;
     return e.ok;
 }
@@ -506,6 +533,8 @@ static bool fused_preferred(const ollie_conv_shape *s, bool tf32, int transposed
     int64_t OH, OW;
     if (!out_hw(s, transposed, &OH, &OW)) return false;
     const PlanEntry &e = plan_entry(s, tf32, transposed, OH, OW);
+    std::lock_guard<std::mutex> g(g_plan_mu);
+    if (e.tuned) return e.ok && e.tuned == 1;
     return e.ok && e.fused_cost <= e.unfused_cost;
 }
 
@@ -1285,4 +1314,76 @@ extern "C" void ollie_debug_force_plan(int mt, int fs, int resident) {
     g_force_mt = mt;
     g_force_fs = fs;
     g_force_res = resident;
+}
+
+// ------------------------------------------------------------------------ autotune
+extern "C" ollie_status ollie_autotune_derived(const ollie_conv_shape *s, ollie_dtype dtype, int transposed,
+                                               const void *x, const void *wp, void *y, void *ws, size_t ws_bytes,
+                                               ollie_stream_t stream_, float *best_us) {
+    int64_t OH, OW;
+    ollie_status st = check_shape(s, transposed, &OH, &OW);
+    if (st != OLLIE_OK) return st;
+    if (dtype != OLLIE_BF16 && dtype != OLLIE_TF32) return fail(OLLIE_E_UNSUPPORTED, "dtype must be BF16 or TF32");
+    if (!x || !wp || !y) return fail(OLLIE_E_INVALID, "null pointer");
+    cudaStream_t stream = (cudaStream_t)stream_;
+    const bool tf32 = dtype == OLLIE_TF32;
+    if (is_identity_offset_add(s, transposed)) {   // nothing to choose: the GEMM writes Y
+        if (best_us) *best_us = 0.f;
+        return ok();
+    }
+    PlanEntry *e = plan_entry_mut(s, tf32, transposed, OH, OW);
+    const int64_t M = s->n * s->h * s->w;
+    const size_t need = (size_t)M * (size_t)ldT_of(s) * sizeof(float);
+    const bool unfused_ok = ws && ws_bytes >= need && !(transposed && s->dilation != 1);
+    std::vector<FusedArgs> cands;
+    {
+        std::lock_guard<std::mutex> g(g_plan_mu);
+        if (e->ok) cands = e->cands;
+    }
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    auto time_it = [&](auto &&run) -> float {
+        if (run() != OLLIE_OK) return 1e30f;                  // warm-up (and plan check)
+        float best = 1e30f;
+        for (int r = 0; r < 3; ++r) {
+            cudaEventRecord(e0, stream);
+            if (run() != OLLIE_OK) return 1e30f;
+            cudaEventRecord(e1, stream);
+            cudaEventSynchronize(e1);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            best = std::min(best, ms);
+        }
+        return best;
+    };
+    float best = 1e30f;
+    int best_k = -1;                                          // -1: unfused
+    for (int k = 0; k < (int)cands.size(); ++k) {
+        {
+            std::lock_guard<std::mutex> g(g_plan_mu);
+            e->args = cands[k];
+        }
+        const float t = time_it([&] { return run_fused(s, tf32, transposed, x, wp, y, OH, OW, stream); });
+        if (t < best) { best = t; best_k = k; }
+    }
+    float t_unf = 1e30f;
+    if (unfused_ok && aligned16(ws)) {
+        t_unf = time_it([&] {
+            ollie_status r = run_gemm(M, s->r * s->s * s->f, s->c, tf32, x, wp, ws, ldT_of(s), false, stream);
+            if (r != OLLIE_OK) return r;
+            return run_offset_add(s, transposed, (const float *)ws, ldT_of(s), !tf32, y, OH, OW, stream);
+        });
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    {
+        std::lock_guard<std::mutex> g(g_plan_mu);
+        if (best_k >= 0) e->args = cands[best_k];
+        e->tuned = (t_unf < best || best_k < 0) ? 2 : 1;
+    }
+    if (best_us) *best_us = 1e3f * std::min(best, t_unf);
+    if (best_k < 0 && !unfused_ok) return fail(OLLIE_E_UNSUPPORTED, "no runnable plan to tune");
+    // leave y holding the chosen plan's result
+    return derived_layer(s, dtype, x, wp, y, ws, ws_bytes, OLLIE_PLAN_AUTO, stream, transposed);
 }

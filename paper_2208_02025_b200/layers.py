@@ -16,7 +16,7 @@ class DerivedConv:
     program merged-GEMM + OffsetAdd / selective addition."""
 
     def __init__(self, n, c, h, w, f, r, s, pad=0, stride=1, dilation=1, output_padding=0,
-                 transposed=False, dtype="bf16", plan=_o.PLAN_AUTO, device="cuda"):
+                 transposed=False, dtype="bf16", plan=_o.PLAN_AUTO, device="cuda", autotune=True):
         self.shape = _o.conv_shape(n, c, h, w, f, r, s, pad, stride, dilation, output_padding)
         self.transposed = bool(transposed)
         self.dtype = dtype
@@ -26,13 +26,20 @@ class DerivedConv:
         self.oh, self.ow = _o.output_hw(self.shape, self.transposed)
         self.w_prep = torch.empty(r * s * f, c, dtype=_TORCH[dtype], device=self.device)
         nbytes = _o.workspace_bytes(self.shape, self.code, plan, self.transposed)
+        self.autotune = autotune and plan == _o.PLAN_AUTO
+        if self.autotune:
+            # the unfused plan is an autotune candidate when its T fits a modest workspace
+            unf = _o.workspace_bytes(self.shape, self.code, _o.PLAN_UNFUSED, self.transposed)
+            if unf <= (1 << 30):
+                nbytes = max(nbytes, unf)
         self.ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device) if nbytes else None
         self.ws_bytes = nbytes
+        self._tuned = False
 
     @classmethod
-    def from_layer(cls, layer, plan=_o.PLAN_AUTO, device="cuda"):
+    def from_layer(cls, layer, plan=_o.PLAN_AUTO, device="cuda", autotune=True):
         return cls(layer.n, layer.c, layer.h, layer.w, layer.f, layer.r, layer.s, layer.pad, layer.stride,
-                   layer.dilation, layer.output_padding, layer.transposed, layer.dtype, plan, device)
+                   layer.dilation, layer.output_padding, layer.transposed, layer.dtype, plan, device, autotune)
 
     def prepare(self, weight: torch.Tensor, stream=None):
         """a0: weight DLT, once ("compile time").  weight is PyTorch-layout, on the device."""
@@ -43,6 +50,11 @@ class DerivedConv:
             _o.prepare_weight_conv2d(self.shape, self.code, weight, self.w_prep, stream)
         return self
 
+    def resolved_plan(self) -> str:
+        """'fused', 'unfused' or 'identity' (unfused GEMM writing Y; OffsetAdd eliminated)."""
+        d = _o.plan_describe(self.shape, self.code, self.plan, self.transposed)
+        return "identity" if d.startswith("unfused-identity") else d.split()[0]
+
     def out_shape(self):
         return (self.shape.n, self.oh, self.ow, self.shape.f)
 
@@ -52,6 +64,12 @@ class DerivedConv:
     def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         if y is None:
             y = self.new_output()
+        if self.autotune and not self._tuned:
+            # first call: pick the plan by measurement; not during graph capture
+            if not torch.cuda.is_current_stream_capturing():
+                _o.autotune_derived(self.shape, self.code, self.transposed, x, self.w_prep, y, self.ws,
+                                    self.ws_bytes, stream)
+                self._tuned = True
         fn = _o.convtranspose2d_derived if self.transposed else _o.conv2d_derived
         fn(self.shape, self.code, x, self.w_prep, y, self.ws, self.ws_bytes, self.plan, stream)
         return y

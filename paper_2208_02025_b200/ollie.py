@@ -89,6 +89,8 @@ _sig = {
     "ollie_convtranspose2d_derived": (c_int, [_P(ConvShape), c_int, c_void_p, c_void_p, c_void_p, c_void_p,
                                               c_size_t, c_int, c_void_p]),
     "ollie_plan_describe": (c_int, [_P(ConvShape), c_int, c_int, c_int, c_char_p, c_size_t]),
+    "ollie_autotune_derived": (c_int, [_P(ConvShape), c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+                                       c_size_t, c_void_p, _P(c_float)]),
     "ollie_merged_gemm": (c_int, [c_int64, c_int64, c_int64, c_int, c_void_p, c_void_p, c_void_p, c_int64,
                                   c_void_p]),
     "ollie_offset_add": (c_int, [_P(ConvShape), c_int, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
@@ -194,6 +196,16 @@ def plan_describe(shape: ConvShape, dtype: int, plan: int = PLAN_AUTO, transpose
     buf = ctypes.create_string_buffer(512)
     _check(_lib.ollie_plan_describe(ctypes.byref(shape), dtype, plan, int(transposed), buf, 512), "ollie_plan_describe")
     return buf.value.decode()
+
+
+def autotune_derived(shape: ConvShape, dtype: int, transposed: bool, x, w_prep, y, ws=None, ws_bytes: int = 0,
+                     stream=None) -> float:
+    """Time the candidate plans on the device; OLLIE_PLAN_AUTO uses the winner from then on."""
+    best = c_float(0.0)
+    _check(_lib.ollie_autotune_derived(ctypes.byref(shape), dtype, int(transposed), _ptr(x), _ptr(w_prep), _ptr(y),
+                                       _ptr(ws), ws_bytes, _stream(stream), ctypes.byref(best)),
+           "ollie_autotune_derived")
+    return best.value
 
 
 def merged_gemm(M: int, N: int, K: int, dtype: int, A, B, T, ldT: int, stream=None):

@@ -88,7 +88,7 @@ class StackLayer:
     def launches(self) -> int:
         """Kernels one call launches (pad eOp + 1 fused / identity-eliminated, or 2 unfused)."""
         n = 1 if self.pad_eop is not None else 0
-        return n + (1 if self.conv.ws_bytes == 0 else 2)
+        return n + (2 if self.conv.resolved_plan() == "unfused" else 1)
 
 
 class DerivedStack:
