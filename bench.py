@@ -497,6 +497,9 @@ def _traffic_from_profiles(cfg, kernel):
 
 
 def _time_cudnn(layers, chained, xs_host, ws_dev, dev, l2_flush, steps, stream):
+    """cuDNN through torch (channels_last, cudnn.benchmark) on the same inputs, timed exactly like
+    our step: one CUDA-graph replay per step after the same L2 flush, CUDA events around it.
+    Per-layer times come from an eager pass (events between layers)."""
     import torch
     import torch.nn.functional as F
     torch.backends.cudnn.benchmark = True
@@ -505,50 +508,56 @@ def _time_cudnn(layers, chained, xs_host, ws_dev, dev, l2_flush, steps, stream):
     xs = [x.to(dev).permute(0, 3, 1, 2).contiguous(memory_format=torch.channels_last) for x in xs_host]
     ws = [w.contiguous(memory_format=torch.channels_last) for w in ws_dev]
 
+    def layer(li, src):
+        lay = layers[li]
+        if lay.transposed:
+            return F.conv_transpose2d(src, ws[li], stride=lay.stride, padding=lay.pad,
+                                      output_padding=lay.output_padding, dilation=lay.dilation)
+        return F.conv2d(src, ws[li], stride=lay.stride, padding=lay.pad, dilation=lay.dilation)
+
     def run():
         x = xs[0]
-        outs = []
-        for li, lay in enumerate(layers):
-            src = x if chained else xs[li]
-            if lay.transposed:
-                y = F.conv_transpose2d(src, ws[li], stride=lay.stride, padding=lay.pad,
-                                       output_padding=lay.output_padding, dilation=lay.dilation)
-            else:
-                y = F.conv2d(src, ws[li], stride=lay.stride, padding=lay.pad, dilation=lay.dilation)
-            outs.append(y)
-            x = y
-        return outs
+        for li in range(len(layers)):
+            x = layer(li, x if chained else xs[li])
+        return x
 
     with torch.cuda.stream(stream):
         for _ in range(5):
             run()
     torch.cuda.synchronize()
-    per_layer = [0.0] * len(layers)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        run()
+    torch.cuda.synchronize()
     tot = []
+    with torch.cuda.stream(stream):
+        for k in range(steps):
+            l2_flush(k)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            graph.replay()
+            e1.record(stream)
+            tot.append((e0, e1))
+    torch.cuda.synchronize()
+    ms = statistics.mean(a.elapsed_time(b) for a, b in tot)
+    per_layer = [0.0] * len(layers)
     with torch.cuda.stream(stream):
         for k in range(steps):
             l2_flush(k)
             evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(layers) + 1)]
             evs[0].record(stream)
             x = xs[0]
-            for li, lay in enumerate(layers):
-                src = x if chained else xs[li]
-                if lay.transposed:
-                    x = F.conv_transpose2d(src, ws[li], stride=lay.stride, padding=lay.pad,
-                                           output_padding=lay.output_padding, dilation=lay.dilation)
-                else:
-                    x = F.conv2d(src, ws[li], stride=lay.stride, padding=lay.pad, dilation=lay.dilation)
+            for li in range(len(layers)):
+                x = layer(li, x if chained else xs[li])
                 evs[li + 1].record(stream)
-            tot.append(evs)
-    torch.cuda.synchronize()
-    for evs in tot:
-        for li in range(len(layers)):
-            per_layer[li] += evs[li].elapsed_time(evs[li + 1]) / steps
-    ms = statistics.mean(e[0].elapsed_time(e[-1]) for e in tot)
+            torch.cuda.synchronize()
+            for li in range(len(layers)):
+                per_layer[li] += evs[li].elapsed_time(evs[li + 1]) / steps
     flops = sum(l.useful_flops for l in layers)
     return {"ms_per_step": ms, "tflops": flops / (ms * 1e-3) / 1e12,
             "per_layer_us": {l.name: 1e3 * t for l, t in zip(layers, per_layer)},
-            "note": "torch F.conv2d/conv_transpose2d channels_last, cudnn.benchmark=True, eager (no graph)"}
+            "note": "torch F.conv2d/conv_transpose2d channels_last, cudnn.benchmark=True; step = CUDA-graph "
+                    "replay after the same L2 flush (like ours); per_layer_us from an eager pass"}
 
 
 def main():

@@ -67,6 +67,7 @@ struct FusedArgs {
     int32_t nbuf;                     // TMEM accumulator sets (2 = epilogue overlaps the next item)
     int32_t acc_cols;                 // TMEM columns per M-tile accumulator (FS rounded up to 32)
     int32_t sw128;                    // 1: patch rows are 128-byte pixel rows, SWIZZLE_128B (BK*es == 128)
+    int32_t tmem_cols;                // 512 (1 CTA / SM) or 256 (2 CTAs / SM share the SM's TMEM)
     void *y;
     long long *trace;                 // debug only (nullptr in production): per-CTA timestamps
     FusedClass cls[FC_MAX_CLASSES];
@@ -116,7 +117,7 @@ __device__ __forceinline__ TileCoord fc_tile(const FusedArgs &a, int tile) {
 }
 
 template <bool kTF32>
-__global__ void __launch_bounds__(FC_THREADS, 1)
+__global__ void __launch_bounds__(FC_THREADS, 2)
 fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                   const __grid_constant__ FusedArgs a) {
     constexpr int ES = kTF32 ? 4 : 2;
@@ -157,7 +158,10 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc<FC_TMEM_COLS>(tmem_slot);
+    if (warp == 2) {
+        if (a.tmem_cols == 256) tmem_alloc<256>(tmem_slot);
+        else tmem_alloc<FC_TMEM_COLS>(tmem_slot);
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -397,7 +401,8 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     if (threadIdx.x == 0) FC_TRACE(7);
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<FC_TMEM_COLS>(tmem_base);
+        if (a.tmem_cols == 256) tmem_dealloc<256>(tmem_base);
+        else tmem_dealloc<FC_TMEM_COLS>(tmem_base);
     }
 }
 

@@ -344,19 +344,24 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                 if (items > INT32_MAX) continue;
                 const int64_t wbytes = (int64_t)wtaps * base.kchunks * bstage;          // whole slice
                 const int64_t tbytes = (int64_t)max_taps * base.kchunks * bstage;       // per item
+                for (int occ = 1; occ <= 2; ++occ)
                 for (int resident = 0; resident <= 1; ++resident) {
                     if (g_force_res >= 0 && resident != g_force_res) continue;
+                    // occ = 2: two CTAs per SM, each with half the smem and 256 TMEM columns
+                    const int bud = occ == 1 ? budget : (113 * 1024 - 2048);
+                    const int nbuf_o = occ == 1 ? nbuf : (2 * MT * acc_cols <= 256 ? 2 : 1);
+                    if (occ == 2 && MT * acc_cols > 256) continue;
                     int na, nb;
                     if (resident) {
-                        if (wbytes + 2 * astage > budget) continue;
-                        na = (int)std::min<int64_t>(4, (budget - wbytes) / astage);
+                        if (wbytes + 2 * astage > bud) continue;
+                        na = (int)std::min<int64_t>(4, (bud - wbytes) / astage);
                         nb = 1;
                     } else {
-                        na = budget >= 3 * astage + 4 * bstage ? 3 : 2;
-                        nb = std::min(8, (budget - na * astage) / bstage);
+                        na = bud >= 3 * astage + 4 * bstage ? 3 : 2;
+                        nb = std::min(8, (bud - na * astage) / bstage);
                         if (nb < 2) continue;
                     }
-                    int grid = (int)std::min<int64_t>(items, sms);
+                    int grid = (int)std::min<int64_t>(items, (int64_t)occ * sms);
                     if (resident) grid = (int)std::max<int64_t>(slices, grid / slices * slices);
                     const double per_cta = (double)ceil_div(items, grid);
                     const double instr = (double)base.kchunks * max_taps * ksteps * MT;
@@ -366,15 +371,17 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                     // 128-byte pixel rows at ~40 B/clk (tools/trace_fused.py)
                     const double ld = (double)base.kchunks * box / (sw128 ? 40.0 : 8.0) +
                                       (resident ? 0.0 : (double)tbytes / 40.0);
-                    const double epi = nbuf == 2 ? 0.0 : MT * (FS / 32.0) * 400.0;
-                    double t = per_cta * (std::max(mma, ld) + epi + 600.0);
+                    const double epi = nbuf_o == 2 ? 0.0 : MT * (FS / 32.0) * 400.0;
+                    // two co-resident CTAs share the SM's tensor core: count both CTAs' work
+                    double t = per_cta * occ * (std::max(mma, ld) + epi + 600.0) / (occ == 2 ? 1.6 : 1.0);
                     if (resident) t += (double)wbytes / 40.0;
                     {
                         FusedArgs a = base;
                         a.XB = XB; a.Xb = Xb; a.Yb = Yb; a.Yp = Yp; a.MT = MT;
                         a.a_box_bytes = box; a.a_stage_bytes = astage;
-                        a.FS = FS; a.acc_cols = acc_cols; a.nbuf = nbuf; a.b_stage_bytes = bstage;
+                        a.FS = FS; a.acc_cols = acc_cols; a.nbuf = nbuf_o; a.b_stage_bytes = bstage;
                         a.resident = resident; a.na = na; a.nb = nb;
+                        a.tmem_cols = occ == 1 ? 512 : 256;
                         all.emplace_back(t, a);
                         if (t < best * 0.995) {
                             best = t;
@@ -435,13 +442,15 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
     std::sort(all.begin(), all.end(), [](const auto &x, const auto &y) { return x.first < y.first; });
     g_last_cands.clear();
     g_last_cands.push_back(*out);
+    // the model's best geometry for every (MT, FS, residency, CTAs-per-SM) family, cheapest first:
+    // structurally different plans the cost model cannot rank reliably are measured instead
     for (auto &c : all) {
-        if ((int)g_last_cands.size() >= 8) break;
+        if ((int)g_last_cands.size() >= 24) break;
         bool dup = false;
         for (auto &d : g_last_cands)
-            dup |= d.XB == c.second.XB && d.Yb == c.second.Yb && d.MT == c.second.MT && d.FS == c.second.FS &&
-                   d.resident == c.second.resident;
-        if (!dup && c.first < 3.0 * best) g_last_cands.push_back(finalize(c.second));
+            dup |= d.MT == c.second.MT && d.FS == c.second.FS && d.resident == c.second.resident &&
+                   d.tmem_cols == c.second.tmem_cols;
+        if (!dup && c.first < 4.0 * best) g_last_cands.push_back(finalize(c.second));
     }
     // the cost of the same layer unfused (GEMM writes T, OffsetAdd reads it back): AUTO only fuses
     // when the fused estimate is lower
@@ -498,7 +507,8 @@ static bool plan_fused(const ollie_conv_shape *s, bool tf32, int transposed, Fus
 }
 
 static int fused_grid(const FusedArgs &a) {
-    int grid = (int)std::min<int64_t>(a.num_tiles, num_sms());
+    const int occ = a.tmem_cols == 256 ? 2 : 1;
+    int grid = (int)std::min<int64_t>(a.num_tiles, (int64_t)occ * num_sms());
     if (a.resident) grid = std::max(a.f_slices, grid / a.f_slices * a.f_slices);   // fixed f-slice per CTA
     return grid;
 }
@@ -1293,9 +1303,10 @@ extern "C" ollie_status ollie_plan_describe(const ollie_conv_shape *s, ollie_dty
         if (!plan_fused(s, tf32, transposed, &a, OH, OW)) return fail(OLLIE_E_UNSUPPORTED, "no fused plan");
         snprintf(buf, len,
                  "fused XB=%d Yb=%d Xb=%d Yp=%d MT=%d FS=%d f_slices=%d resident=%d nbuf=%d na=%d nb=%d BK=%d "
-                 "kchunks=%d tiles=%d grid=%d smem=%zu classes=%d taps=%d sw128=%d",
+                 "kchunks=%d tiles=%d grid=%d smem=%zu classes=%d taps=%d sw128=%d ctas_per_sm=%d",
                  a.XB, a.Yb, a.Xb, a.Yp, a.MT, a.FS, a.f_slices, a.resident, a.nbuf, a.na, a.nb, a.BK, a.kchunks,
-                 a.num_tiles, fused_grid(a), fused_smem_bytes(a), a.nclass, a.max_taps, a.sw128);
+                 a.num_tiles, fused_grid(a), fused_smem_bytes(a), a.nclass, a.max_taps, a.sw128,
+                 a.tmem_cols == 256 ? 2 : 1);
     } else if (is_identity_offset_add(s, transposed)) {
         snprintf(buf, len, "unfused-identity gemm BN=%d (OffsetAdd eliminated)", choose_bn(s->r * s->s * s->f));
     } else {
