@@ -68,6 +68,9 @@ struct FusedArgs {
     int32_t acc_cols;                 // TMEM columns per M-tile accumulator (FS rounded up to 32)
     int32_t sw128;                    // 1: patch rows are 128-byte pixel rows, SWIZZLE_128B (BK*es == 128)
     int32_t tmem_cols;                // 512 (1 CTA / SM) or 256 (2 CTAs / SM share the SM's TMEM)
+    int32_t pair;                     // 1: CTA pairs (cluster of 2) issue cta_group::2 MMAs with M = 256
+    int32_t num_items;                // work items: num_tiles (single) or ceil(spatial / 2) * f_slices (pair)
+    int32_t spatial;                  // spatial tiles = nclass * n * tiles_y * tiles_x
     void *y;
     long long *trace;                 // debug only (nullptr in production): per-CTA timestamps
     FusedClass cls[FC_MAX_CLASSES];
@@ -98,6 +101,7 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *m, uin
 
 struct TileCoord {
     int cls, img, y0, x0, f0;   // y0 / x0: first output row / col of the tile in class-grid units
+    bool valid;                 // false: the odd CTA of a pair past the last spatial tile (no stores)
 };
 // tile = (((cls * n + img) * tiles_y + ty) * tiles_x + tx) * f_slices + fs
 __device__ __forceinline__ TileCoord fc_tile(const FusedArgs &a, int tile) {
@@ -113,10 +117,31 @@ __device__ __forceinline__ TileCoord fc_tile(const FusedArgs &a, int tile) {
     t.y0 = ty * a.Yb * a.MT;
     t.x0 = tx * a.XB;
     t.f0 = fs * a.FS;
+    t.valid = true;
     return t;
 }
+// Pair mode: item = (cls * ppc + pp) * f_slices + fs; CTA `rank` of the pair takes tile 2 * pp + rank
+// of class cls.  Both CTAs share the f-slice (the two halves of B serve both CTAs' MMAs) and the
+// class (the leader issues the MMAs with ITS class's tap table for both).
+__device__ __forceinline__ TileCoord fc_tile_pair(const FusedArgs &a, int item, int rank) {
+    const int fs = item % a.f_slices;
+    const int per_cls = a.spatial / a.nclass, ppc = (per_cls + 1) / 2;
+    const int q = item / a.f_slices;
+    const int cls = q / ppc;
+    int s = 2 * (q - cls * ppc) + rank;
+    const bool valid = s < per_cls;
+    if (!valid) s -= 1;
+    TileCoord t = fc_tile(a, (cls * per_cls + s) * a.f_slices + fs);
+    t.valid = valid;
+    return t;
+}
+template <bool kPair>
+__device__ __forceinline__ TileCoord fc_work(const FusedArgs &a, int item, int rank) {
+    if constexpr (kPair) return fc_tile_pair(a, item, rank);
+    else return fc_tile(a, item);
+}
 
-template <bool kTF32>
+template <bool kTF32, bool kPair>
 __global__ void __launch_bounds__(FC_THREADS, 2)
 fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                   const __grid_constant__ FusedArgs a) {
@@ -141,6 +166,12 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
+    // pair mode: cid = the pair's index, rank 0 = the MMA leader; work is strided over pairs
+    const int rank = kPair ? (int)cluster_ctarank() : 0;
+    const int cid = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int ncl = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    const bool leader = rank == 0;
+    const int fhalf = kPair ? a.FS / 2 : 0;        // B rows this CTA loads start at f0 + rank * fhalf
     const long long t_entry = clock64();
     if (a.trace && threadIdx.x == 0) {
         unsigned long long gt;
@@ -155,15 +186,21 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     if (warp == 1 && lane == 0) {
         for (int i = 0; i < a.na; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
         for (int i = 0; i < a.nb; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], kPair ? 8 : 4); }
         fence_barrier_init();
     }
     if (warp == 2) {
-        if (a.tmem_cols == 256) tmem_alloc<256>(tmem_slot);
-        else tmem_alloc<FC_TMEM_COLS>(tmem_slot);
+        if constexpr (kPair) {
+            if (a.tmem_cols == 256) tmem_alloc_pair<256>(tmem_slot);
+            else tmem_alloc_pair<FC_TMEM_COLS>(tmem_slot);
+        } else {
+            if (a.tmem_cols == 256) tmem_alloc<256>(tmem_slot);
+            else tmem_alloc<FC_TMEM_COLS>(tmem_slot);
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (kPair) cluster_sync();   // the peer's barriers exist before any TMA / arrive targets them
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) FC_TRACE(0);
@@ -174,47 +211,62 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             // ===== TMA producer: per work item, per channel chunk: 1 patch + the class's weight tiles =====
             int as = 0, bs = 0;
             uint32_t ap = 0, bp = 0;
-            if (blockIdx.x < a.num_tiles) {
+            // pair mode: both CTAs' loads complete on the LEADER's full barriers, which the leader
+            // arms with the bytes of both; each CTA waits on its own empty barriers (the leader's
+            // MMA commit multicasts to both)
+            const uint32_t xmul = kPair ? 2u : 1u;
+            if (cid < a.num_items) {
                 // weights are read-only: warm L2 with this CTA's first tiles while the previous
                 // layer (which produces X) may still be running, then wait for it
-                const TileCoord tc0 = fc_tile(a, blockIdx.x);
+                const TileCoord tc0 = fc_work<kPair>(a, cid, rank);
                 const int npre = a.resident ? a.kchunks * wtaps : min(a.nb, a.cls[tc0.cls].ntaps);
                 for (int q = 0; q < npre; ++q) {
                     const int kc = a.resident ? q / wtaps : 0, t = a.resident ? q % wtaps : a.cls[tc0.cls].tap_w[q];
-                    tma_prefetch_3d(&tmW, kc * (128 / ES), tc0.f0, t);
+                    tma_prefetch_3d(&tmW, kc * (128 / ES), tc0.f0 + rank * fhalf, t);
                 }
             }
             pdl_wait();
-            if (a.resident && blockIdx.x < a.num_tiles) {
-                // the CTA's f-slice is fixed (grid is a multiple of f_slices): load it once
-                const TileCoord tc0 = fc_tile(a, blockIdx.x);
-                mbar_arrive_expect_tx(&b_full[0], (uint32_t)(nbst * a.b_stage_bytes));
+            if (a.resident && cid < a.num_items) {
+                // the CTA's f-slice is fixed (pair count is a multiple of f_slices): load it once
+                const TileCoord tc0 = fc_work<kPair>(a, cid, rank);
+                if (leader) mbar_arrive_expect_tx(&b_full[0], xmul * (uint32_t)(nbst * a.b_stage_bytes));
                 for (int kc = 0; kc < a.kchunks; ++kc)
-                    for (int t = 0; t < wtaps; ++t)
-                        tma_load_3d(sB + (kc * wtaps + t) * a.b_stage_bytes, &tmW, &b_full[0], kc * (128 / ES), tc0.f0, t);
+                    for (int t = 0; t < wtaps; ++t) {
+                        uint8_t *dst = sB + (kc * wtaps + t) * a.b_stage_bytes;
+                        if constexpr (kPair) tma_load_3d_pair(dst, &tmW, &b_full[0], kc * (128 / ES), tc0.f0 + rank * fhalf, t);
+                        else tma_load_3d(dst, &tmW, &b_full[0], kc * (128 / ES), tc0.f0, t);
+                    }
             }
-            for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
-                const TileCoord tc = fc_tile(a, tile);
+            for (int item = cid; item < a.num_items; item += ncl) {
+                const TileCoord tc = fc_work<kPair>(a, item, rank);
                 const FusedClass &cl = a.cls[tc.cls];
                 const int ntaps = cl.ntaps;
                 // per-CTA rotation of the (chunk, tap) order spreads identical weight requests in time
-                int kc = ((int)blockIdx.x / ntaps) % a.kchunks;
+                int kc = (cid / ntaps) % a.kchunks;
                 for (int kci = 0; kci < a.kchunks; ++kci) {
                     mbar_wait(&a_empty[as], ap ^ 1);
-                    mbar_arrive_expect_tx(&a_full[as], (uint32_t)a.a_box_bytes);
-                    if (a.sw128)
-                        tma_load_4d(sA + as * a.a_stage_bytes, &tmX, &a_full[as], kc * a.BK, tc.x0 + cl.px,
-                                    tc.y0 + cl.py, tc.img);
-                    else
-                        tma_load_5d(sA + as * a.a_stage_bytes, &tmX, &a_full[as], 0, tc.x0 + cl.px, tc.y0 + cl.py,
-                                    tc.img, kc * (a.BK / CI));
+                    if (leader) mbar_arrive_expect_tx(&a_full[as], xmul * (uint32_t)a.a_box_bytes);
+                    uint8_t *dstA = sA + as * a.a_stage_bytes;
+                    if (a.sw128) {
+                        if constexpr (kPair) tma_load_4d_pair(dstA, &tmX, &a_full[as], kc * a.BK, tc.x0 + cl.px, tc.y0 + cl.py, tc.img);
+                        else tma_load_4d(dstA, &tmX, &a_full[as], kc * a.BK, tc.x0 + cl.px, tc.y0 + cl.py, tc.img);
+                    } else {
+                        if constexpr (kPair)
+                            tma_load_5d_pair(dstA, &tmX, &a_full[as], 0, tc.x0 + cl.px, tc.y0 + cl.py, tc.img, kc * (a.BK / CI));
+                        else
+                            tma_load_5d(dstA, &tmX, &a_full[as], 0, tc.x0 + cl.px, tc.y0 + cl.py, tc.img, kc * (a.BK / CI));
+                    }
                     if (++as == a.na) { as = 0; ap ^= 1; }
                     if (!a.resident) {
-                        int t = (int)blockIdx.x % ntaps;
+                        int t = cid % ntaps;
                         for (int ti = 0; ti < ntaps; ++ti) {
                             mbar_wait(&b_empty[bs], bp ^ 1);
-                            mbar_arrive_expect_tx(&b_full[bs], (uint32_t)a.b_stage_bytes);
-                            tma_load_3d(sB + bs * a.b_stage_bytes, &tmW, &b_full[bs], kc * (128 / ES), tc.f0, cl.tap_w[t]);
+                            if (leader) mbar_arrive_expect_tx(&b_full[bs], xmul * (uint32_t)a.b_stage_bytes);
+                            uint8_t *dstB = sB + bs * a.b_stage_bytes;
+                            if constexpr (kPair)
+                                tma_load_3d_pair(dstB, &tmW, &b_full[bs], kc * (128 / ES), tc.f0 + rank * fhalf, cl.tap_w[t]);
+                            else
+                                tma_load_3d(dstB, &tmW, &b_full[bs], kc * (128 / ES), tc.f0, cl.tap_w[t]);
                             if (++bs == a.nb) { bs = 0; bp ^= 1; }
                             if (++t == ntaps) t = 0;
                         }
@@ -222,13 +274,26 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                     if (++kc == a.kchunks) kc = 0;
                 }
             }
+            if constexpr (kPair) {
+                // producer tail: every stage's last release (a multicast commit from the leader)
+                // has landed before this CTA may exit
+                for (int i = 0; i < a.na; ++i) {
+                    mbar_wait(&a_empty[as], ap ^ 1);
+                    if (++as == a.na) { as = 0; ap ^= 1; }
+                }
+                if (!a.resident)
+                    for (int i = 0; i < a.nb; ++i) {
+                        mbar_wait(&b_empty[bs], bp ^ 1);
+                        if (++bs == a.nb) { bs = 0; bp ^= 1; }
+                    }
+            }
         }
-    } else if (warp == 1) {
+    } else if (warp == 1 && leader) {
         // ===== MMA issuer: D[lane, f] += Patch[lane + off(tap), c] * W'[tap, f, c] =====
         // The whole warp walks the schedule (warp-uniform values live in uniform registers); one
         // elected thread issues a whole channel chunk: taps x MT x ksteps tcgen05.mma, with
         // descriptors built as templates + 16-byte-unit address adds.
-        const uint32_t idesc = make_idesc(kTF32, 128, (uint32_t)a.FS);
+        const uint32_t idesc = make_idesc(kTF32, kPair ? 256 : 128, (uint32_t)a.FS);
         const bool sw = a.sw128 != 0;
         // A: interleaved (LBO = planar chunk stride, SBO = 128 B) or SWIZZLE_128B (SBO = 1024 B)
         const uint64_t adesc_t = sw ? (((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
@@ -250,25 +315,25 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         uint32_t ap = 0, bp = 0;
         int acc = 0;
         uint32_t accp = 0;
-        if (resident && blockIdx.x < a.num_tiles) {
+        if (resident && cid < a.num_items) {
             mbar_wait(&b_full[0], 0);
             tc_fence_after();
         }
-        for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
-            const TileCoord tc = fc_tile(a, tile);
+        for (int item = cid; item < a.num_items; item += ncl) {
+            const TileCoord tc = fc_work<kPair>(a, item, 0);
             const FusedClass &cl = a.cls[tc.cls];
             const int ntaps = cl.ntaps;
             mbar_wait(&tempty[acc], accp ^ 1);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + (uint32_t)acc * (uint32_t)MT * acc_cols;
-            int kc = ((int)blockIdx.x / ntaps) % kchunks;
-            const int t0 = (int)blockIdx.x % ntaps;
+            int kc = (cid / ntaps) % kchunks;
+            const int t0 = cid % ntaps;
             for (int kci = 0; kci < kchunks; ++kci) {
                 const int kvalid = min(BK, C - kc * BK);
                 const int ksteps = (kvalid + KI - 1) / KI;
                 mbar_wait(&a_full[as], ap);
                 tc_fence_after();
-                if (tile == (int)blockIdx.x && kci == 0 && lane == 0) FC_TRACE(1);
+                if (item == cid && kci == 0 && lane == 0) FC_TRACE(1);
                 const uint32_t a16 = sA16 + (uint32_t)as * astage16;
                 if (elect_one()) {
                     int t = t0, lbs = bs;
@@ -295,22 +360,34 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                             const uint32_t dm = d_tmem + (uint32_t)m * acc_cols;
                             if (full_k) {
 #pragma unroll
-                                for (int k = 0; k < 4; ++k)
-                                    umma<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16), bd + (uint64_t)(2 * k), idesc,
-                                                accum | (uint32_t)k);
+                                for (int k = 0; k < 4; ++k) {
+                                    if constexpr (kPair)
+                                        umma_pair<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16), bd + (uint64_t)(2 * k),
+                                                         idesc, accum | (uint32_t)k);
+                                    else
+                                        umma<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16), bd + (uint64_t)(2 * k), idesc,
+                                                    accum | (uint32_t)k);
+                                }
                             } else {
-                                for (int k = 0; k < ksteps; ++k)
-                                    umma<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16), bd + (uint64_t)(2 * k), idesc,
-                                                accum | (uint32_t)k);
+                                for (int k = 0; k < ksteps; ++k) {
+                                    if constexpr (kPair)
+                                        umma_pair<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16), bd + (uint64_t)(2 * k),
+                                                         idesc, accum | (uint32_t)k);
+                                    else
+                                        umma<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16), bd + (uint64_t)(2 * k), idesc,
+                                                    accum | (uint32_t)k);
+                                }
                             }
                         }
                         if (!resident) {
-                            umma_commit(&b_empty[lbs]);
+                            if constexpr (kPair) umma_commit_pair(&b_empty[lbs], 3);
+                            else umma_commit(&b_empty[lbs]);
                             if (++lbs == nb) { lbs = 0; lbp ^= 1; }
                         }
                         if (++t == ntaps) t = 0;
                     }
-                    umma_commit(&a_empty[as]);
+                    if constexpr (kPair) umma_commit_pair(&a_empty[as], 3);
+                    else umma_commit(&a_empty[as]);
                 }
                 __syncwarp();
                 if (!resident) {          // every lane replays the ring counters
@@ -320,9 +397,12 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                 if (++as == na) { as = 0; ap ^= 1; }
                 if (++kc == kchunks) kc = 0;
             }
-            if (elect_one()) umma_commit(&tfull[acc]);
+            if (elect_one()) {
+                if constexpr (kPair) umma_commit_pair(&tfull[acc], 3);
+                else umma_commit(&tfull[acc]);
+            }
             __syncwarp();
-            if (tile == (int)blockIdx.x && lane == 0) FC_TRACE(3);
+            if (item == cid && lane == 0) FC_TRACE(3);
             if (++acc == nbuf) { acc = 0; accp ^= 1; }
         }
     } else if (warp >= 4) {
@@ -334,14 +414,16 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         uint32_t accp = 0;
         const bool vec = (a.F % (kTF32 ? 4 : 8)) == 0;
         pdl_wait();   // Y may still be read by the previous kernel: order our stores after it
-        for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
-            const TileCoord tc = fc_tile(a, tile);
+        // pair mode: the follower's warps release the LEADER's accumulator barrier (count 8)
+        const uint32_t tempty_leader0 = kPair ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
+        for (int item = cid; item < a.num_items; item += ncl) {
+            const TileCoord tc = fc_work<kPair>(a, item, rank);
             const FusedClass &cl = a.cls[tc.cls];
             mbar_wait(&tfull[acc], accp);
             tc_fence_after();
             for (int m = 0; m < a.MT; ++m) {
                 const int oy = (tc.y0 + m * a.Yb + ly) * a.ost + cl.oy0, ox = (tc.x0 + lx) * a.ost + cl.ox0;
-                const bool valid = ly < a.Yb && lx < a.XB && oy < a.OH && ox < a.OW;
+                const bool valid = tc.valid && ly < a.Yb && lx < a.XB && oy < a.OH && ox < a.OW;
                 const int64_t pix = ((int64_t)tc.img * a.OH + oy) * a.OW + ox;
                 const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((acc * a.MT + m) * a.acc_cols);
                 // up to 64 columns per round: both TMEM loads in flight before one wait
@@ -389,20 +471,29 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-            if (threadIdx.x == 128 && tile == (int)blockIdx.x) FC_TRACE(5);
+            if (lane == 0) {
+                if constexpr (kPair) mbar_arrive_cluster(tempty_leader0 + (uint32_t)acc * 8u);
+                else mbar_arrive(&tempty[acc]);
+            }
+            if (threadIdx.x == 128 && item == cid) FC_TRACE(5);
             if (++acc == a.nbuf) { acc = 0; accp ^= 1; }
         }
         if (threadIdx.x == 128) FC_TRACE(6);
     }
 
     tc_fence_before();
-    __syncthreads();
+    if constexpr (kPair) cluster_sync();   // neither CTA leaves while the pair's MMAs / arrives may target it
+    else __syncthreads();
     if (threadIdx.x == 0) FC_TRACE(7);
     if (warp == 2) {
         tc_fence_after();
-        if (a.tmem_cols == 256) tmem_dealloc<256>(tmem_base);
-        else tmem_dealloc<FC_TMEM_COLS>(tmem_base);
+        if constexpr (kPair) {
+            if (a.tmem_cols == 256) tmem_dealloc_pair<256>(tmem_base);
+            else tmem_dealloc_pair<FC_TMEM_COLS>(tmem_base);
+        } else {
+            if (a.tmem_cols == 256) tmem_dealloc<256>(tmem_base);
+            else tmem_dealloc<FC_TMEM_COLS>(tmem_base);
+        }
     }
 }
 

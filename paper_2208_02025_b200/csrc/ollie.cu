@@ -115,6 +115,26 @@ static cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t 
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
+// Same, with thread-block clusters of `cluster_x` CTAs along x (CTA pairs for cta_group::2).
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                                  int cluster_x, Args &&...args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cluster_x;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ------------------------------------------------------------------------ TMA
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -234,6 +254,7 @@ extern "C" ollie_status ollie_merged_gemm(int64_t M, int64_t N, int64_t K, ollie
 // ------------------------------------------------------------------------ fused plan (a8)
 // Tile geometry + f-slice choice for fused_conv_kernel; see fused_conv.cuh for the design.
 static int g_force_mt = 0, g_force_fs = 0, g_force_res = -1;   // debug plan overrides (0 / -1 = auto)
+static int g_force_pair = -1;                                   // debug: -1 auto, 0 single CTAs, 1 CTA pairs
 static thread_local double g_last_fused_cost = 0, g_last_unfused_cost = 0;
 static thread_local std::vector<FusedArgs> g_last_cands;
 
@@ -344,44 +365,55 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                 if (items > INT32_MAX) continue;
                 const int64_t wbytes = (int64_t)wtaps * base.kchunks * bstage;          // whole slice
                 const int64_t tbytes = (int64_t)max_taps * base.kchunks * bstage;       // per item
+                for (int pair = 0; pair <= 1; ++pair)
                 for (int occ = 1; occ <= 2; ++occ)
                 for (int resident = 0; resident <= 1; ++resident) {
                     if (g_force_res >= 0 && resident != g_force_res) continue;
+                    if (g_force_pair >= 0 && pair != g_force_pair) continue;
+                    // pair = 1: a CTA pair computes two spatial tiles with M = 256 cta_group::2 MMAs;
+                    // each CTA holds half of every weight tile (FS / 2 rows, SW128 atoms of 8 rows)
+                    if (pair && (FS % 16 != 0 || items_sp < 2)) continue;
+                    const int bstage_c = pair ? bstage / 2 : bstage;
+                    const int64_t wbytes_c = pair ? wbytes / 2 : wbytes;
+                    const int64_t items_c = pair ? nclass * ceil_div(items_sp / nclass, 2) * slices : items;
                     // occ = 2: two CTAs per SM, each with half the smem and 256 TMEM columns
                     const int bud = occ == 1 ? budget : (113 * 1024 - 2048);
                     const int nbuf_o = occ == 1 ? nbuf : (2 * MT * acc_cols <= 256 ? 2 : 1);
                     if (occ == 2 && MT * acc_cols > 256) continue;
                     int na, nb;
                     if (resident) {
-                        if (wbytes + 2 * astage > bud) continue;
-                        na = (int)std::min<int64_t>(4, (bud - wbytes) / astage);
+                        if (wbytes_c + 2 * astage > bud) continue;
+                        na = (int)std::min<int64_t>(4, (bud - wbytes_c) / astage);
                         nb = 1;
                     } else {
-                        na = bud >= 3 * astage + 4 * bstage ? 3 : 2;
-                        nb = std::min(8, (bud - na * astage) / bstage);
+                        na = bud >= 3 * astage + 4 * bstage_c ? 3 : 2;
+                        nb = std::min(8, (bud - na * astage) / bstage_c);
                         if (nb < 2) continue;
                     }
-                    int grid = (int)std::min<int64_t>(items, (int64_t)occ * sms);
+                    // grid in work units: CTAs (single) or CTA pairs
+                    const int units = pair ? occ * sms / 2 : occ * sms;
+                    int grid = (int)std::min<int64_t>(items_c, (int64_t)units);
                     if (resident) grid = (int)std::max<int64_t>(slices, grid / slices * slices);
-                    const double per_cta = (double)ceil_div(items, grid);
+                    const double per_cta = (double)ceil_div(items_c, grid);
                     const double instr = (double)base.kchunks * max_taps * ksteps * MT;
                     const double mma = instr * std::max(FS / 2.0, 40.0 + FS / 3.0) +
                                        (resident ? 0.0 : 250.0 * base.kchunks * max_taps);
                     // TMA issues one request per box row: 16-byte planar rows stream at ~8 B/clk,
                     // 128-byte pixel rows at ~40 B/clk (tools/trace_fused.py)
                     const double ld = (double)base.kchunks * box / (sw128 ? 40.0 : 8.0) +
-                                      (resident ? 0.0 : (double)tbytes / 40.0);
+                                      (resident ? 0.0 : (double)(pair ? tbytes / 2 : tbytes) / 40.0);
                     const double epi = nbuf_o == 2 ? 0.0 : MT * (FS / 32.0) * 400.0;
                     // two co-resident CTAs share the SM's tensor core: count both CTAs' work
                     double t = per_cta * occ * (std::max(mma, ld) + epi + 600.0) / (occ == 2 ? 1.6 : 1.0);
-                    if (resident) t += (double)wbytes / 40.0;
+                    if (resident) t += (double)wbytes_c / 40.0;
                     {
                         FusedArgs a = base;
                         a.XB = XB; a.Xb = Xb; a.Yb = Yb; a.Yp = Yp; a.MT = MT;
                         a.a_box_bytes = box; a.a_stage_bytes = astage;
-                        a.FS = FS; a.acc_cols = acc_cols; a.nbuf = nbuf_o; a.b_stage_bytes = bstage;
+                        a.FS = FS; a.acc_cols = acc_cols; a.nbuf = nbuf_o; a.b_stage_bytes = bstage_c;
                         a.resident = resident; a.na = na; a.nb = nb;
                         a.tmem_cols = occ == 1 ? 512 : 256;
+                        a.pair = pair;
                         all.emplace_back(t, a);
                         if (t < best * 0.995) {
                             best = t;
@@ -402,6 +434,8 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
     a.tiles_y = (int)ceil_div(GH, (int64_t)a.Yb * a.MT);
     a.f_slices = (int)ceil_div(s->f, a.FS);
     a.num_tiles = (int)((int64_t)nclass * a.n * a.tiles_x * a.tiles_y * a.f_slices);
+    a.spatial = (int)((int64_t)nclass * a.n * a.tiles_x * a.tiles_y);
+    a.num_items = a.pair ? (int)(nclass * ceil_div(a.spatial / nclass, 2) * a.f_slices) : a.num_tiles;
     // class tables
     if (!transposed) {
         FusedClass &c = a.cls[0];
@@ -445,11 +479,11 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
     // the model's best geometry for every (MT, FS, residency, CTAs-per-SM) family, cheapest first:
     // structurally different plans the cost model cannot rank reliably are measured instead
     for (auto &c : all) {
-        if ((int)g_last_cands.size() >= 24) break;
+        if ((int)g_last_cands.size() >= 32) break;
         bool dup = false;
         for (auto &d : g_last_cands)
             dup |= d.MT == c.second.MT && d.FS == c.second.FS && d.resident == c.second.resident &&
-                   d.tmem_cols == c.second.tmem_cols;
+                   d.tmem_cols == c.second.tmem_cols && d.pair == c.second.pair;
         if (!dup && c.first < 4.0 * best) g_last_cands.push_back(finalize(c.second));
     }
     // the cost of the same layer unfused (GEMM writes T, OffsetAdd reads it back): AUTO only fuses
@@ -481,7 +515,7 @@ static std::map<PlanKey, PlanEntry> g_plan_cache;
 static PlanEntry *plan_entry_mut(const ollie_conv_shape *s, bool tf32, int transposed, int64_t OH, int64_t OW) {
     PlanKey k{{s->n, s->c, s->h, s->w, s->f, s->r * 65536 + s->s, s->pad, s->stride * 65536 + s->dilation,
                (int64_t)tf32 * 2 + transposed + 4 * (int64_t)s->output_padding, num_sms(),
-               g_force_mt * 1000 + g_force_fs, g_force_res}};
+               g_force_mt * 1000 + g_force_fs, g_force_res * 16 + g_force_pair}};
     {
         std::lock_guard<std::mutex> g(g_plan_mu);
         auto it = g_plan_cache.find(k);
@@ -506,11 +540,13 @@ static bool plan_fused(const ollie_conv_shape *s, bool tf32, int transposed, Fus
     return e.ok;
 }
 
+// CTAs launched: work units (CTAs, or CTA pairs in pair mode) x units' CTA count.
 static int fused_grid(const FusedArgs &a) {
     const int occ = a.tmem_cols == 256 ? 2 : 1;
-    int grid = (int)std::min<int64_t>(a.num_tiles, (int64_t)occ * num_sms());
-    if (a.resident) grid = std::max(a.f_slices, grid / a.f_slices * a.f_slices);   // fixed f-slice per CTA
-    return grid;
+    const int units = a.pair ? occ * num_sms() / 2 : occ * num_sms();
+    int grid = (int)std::min<int64_t>(a.num_items, (int64_t)units);
+    if (a.resident) grid = std::max(a.f_slices, grid / a.f_slices * a.f_slices);   // fixed f-slice per unit
+    return a.pair ? 2 * grid : grid;
 }
 
 static size_t fused_smem_bytes(const FusedArgs &a) {
@@ -548,9 +584,9 @@ static bool fused_preferred(const ollie_conv_shape *s, bool tf32, int transposed
     return e.ok && e.fused_cost <= e.unfused_cost;
 }
 
-template <bool TF32>
+template <bool TF32, bool PAIR>
 static ollie_status launch_fused_t(const CUtensorMap &tx, const CUtensorMap &tw, const FusedArgs &a, cudaStream_t stream) {
-    auto kern = fused_conv_kernel<TF32>;
+    auto kern = fused_conv_kernel<TF32, PAIR>;
     static bool attr_done[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -558,7 +594,10 @@ static ollie_status launch_fused_t(const CUtensorMap &tx, const CUtensorMap &tw,
         CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr_done[dev & 63] = true;
     }
-    CUDA_TRY(launch(kern, dim3(fused_grid(a)), dim3(FC_THREADS), fused_smem_bytes(a), stream, tx, tw, a));
+    if (PAIR)
+        CUDA_TRY(launch_cluster(kern, dim3(fused_grid(a)), dim3(FC_THREADS), fused_smem_bytes(a), stream, 2, tx, tw, a));
+    else
+        CUDA_TRY(launch(kern, dim3(fused_grid(a)), dim3(FC_THREADS), fused_smem_bytes(a), stream, tx, tw, a));
     return OLLIE_OK;
 }
 
@@ -593,13 +632,14 @@ static ollie_status run_fused(const ollie_conv_shape *s, bool tf32, int transpos
     {   // W' as 3-D {c, f, tap}: f >= F reads are out of bounds -> zero
         cuuint64_t dims[3] = {(cuuint64_t)s->c, (cuuint64_t)s->f, (cuuint64_t)(s->r * s->s)};
         cuuint64_t strides[2] = {(cuuint64_t)(s->c * es), (cuuint64_t)(s->f * s->c * es)};
-        cuuint32_t box[3] = {(cuuint32_t)(128 / es), (cuuint32_t)a.FS, 1};
+        cuuint32_t box[3] = {(cuuint32_t)(128 / es), (cuuint32_t)(a.pair ? a.FS / 2 : a.FS), 1};   // pair: this CTA's half
         cuuint32_t estr[3] = {1, 1, 1};
         CUresult r = enc(&tw, dt, 3, const_cast<void *>(wp), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (weights) failed (%d)", (int)r);
     }
-    return tf32 ? launch_fused_t<true>(tx, tw, a, stream) : launch_fused_t<false>(tx, tw, a, stream);
+    if (a.pair) return tf32 ? launch_fused_t<true, true>(tx, tw, a, stream) : launch_fused_t<false, true>(tx, tw, a, stream);
+    return tf32 ? launch_fused_t<true, false>(tx, tw, a, stream) : launch_fused_t<false, false>(tx, tw, a, stream);
 }
 
 // ------------------------------------------------------------------------ shapes
@@ -1303,10 +1343,10 @@ extern "C" ollie_status ollie_plan_describe(const ollie_conv_shape *s, ollie_dty
         if (!plan_fused(s, tf32, transposed, &a, OH, OW)) return fail(OLLIE_E_UNSUPPORTED, "no fused plan");
         snprintf(buf, len,
                  "fused XB=%d Yb=%d Xb=%d Yp=%d MT=%d FS=%d f_slices=%d resident=%d nbuf=%d na=%d nb=%d BK=%d "
-                 "kchunks=%d tiles=%d grid=%d smem=%zu classes=%d taps=%d sw128=%d ctas_per_sm=%d",
+                 "kchunks=%d tiles=%d grid=%d smem=%zu classes=%d taps=%d sw128=%d ctas_per_sm=%d pair=%d",
                  a.XB, a.Yb, a.Xb, a.Yp, a.MT, a.FS, a.f_slices, a.resident, a.nbuf, a.na, a.nb, a.BK, a.kchunks,
                  a.num_tiles, fused_grid(a), fused_smem_bytes(a), a.nclass, a.max_taps, a.sw128,
-                 a.tmem_cols == 256 ? 2 : 1);
+                 a.tmem_cols == 256 ? 2 : 1, a.pair);
     } else if (is_identity_offset_add(s, transposed)) {
         snprintf(buf, len, "unfused-identity gemm BN=%d (OffsetAdd eliminated)", choose_bn(s->r * s->s * s->f));
     } else {
@@ -1326,6 +1366,8 @@ extern "C" void ollie_debug_force_plan(int mt, int fs, int resident) {
     g_force_fs = fs;
     g_force_res = resident;
 }
+// Debug hook (not part of include/ollie.h): -1 auto, 0 single-CTA plans only, 1 CTA-pair plans only.
+extern "C" void ollie_debug_force_pair(int pair) { g_force_pair = pair; }
 
 // ------------------------------------------------------------------------ autotune
 extern "C" ollie_status ollie_autotune_derived(const ollie_conv_shape *s, ollie_dtype dtype, int transposed,

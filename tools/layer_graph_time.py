@@ -8,8 +8,17 @@ import ollie_synth as syn
 from paper_2208_02025_b200.layers import DerivedConv
 
 torch.backends.cudnn.benchmark = True
-cfg = sys.argv[1] if len(sys.argv) > 1 else "resnet18"
+import argparse
+ap = argparse.ArgumentParser()
+ap.add_argument("cfg", nargs="?", default="resnet18")
+ap.add_argument("--pair", type=int, default=-1, help="-1 auto, 0 single-CTA plans, 1 CTA-pair plans")
+ap.add_argument("--no-cudnn", action="store_true")
+ap.add_argument("--describe", action="store_true")
+args = ap.parse_args()
+cfg = args.cfg
 REPS = 10
+from paper_2208_02025_b200 import ollie as O
+O._lib.ollie_debug_force_pair(args.pair)
 
 
 def graph_time(fn):
@@ -43,7 +52,9 @@ for i, lay in enumerate(syn.CONFIGS[cfg]):
         fc = lambda s: F.conv_transpose2d(xc, wc, stride=lay.stride, padding=lay.pad, output_padding=lay.output_padding)
     else:
         fc = lambda s: F.conv2d(xc, wc, stride=lay.stride, padding=lay.pad, dilation=lay.dilation)
-    t_c = graph_time(fc)
+    t_c = 0.0 if args.no_cudnn else graph_time(fc)
     tot_o += t_o; tot_c += t_c
     print(f"{lay.name:24s} ours {t_o:7.2f} us   cudnn(graph) {t_c:7.2f} us   {conv.resolved_plan()}")
+    if args.describe:
+        print("    ", O.plan_describe(conv.shape, conv.code, conv.plan, conv.transposed))
 print(f"{'sum':24s} ours {tot_o:7.2f} us   cudnn(graph) {tot_c:7.2f} us")
