@@ -127,6 +127,37 @@ ollie_status ollie_convtranspose2d_derived(const ollie_conv_shape *shape, ollie_
                                            const void *x_nhwc, const void *w_prep, void *y_nhwc,
                                            void *ws, size_t ws_bytes, int plan, ollie_stream_t stream);
 
+/* ---------------------------------------------------------------------------------
+ * NEXT-3 -- element-wise epilogue fused into the kernel that writes Y ("OffsetAdd ...
+ * fused with following element-wise operators"; reading Q19):
+ *     v = acc + bias[f] + residual[n][oh][ow][f];     Y = act(v)
+ *   bias     : fp32 [f] (device) or NULL
+ *   residual : [n][OH][OW][f] in Y's storage dtype (device) or NULL; may alias y_nhwc
+ *   act      : OLLIE_ACT_NONE, OLLIE_ACT_RELU (max(v, 0)) or OLLIE_ACT_PRELU
+ *              (v > 0 ? v : alpha[f] * v)
+ *   alpha    : fp32 [f] PReLU slopes (device), required for OLLIE_ACT_PRELU
+ * Arithmetic is fp32 on the fp32 accumulator, then the usual RNE store; every plan applies it
+ * (fused epilogue, OffsetAdd / selective-add kernel, or the identity plan's GEMM epilogue).
+ * Errors: E_INVALID for an unknown act or PReLU without alpha (before any launch).
+ * ollie_*_derived_ex(..., epilogue = NULL, ...) == ollie_*_derived(...).
+ * --------------------------------------------------------------------------------- */
+enum { OLLIE_ACT_NONE = 0, OLLIE_ACT_RELU = 1, OLLIE_ACT_PRELU = 2 };
+typedef struct {
+    const float *bias;
+    const void *residual;
+    int32_t act;
+    const float *alpha;
+} ollie_epilogue;
+
+ollie_status ollie_conv2d_derived_ex(const ollie_conv_shape *shape, ollie_dtype dtype,
+                                     const void *x_nhwc, const void *w_prep, void *y_nhwc,
+                                     void *ws, size_t ws_bytes, int plan,
+                                     const ollie_epilogue *epilogue, ollie_stream_t stream);
+ollie_status ollie_convtranspose2d_derived_ex(const ollie_conv_shape *shape, ollie_dtype dtype,
+                                              const void *x_nhwc, const void *w_prep, void *y_nhwc,
+                                              void *ws, size_t ws_bytes, int plan,
+                                              const ollie_epilogue *epilogue, ollie_stream_t stream);
+
 /* Introspection: writes a one-line description of the plan `plan` resolves to for this layer
  * (kernel choice, tile geometry, f-slice, stages) into buf (NUL-terminated, truncated to len).
  * Host-only; no launch. */

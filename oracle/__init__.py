@@ -199,3 +199,23 @@ def conv_transpose2d_derived(x_nhwc, w_cfrs, pad=0, stride=1, dilation=1, output
     _, f, r, s = np.shape(w_cfrs)
     T = merged_gemm(x, weight_dlt_convt(w_cfrs))
     return selective_add(T, n, h, w, f, r, s, pad, stride, dilation, output_padding)
+
+
+# ----------------------------------------------------------------------------- NEXT-3 epilogue
+def epilogue(y, bias=None, residual=None, act: str = "none", alpha=None) -> np.ndarray:
+    """Element-wise operators following the convolution ("fused with following
+    element-wise operators"; reading Q19), written out in fp64:
+        v = y + bias[f] + residual;   relu: max(v, 0);   prelu: v if v > 0 else alpha[f] * v
+    y / residual are NHWC [n, OH, OW, f]; bias / alpha are [f]."""
+    v = _f64(y).copy()
+    if bias is not None:
+        v = v + _f64(bias)[None, None, None, :]
+    if residual is not None:
+        v = v + _f64(residual)
+    if act == "relu":
+        v = np.where(v > 0, v, 0.0)
+    elif act == "prelu":
+        v = np.where(v > 0, v, _f64(alpha)[None, None, None, :] * v)
+    elif act != "none":
+        raise ValueError(f"unknown activation {act!r}")
+    return v

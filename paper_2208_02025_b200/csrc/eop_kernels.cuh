@@ -15,6 +15,7 @@
 // before summing.  Tap order (i, j) is fixed, so results are deterministic.
 #pragma once
 #include "sm100_ptx.cuh"
+#include "epilogue.cuh"
 
 namespace ollie {
 
@@ -26,6 +27,7 @@ struct OffsetAddArgs {
     int64_t oh, ow;
     int32_t pad, stride, dil;
     int64_t items;             // n*oh*ow*(f/VEC)
+    EpiArgs epi;               // NEXT-3 element-wise epilogue
 };
 
 __device__ __forceinline__ float4 ld_stream_f4(const float *p) {
@@ -114,6 +116,7 @@ __global__ void __launch_bounds__(256) offset_add_kernel(OffsetAddArgs a) {
                 acc[0] += tv[q].x;
                 if constexpr (VEC == 4) { acc[1] += tv[q].y; acc[2] += tv[q].z; acc[3] += tv[q].w; }
             }
+            if (a.epi.on) epi_apply<kOutBF16, VEC>(a.epi, acc, px * a.f + fv * VEC, (int)(fv * VEC), VEC);
             store_y<VEC, kOutBF16>(a.y, px * a.f + fv * VEC, acc);
             continue;
         }
@@ -128,6 +131,7 @@ __global__ void __launch_bounds__(256) offset_add_kernel(OffsetAddArgs a) {
                 accum_tap<VEC>(acc, Trow + t2 * a.ldT + j * a.f);
             }
         }
+        if (a.epi.on) epi_apply<kOutBF16, VEC>(a.epi, acc, px * a.f + fv * VEC, (int)(fv * VEC), VEC);
         store_y<VEC, kOutBF16>(a.y, px * a.f + fv * VEC, acc);
     }
 }
@@ -166,6 +170,7 @@ __global__ void __launch_bounds__(256) selective_add_kernel(OffsetAddArgs a) {
                 accum_tap<VEC>(acc, Trow + iw * a.ldT + j * a.f);
             }
         }
+        if (a.epi.on) epi_apply<kOutBF16, VEC>(a.epi, acc, px * a.f + fv * VEC, (int)(fv * VEC), VEC);
         store_y<VEC, kOutBF16>(a.y, px * a.f + fv * VEC, acc);
     }
 }

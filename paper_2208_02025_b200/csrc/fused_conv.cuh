@@ -32,6 +32,7 @@
 #pragma once
 #include "../../include/ollie.h"
 #include "sm100_ptx.cuh"
+#include "epilogue.cuh"
 
 namespace ollie {
 
@@ -72,6 +73,7 @@ struct FusedArgs {
     int32_t num_items;                // work items: num_tiles (single) or ceil(spatial / 2) * f_slices (pair)
     int32_t spatial;                  // spatial tiles = nclass * n * tiles_y * tiles_x
     void *y;
+    EpiArgs epi;                      // NEXT-3 element-wise epilogue (bias / residual / ReLU / PReLU)
     long long *trace;                 // debug only (nullptr in production): per-CTA timestamps
     FusedClass cls[FC_MAX_CLASSES];
 };
@@ -436,6 +438,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                     const int f = tc.f0 + c0;
                     if (!valid || f >= a.F) continue;
                     const int nf = min(min(64, a.FS - c0), a.F - f);
+                    if (a.epi.on) epi_apply_bits<!kTF32, 64>(a.epi, v, pix * a.F + f, f, nf);
                     if constexpr (kTF32) {
                         float *yp = reinterpret_cast<float *>(a.y) + pix * a.F + f;
                         const int nv = vec ? (nf & ~3) : 0;      // whole 16-byte groups, then a scalar tail

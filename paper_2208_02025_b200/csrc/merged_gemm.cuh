@@ -14,6 +14,7 @@
 // minimise N-tail waste.  M / N / K tails are handled by TMA zero fill and store guards.
 #pragma once
 #include "sm100_ptx.cuh"
+#include "epilogue.cuh"
 
 namespace ollie {
 
@@ -37,6 +38,7 @@ struct GemmArgs {
     int32_t BN;          // UMMA N of a tile
     void *out;           // fp32 or bf16, row-major with leading dimension ldo
     int64_t ldo;
+    EpiArgs epi;         // element-wise epilogue (identity plan only: out is Y, column = channel)
 };
 
 template <bool kTF32, bool kOutBF16>
@@ -169,6 +171,8 @@ merged_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
                 tmem_ld_wait();
                 if (row >= M) continue;
                 const int nc = (int)min((int64_t)64, col_end - (col_base + c0));
+                if (args.epi.on)
+                    epi_apply_bits<kOutBF16, 64>(args.epi, v, row * args.ldo + col_base + c0, (int)(col_base + c0), nc);
                 if constexpr (kOutBF16) {
                     uint16_t *o = reinterpret_cast<uint16_t *>(args.out) + row * args.ldo + col_base + c0;
                     {

@@ -221,7 +221,7 @@ static ollie_status launch_gemm_t(const CUtensorMap &ta, const CUtensorMap &tb, 
 
 // out = A[M,K] * B[N,K]^T ; out fp32 (out_bf16 = false) or bf16, leading dim ldo.
 static ollie_status run_gemm(int64_t M, int64_t N, int64_t K, bool tf32, const void *A, const void *B, void *out,
-                             int64_t ldo, bool out_bf16, cudaStream_t stream) {
+                             int64_t ldo, bool out_bf16, cudaStream_t stream, const EpiArgs *epi = nullptr) {
     const size_t es = tf32 ? 4 : 2;
     if ((K * es) % 16 != 0)
         return fail(OLLIE_E_ALIGN, "K*sizeof(elem) = %lld is not a multiple of 16 (TMA rule); pad channels",
@@ -236,7 +236,7 @@ static ollie_status run_gemm(int64_t M, int64_t N, int64_t K, bool tf32, const v
     if (st != OLLIE_OK) return st;
     st = make_tmap_2d(&tb, B, tf32, (uint64_t)K, (uint64_t)N, (uint64_t)(K * es), BK, (uint32_t)BN);
     if (st != OLLIE_OK) return st;
-    GemmArgs ga{M, N, K, BN, out, ldo};
+    GemmArgs ga{M, N, K, BN, out, ldo, epi ? *epi : EpiArgs{}};
     if (tf32) return out_bf16 ? launch_gemm_t<true, true>(ta, tb, ga, stream) : launch_gemm_t<true, false>(ta, tb, ga, stream);
     return out_bf16 ? launch_gemm_t<false, true>(ta, tb, ga, stream) : launch_gemm_t<false, false>(ta, tb, ga, stream);
 }
@@ -604,10 +604,11 @@ static ollie_status launch_fused_t(const CUtensorMap &tx, const CUtensorMap &tw,
 static long long *g_fc_trace = nullptr;   // debug timeline buffer (ollie_debug_set_trace), off by default
 
 static ollie_status run_fused(const ollie_conv_shape *s, bool tf32, int transposed, const void *x, const void *wp,
-                              void *y, int64_t OH, int64_t OW, cudaStream_t stream) {
+                              void *y, int64_t OH, int64_t OW, cudaStream_t stream, const EpiArgs *epi = nullptr) {
     FusedArgs a;
     if (!plan_fused(s, tf32, transposed, &a, OH, OW)) return fail(OLLIE_E_UNSUPPORTED, "no fused plan for this shape");
     a.y = y;
+    a.epi = epi ? *epi : EpiArgs{};
     a.trace = g_fc_trace;
     PFN_encodeTiled enc = get_encode();
     if (!enc) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
@@ -714,8 +715,9 @@ extern "C" ollie_status ollie_prepare_weight_convtranspose2d(const ollie_conv_sh
 
 // ------------------------------------------------------------------------ a3 / a4 standalone
 static ollie_status run_offset_add(const ollie_conv_shape *s, int transposed, const float *T, int64_t ldT, bool out_bf16,
-                                   void *y, int64_t OH, int64_t OW, cudaStream_t stream) {
+                                   void *y, int64_t OH, int64_t OW, cudaStream_t stream, const EpiArgs *epi = nullptr) {
     OffsetAddArgs a;
+    a.epi = epi ? *epi : EpiArgs{};
     a.T = T;
     a.ldT = ldT;
     a.y = y;
@@ -779,10 +781,28 @@ extern "C" size_t ollie_workspace_bytes(const ollie_conv_shape *s, ollie_dtype d
     return (size_t)(s->n * s->h * s->w) * (size_t)ldT_of(s) * sizeof(float);
 }
 
+// NEXT-3 epilogue descriptor -> device form (validated before any launch).
+static ollie_status make_epi(const ollie_epilogue *e, EpiArgs *out) {
+    *out = EpiArgs{};
+    if (!e) return OLLIE_OK;
+    if (e->act < OLLIE_ACT_NONE || e->act > OLLIE_ACT_PRELU) return fail(OLLIE_E_INVALID, "unknown activation %d", e->act);
+    if (e->act == OLLIE_ACT_PRELU && !e->alpha) return fail(OLLIE_E_INVALID, "PReLU needs alpha[f]");
+    out->bias = e->bias;
+    out->res = e->residual;
+    out->alpha = e->alpha;
+    out->act = e->act;
+    out->on = (e->bias || e->residual || e->act != OLLIE_ACT_NONE) ? 1 : 0;
+    return OLLIE_OK;
+}
+
 static ollie_status derived_layer(const ollie_conv_shape *s, ollie_dtype dtype, const void *x, const void *wp, void *y,
-                                  void *ws, size_t ws_bytes, int plan, cudaStream_t stream, int transposed) {
+                                  void *ws, size_t ws_bytes, int plan, cudaStream_t stream, int transposed,
+                                  const ollie_epilogue *epilogue = nullptr) {
     int64_t OH, OW;
     ollie_status st = check_shape(s, transposed, &OH, &OW);
+    if (st != OLLIE_OK) return st;
+    EpiArgs epi;
+    st = make_epi(epilogue, &epi);
     if (st != OLLIE_OK) return st;
     if (dtype != OLLIE_BF16 && dtype != OLLIE_TF32) return fail(OLLIE_E_UNSUPPORTED, "dtype must be BF16 or TF32");
     if (transposed && s->dilation != 1) return fail(OLLIE_E_UNSUPPORTED, "ConvTranspose2d with dilation != 1");
@@ -797,12 +817,12 @@ static ollie_status derived_layer(const ollie_conv_shape *s, ollie_dtype dtype, 
     if (rp == OLLIE_PLAN_FUSED) {
         if (!fused_supported(s, tf32, transposed))
             return fail(OLLIE_E_UNSUPPORTED, "fused plan not available for this shape/dtype");
-        st = run_fused(s, tf32, transposed, x, wp, y, OH, OW, stream);
+        st = run_fused(s, tf32, transposed, x, wp, y, OH, OW, stream, &epi);
         return st == OLLIE_OK ? ok() : st;
     }
     if (is_identity_offset_add(s, transposed)) {
         // a6: identity eOperator eliminated -- the GEMM writes Y = X W'^T directly.
-        st = run_gemm(M, N, K, tf32, x, wp, y, N, !tf32, stream);
+        st = run_gemm(M, N, K, tf32, x, wp, y, N, !tf32, stream, &epi);
         return st == OLLIE_OK ? ok() : st;
     }
     const int64_t ldT = ldT_of(s);
@@ -812,7 +832,7 @@ static ollie_status derived_layer(const ollie_conv_shape *s, ollie_dtype dtype, 
     if (!aligned16(ws)) return fail(OLLIE_E_ALIGN, "workspace must be 16-byte aligned");
     st = run_gemm(M, N, K, tf32, x, wp, ws, ldT, false, stream);
     if (st != OLLIE_OK) return st;
-    st = run_offset_add(s, transposed, (const float *)ws, ldT, !tf32, y, OH, OW, stream);
+    st = run_offset_add(s, transposed, (const float *)ws, ldT, !tf32, y, OH, OW, stream, &epi);
     return st == OLLIE_OK ? ok() : st;
 }
 
@@ -825,6 +845,17 @@ extern "C" ollie_status ollie_convtranspose2d_derived(const ollie_conv_shape *sh
                                                       const void *x_nhwc, const void *w_prep, void *y_nhwc, void *ws,
                                                       size_t ws_bytes, int plan, ollie_stream_t stream) {
     return derived_layer(shape, dtype, x_nhwc, w_prep, y_nhwc, ws, ws_bytes, plan, (cudaStream_t)stream, 1);
+}
+extern "C" ollie_status ollie_conv2d_derived_ex(const ollie_conv_shape *shape, ollie_dtype dtype, const void *x_nhwc,
+                                                const void *w_prep, void *y_nhwc, void *ws, size_t ws_bytes, int plan,
+                                                const ollie_epilogue *epilogue, ollie_stream_t stream) {
+    return derived_layer(shape, dtype, x_nhwc, w_prep, y_nhwc, ws, ws_bytes, plan, (cudaStream_t)stream, 0, epilogue);
+}
+extern "C" ollie_status ollie_convtranspose2d_derived_ex(const ollie_conv_shape *shape, ollie_dtype dtype,
+                                                         const void *x_nhwc, const void *w_prep, void *y_nhwc, void *ws,
+                                                         size_t ws_bytes, int plan, const ollie_epilogue *epilogue,
+                                                         ollie_stream_t stream) {
+    return derived_layer(shape, dtype, x_nhwc, w_prep, y_nhwc, ws, ws_bytes, plan, (cudaStream_t)stream, 1, epilogue);
 }
 
 // ------------------------------------------------------------------------ eOperators

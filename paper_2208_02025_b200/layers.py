@@ -61,15 +61,26 @@ class DerivedConv:
     def new_output(self):
         return torch.empty(self.out_shape(), dtype=_TORCH[self.dtype], device=self.device)
 
-    def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None, stream=None, *, bias=None, residual=None,
+                 act: int = _o.ACT_NONE, alpha=None) -> torch.Tensor:
+        """Y = act(conv(x) + bias[f] + residual) -- the element-wise epilogue (NEXT-3) runs
+        inside whichever kernel writes Y; bias / alpha are fp32 [f], residual is NHWC like Y."""
         if y is None:
             y = self.new_output()
+        epi = None
+        if bias is not None or residual is not None or act != _o.ACT_NONE:
+            epi = _o.make_epilogue(bias, residual, act, alpha)
         if self.autotune and not self._tuned:
             # first call: pick the plan by measurement (P:1220); not during graph capture
             if not torch.cuda.is_current_stream_capturing():
-                _o.autotune_derived(self.shape, self.code, self.transposed, x, self.w_prep, y, self.ws,
-                                    self.ws_bytes, stream)
+                # candidates write a scratch output: y may alias the residual (in-place epilogue)
+                _o.autotune_derived(self.shape, self.code, self.transposed, x, self.w_prep, self.new_output(),
+                                    self.ws, self.ws_bytes, stream)
                 self._tuned = True
-        fn = _o.convtranspose2d_derived if self.transposed else _o.conv2d_derived
-        fn(self.shape, self.code, x, self.w_prep, y, self.ws, self.ws_bytes, self.plan, stream)
+        if epi is None:
+            fn = _o.convtranspose2d_derived if self.transposed else _o.conv2d_derived
+            fn(self.shape, self.code, x, self.w_prep, y, self.ws, self.ws_bytes, self.plan, stream)
+        else:
+            fn = _o.convtranspose2d_derived_ex if self.transposed else _o.conv2d_derived_ex
+            fn(self.shape, self.code, x, self.w_prep, y, self.ws, self.ws_bytes, self.plan, epi, stream)
         return y

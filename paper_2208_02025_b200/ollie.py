@@ -27,6 +27,7 @@ PLAN_AUTO, PLAN_FUSED, PLAN_UNFUSED = 0, 1, 2
 ATOM_ITER, ATOM_FLOORDIV, ATOM_MOD = 0, 1, 2
 OP_PUSH_ACCESS, OP_PUSH_CONST, OP_ADD, OP_MUL, OP_SUB, OP_NEG, OP_MAX, OP_MIN = range(8)
 MAX_DIMS, MAX_TERMS, MAX_ACCESS, MAX_INSTR, MAX_INPUTS = 8, 8, 8, 32, 8
+ACT_NONE, ACT_RELU, ACT_PRELU = 0, 1, 2
 
 
 class ConvShape(Structure):
@@ -69,6 +70,10 @@ class Eop(Structure):
                 ("n_scopes", c_int32), ("scope", Scope * 2)]
 
 
+class Epilogue(Structure):
+    _fields_ = [("bias", c_void_p), ("residual", c_void_p), ("act", c_int32), ("alpha", c_void_p)]
+
+
 class EopInfo(Structure):
     _fields_ = [("is_identity", c_int32), ("pure_indexing", c_int32), ("out_elems", c_int64),
                 ("bytes_in", c_int64), ("bytes_out", c_int64)]
@@ -88,6 +93,10 @@ _sig = {
                                      c_int, c_void_p]),
     "ollie_convtranspose2d_derived": (c_int, [_P(ConvShape), c_int, c_void_p, c_void_p, c_void_p, c_void_p,
                                               c_size_t, c_int, c_void_p]),
+    "ollie_conv2d_derived_ex": (c_int, [_P(ConvShape), c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
+                                        c_int, _P(Epilogue), c_void_p]),
+    "ollie_convtranspose2d_derived_ex": (c_int, [_P(ConvShape), c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+                                                 c_size_t, c_int, _P(Epilogue), c_void_p]),
     "ollie_plan_describe": (c_int, [_P(ConvShape), c_int, c_int, c_int, c_char_p, c_size_t]),
     "ollie_autotune_derived": (c_int, [_P(ConvShape), c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
                                        c_size_t, c_void_p, _P(c_float)]),
@@ -190,6 +199,26 @@ def convtranspose2d_derived(shape: ConvShape, dtype: int, x, w_prep, y, ws=None,
     _check(_lib.ollie_convtranspose2d_derived(ctypes.byref(shape), dtype, _ptr(x), _ptr(w_prep), _ptr(y),
                                               _ptr(ws), ws_bytes, plan, _stream(stream)),
            "ollie_convtranspose2d_derived")
+
+
+def make_epilogue(bias=None, residual=None, act: int = ACT_NONE, alpha=None) -> Epilogue:
+    """NEXT-3 epilogue descriptor: Y = act(acc + bias[f] + residual); tensors must outlive the call."""
+    return Epilogue(_ptr(bias), _ptr(residual), int(act), _ptr(alpha))
+
+
+def conv2d_derived_ex(shape: ConvShape, dtype: int, x, w_prep, y, ws=None, ws_bytes: int = 0,
+                      plan: int = PLAN_AUTO, epilogue: Epilogue | None = None, stream=None):
+    _check(_lib.ollie_conv2d_derived_ex(ctypes.byref(shape), dtype, _ptr(x), _ptr(w_prep), _ptr(y), _ptr(ws),
+                                        ws_bytes, plan, ctypes.byref(epilogue) if epilogue is not None else None,
+                                        _stream(stream)), "ollie_conv2d_derived_ex")
+
+
+def convtranspose2d_derived_ex(shape: ConvShape, dtype: int, x, w_prep, y, ws=None, ws_bytes: int = 0,
+                               plan: int = PLAN_AUTO, epilogue: Epilogue | None = None, stream=None):
+    _check(_lib.ollie_convtranspose2d_derived_ex(ctypes.byref(shape), dtype, _ptr(x), _ptr(w_prep), _ptr(y),
+                                                 _ptr(ws), ws_bytes, plan,
+                                                 ctypes.byref(epilogue) if epilogue is not None else None,
+                                                 _stream(stream)), "ollie_convtranspose2d_derived_ex")
 
 
 def plan_describe(shape: ConvShape, dtype: int, plan: int = PLAN_AUTO, transposed: bool = False) -> str:
