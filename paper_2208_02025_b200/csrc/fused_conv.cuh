@@ -39,15 +39,18 @@ namespace ollie {
 constexpr int FC_THREADS = 256;
 constexpr uint32_t FC_TMEM_COLS = 512;
 constexpr int FC_SMEM_BUDGET = 225 * 1024;
-constexpr int FC_MAX_CLASSES = 4;
+constexpr int FC_MAX_CLASSES = 9;            // table entries: ConvT output classes x strided-conv input phases
 constexpr int FC_MAX_TAPS = 32;
 
-struct FusedClass {
+struct FusedClass {                   // one (output class, input phase) table entry
     int32_t ntaps;
     int32_t oy0, ox0;                 // output residue (ConvT) -- 0 for Conv2d
-    int32_t py, px;                   // patch origin relative to the tile origin (input pixels)
+    int32_t py, px;                   // patch origin: input pixel ist * (tile origin) + (py, px)
+    int32_t wi0, wj0;                 // first kernel row / col of the entry's taps (weight box origin)
+    int32_t ngroups;                  // weight boxes per step: kernel-row groups of grb rows
+    int32_t bres;                     // resident layout: tile offset of the entry's boxes in a channel chunk
     uint16_t tap_off[FC_MAX_TAPS];    // row offset of the tap inside the patch (16-byte rows)
-    uint8_t tap_w[FC_MAX_TAPS];       // weight tap index i*S + j in W'
+    uint8_t tap_pos[FC_MAX_TAPS];     // tile position in the entry's box grid: k * nsb + l (sorted)
 };
 
 struct FusedArgs {
@@ -55,13 +58,19 @@ struct FusedArgs {
     int32_t OH, OW;
     int32_t ost;                      // output stride: 1 (Conv2d) or st (ConvTranspose2d classes)
     int32_t nclass, max_taps;
+    int32_t nph;                      // input phases per class (strided Conv2d: nonempty residues of i*dil-pad mod st)
+    int32_t ist;                      // input stride of the patch (TMA element stride): st for Conv2d, 1 for ConvT
     int32_t XB, Yb, Xb, Yp;           // output cols / rows per tile, patch width / rows
     int32_t tiles_x, tiles_y, f_slices, FS, num_tiles;
     int32_t kchunks, BK;              // channel chunks of BK elements
     int32_t a_box_bytes;              // bytes TMA writes per patch load
     int32_t a_stage_bytes;            // patch stage stride in smem (box + slack, 1024-aligned)
     int32_t lbo;                      // planar chunk stride (bytes) = Yp*Xb*16
-    int32_t b_stage_bytes;            // FS * 128
+    int32_t b_tile_bytes;             // one tap's weight tile: FS (pair: FS / 2) rows x 128 B
+    int32_t b_stage_bytes;            // one weight box = box_tiles tiles
+    int32_t nsb, grb, westr;          // weight box: nsb kernel cols x grb kernel rows, element stride westr
+    int32_t box_tiles;                // nsb * grb
+    int32_t kc_tiles;                 // resident tiles per channel chunk (all entries' boxes)
     int32_t na, nb;                   // ring depths
     int32_t MT;                       // M-tiles stacked vertically per work item
     int32_t resident;                 // 1: the CTA's whole weight slice stays in smem (loaded once)
@@ -153,11 +162,11 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int wtaps = a.R * a.S;                                    // weight taps (resident layout)
-    const int nbst = a.resident ? wtaps * a.kchunks : a.nb;         // B buffers
+    // B region: nb streamed boxes, or (resident) kchunks x kc_tiles weight tiles loaded once
+    const int b_region = a.resident ? a.kchunks * a.kc_tiles * a.b_tile_bytes : a.nb * a.b_stage_bytes;
     uint8_t *sA = smem;
     uint8_t *sB = sA + a.na * a.a_stage_bytes;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sB + nbst * a.b_stage_bytes);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sB + b_region);
     uint64_t *a_full = bars;
     uint64_t *a_empty = a_full + a.na;
     uint64_t *b_full = a_empty + a.na;      // [nb]   (resident: b_full[0] = "all weights loaded")
@@ -221,59 +230,72 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                 // weights are read-only: warm L2 with this CTA's first tiles while the previous
                 // layer (which produces X) may still be running, then wait for it
                 const TileCoord tc0 = fc_work<kPair>(a, cid, rank);
-                const int npre = a.resident ? a.kchunks * wtaps : min(a.nb, a.cls[tc0.cls].ntaps);
-                for (int q = 0; q < npre; ++q) {
-                    const int kc = a.resident ? q / wtaps : 0, t = a.resident ? q % wtaps : a.cls[tc0.cls].tap_w[q];
-                    tma_prefetch_3d(&tmW, kc * (128 / ES), tc0.f0 + rank * fhalf, t);
-                }
+                const int nent = a.resident ? a.nclass * a.nph : a.nph;
+                const int ebase = a.resident ? 0 : tc0.cls * a.nph;
+                for (int kc = 0; kc < (a.resident ? a.kchunks : 1); ++kc)
+                    for (int e = 0; e < nent; ++e) {
+                        const FusedClass &en = a.cls[ebase + e];
+                        for (int g = 0; g < en.ngroups; ++g)
+                            tma_prefetch_4d(&tmW, kc * (128 / ES), tc0.f0 + rank * fhalf, en.wj0, en.wi0 + g * a.grb * a.westr);
+                    }
             }
             pdl_wait();
             if (a.resident && cid < a.num_items) {
                 // the CTA's f-slice is fixed (pair count is a multiple of f_slices): load it once
                 const TileCoord tc0 = fc_work<kPair>(a, cid, rank);
-                if (leader) mbar_arrive_expect_tx(&b_full[0], xmul * (uint32_t)(nbst * a.b_stage_bytes));
+                if (leader) mbar_arrive_expect_tx(&b_full[0], xmul * (uint32_t)b_region);
+                // one TMA box per (chunk, entry, kernel-row group): few, large copies (a CTA's TMA
+                // ops are ~serialised at ~275 cycles each, tools/tma_bench.cu)
                 for (int kc = 0; kc < a.kchunks; ++kc)
-                    for (int t = 0; t < wtaps; ++t) {
-                        uint8_t *dst = sB + (kc * wtaps + t) * a.b_stage_bytes;
-                        if constexpr (kPair) tma_load_3d_pair(dst, &tmW, &b_full[0], kc * (128 / ES), tc0.f0 + rank * fhalf, t);
-                        else tma_load_3d(dst, &tmW, &b_full[0], kc * (128 / ES), tc0.f0, t);
+                    for (int e = 0; e < a.nclass * a.nph; ++e) {
+                        const FusedClass &en = a.cls[e];
+                        for (int g = 0; g < en.ngroups; ++g) {
+                            uint8_t *dst = sB + (kc * a.kc_tiles + en.bres + g * a.box_tiles) * a.b_tile_bytes;
+                            const int wi = en.wi0 + g * a.grb * a.westr;
+                            if constexpr (kPair)
+                                tma_load_4d_pair(dst, &tmW, &b_full[0], kc * (128 / ES), tc0.f0 + rank * fhalf, en.wj0, wi);
+                            else
+                                tma_load_4d(dst, &tmW, &b_full[0], kc * (128 / ES), tc0.f0, en.wj0, wi);
+                        }
                     }
             }
             for (int item = cid; item < a.num_items; item += ncl) {
                 const TileCoord tc = fc_work<kPair>(a, item, rank);
-                const FusedClass &cl = a.cls[tc.cls];
-                const int ntaps = cl.ntaps;
-                // per-CTA rotation of the (chunk, tap) order spreads identical weight requests in time
-                int kc = (cid / ntaps) % a.kchunks;
-                for (int kci = 0; kci < a.kchunks; ++kci) {
+                // steps (kc, ph): channel chunk kc of input phase ph -- one patch, that phase's taps.
+                // A per-CTA rotation of the step and tap order spreads identical weight requests in time.
+                const int nq = a.kchunks * a.nph;
+                int q = (cid / a.max_taps) % nq;
+                for (int qi = 0; qi < nq; ++qi) {
+                    const int kc = q / a.nph;
+                    const FusedClass &cl = a.cls[tc.cls * a.nph + (q - kc * a.nph)];
+                    const int xin = a.ist * tc.x0 + cl.px, yin = a.ist * tc.y0 + cl.py;
                     mbar_wait(&a_empty[as], ap ^ 1);
                     if (leader) mbar_arrive_expect_tx(&a_full[as], xmul * (uint32_t)a.a_box_bytes);
                     uint8_t *dstA = sA + as * a.a_stage_bytes;
                     if (a.sw128) {
-                        if constexpr (kPair) tma_load_4d_pair(dstA, &tmX, &a_full[as], kc * a.BK, tc.x0 + cl.px, tc.y0 + cl.py, tc.img);
-                        else tma_load_4d(dstA, &tmX, &a_full[as], kc * a.BK, tc.x0 + cl.px, tc.y0 + cl.py, tc.img);
+                        if constexpr (kPair) tma_load_4d_pair(dstA, &tmX, &a_full[as], kc * a.BK, xin, yin, tc.img);
+                        else tma_load_4d(dstA, &tmX, &a_full[as], kc * a.BK, xin, yin, tc.img);
                     } else {
                         if constexpr (kPair)
-                            tma_load_5d_pair(dstA, &tmX, &a_full[as], 0, tc.x0 + cl.px, tc.y0 + cl.py, tc.img, kc * (a.BK / CI));
+                            tma_load_5d_pair(dstA, &tmX, &a_full[as], 0, xin, yin, tc.img, kc * (a.BK / CI));
                         else
-                            tma_load_5d(dstA, &tmX, &a_full[as], 0, tc.x0 + cl.px, tc.y0 + cl.py, tc.img, kc * (a.BK / CI));
+                            tma_load_5d(dstA, &tmX, &a_full[as], 0, xin, yin, tc.img, kc * (a.BK / CI));
                     }
                     if (++as == a.na) { as = 0; ap ^= 1; }
                     if (!a.resident) {
-                        int t = cid % ntaps;
-                        for (int ti = 0; ti < ntaps; ++ti) {
+                        for (int g = 0; g < cl.ngroups; ++g) {
                             mbar_wait(&b_empty[bs], bp ^ 1);
                             if (leader) mbar_arrive_expect_tx(&b_full[bs], xmul * (uint32_t)a.b_stage_bytes);
                             uint8_t *dstB = sB + bs * a.b_stage_bytes;
+                            const int wi = cl.wi0 + g * a.grb * a.westr;
                             if constexpr (kPair)
-                                tma_load_3d_pair(dstB, &tmW, &b_full[bs], kc * (128 / ES), tc.f0 + rank * fhalf, cl.tap_w[t]);
+                                tma_load_4d_pair(dstB, &tmW, &b_full[bs], kc * (128 / ES), tc.f0 + rank * fhalf, cl.wj0, wi);
                             else
-                                tma_load_3d(dstB, &tmW, &b_full[bs], kc * (128 / ES), tc.f0, cl.tap_w[t]);
+                                tma_load_4d(dstB, &tmW, &b_full[bs], kc * (128 / ES), tc.f0, cl.wj0, wi);
                             if (++bs == a.nb) { bs = 0; bp ^= 1; }
-                            if (++t == ntaps) t = 0;
                         }
                     }
-                    if (++kc == a.kchunks) kc = 0;
+                    if (++q == nq) q = 0;
                 }
             }
             if constexpr (kPair) {
@@ -310,6 +332,8 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         const uint32_t kstep16 = sw ? 2u : 2u * lbo16;                  // one K=16|8 step, 16-byte units
         const uint32_t sA16 = smem_u32(sA) >> 4, sB16 = smem_u32(sB) >> 4;
         const uint32_t astage16 = (uint32_t)a.a_stage_bytes >> 4, bstage16 = (uint32_t)a.b_stage_bytes >> 4;
+        const uint32_t btile16 = (uint32_t)a.b_tile_bytes >> 4;
+        const int box_tiles = a.box_tiles, kc_tiles = a.kc_tiles;
         const int MT = a.MT, nb = a.nb, na = a.na, kchunks = a.kchunks, nbuf = a.nbuf, BK = a.BK, C = a.C;
         const uint32_t acc_cols = (uint32_t)a.acc_cols;
         const bool resident = a.resident != 0;
@@ -323,86 +347,86 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         }
         for (int item = cid; item < a.num_items; item += ncl) {
             const TileCoord tc = fc_work<kPair>(a, item, 0);
-            const FusedClass &cl = a.cls[tc.cls];
-            const int ntaps = cl.ntaps;
             mbar_wait(&tempty[acc], accp ^ 1);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + (uint32_t)acc * (uint32_t)MT * acc_cols;
-            int kc = (cid / ntaps) % kchunks;
-            const int t0 = cid % ntaps;
-            for (int kci = 0; kci < kchunks; ++kci) {
+            const int nph = a.nph, nq = kchunks * nph;
+            int q = (cid / a.max_taps) % nq;
+            for (int qi = 0; qi < nq; ++qi) {
+                const int kc = q / nph;
+                const FusedClass &cl = a.cls[tc.cls * nph + (q - kc * nph)];
+                const int ntaps = cl.ntaps;
                 const int kvalid = min(BK, C - kc * BK);
                 const int ksteps = (kvalid + KI - 1) / KI;
                 mbar_wait(&a_full[as], ap);
                 tc_fence_after();
-                if (item == cid && kci == 0 && lane == 0) FC_TRACE(1);
+                if (item == cid && qi == 0 && lane == 0) FC_TRACE(1);
                 const uint32_t a16 = sA16 + (uint32_t)as * astage16;
-                if (elect_one()) {
-                    int t = t0, lbs = bs;
-                    uint32_t lbp = bp;
+                {
+                    // the whole (converged) warp walks the taps with warp-uniform values; only the
+                    // tcgen05.mma / commit instructions are issued by one elected lane.  Taps come in
+                    // weight boxes (kernel-row groups): one wait / commit per box.
+                    int t = 0;
                     const bool full_k = ksteps == 4;
-                    for (int ti = 0; ti < ntaps; ++ti) {
-                        uint32_t b16;
+                    for (int g = 0; g < cl.ngroups; ++g) {
+                        uint32_t gb16;
                         if (resident) {
-                            b16 = sB16 + (uint32_t)(kc * (a.R * a.S) + cl.tap_w[t]) * bstage16;
+                            gb16 = sB16 + (uint32_t)(kc * kc_tiles + cl.bres + g * box_tiles) * btile16;
                         } else {
-                            mbar_wait(&b_full[lbs], lbp);
+                            mbar_wait(&b_full[bs], bp);
                             tc_fence_after();
-                            b16 = sB16 + (uint32_t)lbs * bstage16;
+                            gb16 = sB16 + (uint32_t)bs * bstage16;
                         }
-                        const uint32_t at16 = a16 + (uint32_t)cl.tap_off[t] * rowb16;
-                        const uint64_t bd = bdesc_t | (uint64_t)(b16 & 0x3FFF);
-                        const uint32_t accum = (uint32_t)(kci | ti);
-                        for (int m = 0; m < MT; ++m) {
-                            const uint32_t am16 = at16 + (uint32_t)m * mstride16;
-                            // SWIZZLE_128B rows may start anywhere inside a 1024-byte atom: the tensor
-                            // core XORs with absolute smem address bits, exactly as TMA wrote them, so
-                            // the descriptor's base-offset field stays 0 (verified on B200 by parity)
-                            const uint64_t adm = adesc_t | (uint64_t)(am16 & 0x3FFF);
-                            const uint32_t dm = d_tmem + (uint32_t)m * acc_cols;
-                            if (full_k) {
+                        const int pend = (g + 1) * box_tiles;
+                        for (; t < ntaps && (int)cl.tap_pos[t] < pend; ++t) {
+                            const uint32_t b16 = gb16 + (uint32_t)((int)cl.tap_pos[t] - g * box_tiles) * btile16;
+                            const uint32_t at16 = a16 + (uint32_t)cl.tap_off[t] * rowb16;
+                            const uint64_t bd = bdesc_t | (uint64_t)(b16 & 0x3FFF);
+                            const uint32_t accum = (uint32_t)(qi | t);
+                            for (int m = 0; m < MT; ++m) {
+                                const uint32_t am16 = at16 + (uint32_t)m * mstride16;
+                                // SWIZZLE_128B rows may start anywhere inside a 1024-byte atom: the tensor
+                                // core XORs with absolute smem address bits, exactly as TMA wrote them, so
+                                // the descriptor's base-offset field stays 0 (verified on B200 by parity)
+                                const uint64_t adm = adesc_t | (uint64_t)(am16 & 0x3FFF);
+                                const uint32_t dm = d_tmem + (uint32_t)m * acc_cols;
+                                if (full_k) {
 #pragma unroll
-                                for (int k = 0; k < 4; ++k) {
-                                    if constexpr (kPair)
-                                        umma_pair<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16), bd + (uint64_t)(2 * k),
-                                                         idesc, accum | (uint32_t)k);
-                                    else
-                                        umma<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16), bd + (uint64_t)(2 * k), idesc,
-                                                    accum | (uint32_t)k);
-                                }
-                            } else {
-                                for (int k = 0; k < ksteps; ++k) {
-                                    if constexpr (kPair)
-                                        umma_pair<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16), bd + (uint64_t)(2 * k),
-                                                         idesc, accum | (uint32_t)k);
-                                    else
-                                        umma<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16), bd + (uint64_t)(2 * k), idesc,
-                                                    accum | (uint32_t)k);
+                                    for (int k = 0; k < 4; ++k) {
+                                        if constexpr (kPair)
+                                            umma_pair_elect<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16),
+                                                                   bd + (uint64_t)(2 * k), idesc, accum | (uint32_t)k);
+                                        else
+                                            umma_elect<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16),
+                                                              bd + (uint64_t)(2 * k), idesc, accum | (uint32_t)k);
+                                    }
+                                } else {
+                                    for (int k = 0; k < ksteps; ++k) {
+                                        if constexpr (kPair)
+                                            umma_pair_elect<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16),
+                                                                   bd + (uint64_t)(2 * k), idesc, accum | (uint32_t)k);
+                                        else
+                                            umma_elect<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16),
+                                                              bd + (uint64_t)(2 * k), idesc, accum | (uint32_t)k);
+                                    }
                                 }
                             }
                         }
                         if (!resident) {
-                            if constexpr (kPair) umma_commit_pair(&b_empty[lbs], 3);
-                            else umma_commit(&b_empty[lbs]);
-                            if (++lbs == nb) { lbs = 0; lbp ^= 1; }
+                            if constexpr (kPair) umma_commit_pair_elect(&b_empty[bs], 3);
+                            else umma_commit_elect(&b_empty[bs]);
+                            if (++bs == nb) { bs = 0; bp ^= 1; }
                         }
-                        if (++t == ntaps) t = 0;
                     }
-                    if constexpr (kPair) umma_commit_pair(&a_empty[as], 3);
-                    else umma_commit(&a_empty[as]);
+                    if constexpr (kPair) umma_commit_pair_elect(&a_empty[as], 3);
+                    else umma_commit_elect(&a_empty[as]);
                 }
                 __syncwarp();
-                if (!resident) {          // every lane replays the ring counters
-                    bs += ntaps;
-                    while (bs >= nb) { bs -= nb; bp ^= 1; }
-                }
                 if (++as == na) { as = 0; ap ^= 1; }
-                if (++kc == kchunks) kc = 0;
+                if (++q == nq) q = 0;
             }
-            if (elect_one()) {
-                if constexpr (kPair) umma_commit_pair(&tfull[acc], 3);
-                else umma_commit(&tfull[acc]);
-            }
+            if constexpr (kPair) umma_commit_pair_elect(&tfull[acc], 3);
+            else umma_commit_elect(&tfull[acc]);
             __syncwarp();
             if (item == cid && lane == 0) FC_TRACE(3);
             if (++acc == nbuf) { acc = 0; accp ^= 1; }
@@ -420,7 +444,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         const uint32_t tempty_leader0 = kPair ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
         for (int item = cid; item < a.num_items; item += ncl) {
             const TileCoord tc = fc_work<kPair>(a, item, rank);
-            const FusedClass &cl = a.cls[tc.cls];
+            const FusedClass &cl = a.cls[tc.cls * a.nph];
             mbar_wait(&tfull[acc], accp);
             tc_fence_after();
             for (int m = 0; m < a.MT; ++m) {

@@ -274,22 +274,94 @@ static void class_geom(const ollie_conv_shape *s, int a, int b, ClassGeom *g) {
     g->cb = (b + s->pad - g->j0) / st;
 }
 
+// Strided Conv2d input phases (NEXT-2, expression splitting by input residue): tap i reads
+// input row st*(oy + q_i) + rho_i with i*dil - pad = st*q_i + rho_i, 0 <= rho_i < st, so the taps
+// of one residue (rho_y, rho_x) are a stride-1 convolution over the subsampled image
+// X_rho[u][v] = X[st*u + rho_y][st*v + rho_x] -- which TMA loads directly with element stride st.
+// Stride 1 gives one phase with q_i = i*dil - pad (the plain haloed patch).
+static int floordiv_i(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
+struct PhaseGeom {
+    int nph, qmin_y, qmin_x, span_y, span_x, max_taps, westr;
+    int rho_y[FC_MAX_CLASSES], rho_x[FC_MAX_CLASSES], ntaps[FC_MAX_CLASSES];
+    int nr[FC_MAX_CLASSES], ns[FC_MAX_CLASSES], wi0[FC_MAX_CLASSES], wj0[FC_MAX_CLASSES];
+};
+static int gcd_i(int a, int b) { while (b) { int t = a % b; a = b; b = t; } return a; }
+static bool conv_phases(const ollie_conv_shape *s, PhaseGeom *g) {
+    const int st = s->stride, dil = s->dilation, pad = s->pad;
+    if (st * st > FC_MAX_CLASSES) return false;
+    int qy0 = INT32_MAX, qy1 = INT32_MIN, qx0 = INT32_MAX, qx1 = INT32_MIN;
+    for (int i = 0; i < s->r; ++i) {
+        const int q = floordiv_i(i * dil - pad, st);
+        qy0 = std::min(qy0, q); qy1 = std::max(qy1, q);
+    }
+    for (int j = 0; j < s->s; ++j) {
+        const int q = floordiv_i(j * dil - pad, st);
+        qx0 = std::min(qx0, q); qx1 = std::max(qx1, q);
+    }
+    g->qmin_y = qy0; g->qmin_x = qx0; g->span_y = qy1 - qy0; g->span_x = qx1 - qx0;
+    g->westr = st / gcd_i(st, dil);
+    g->nph = 0; g->max_taps = 0;
+    for (int ry = 0; ry < st; ++ry)
+        for (int rx = 0; rx < st; ++rx) {
+            int n = 0;
+            for (int i = 0; i < s->r; ++i)
+                for (int j = 0; j < s->s; ++j)
+                    if (i * dil - pad - st * floordiv_i(i * dil - pad, st) == ry &&
+                        j * dil - pad - st * floordiv_i(j * dil - pad, st) == rx)
+                        ++n;
+            if (n == 0) continue;                       // residue no tap reads: no load, no work
+            if (n > FC_MAX_TAPS) return false;
+            // the phase's kernel rows / cols are arithmetic progressions of step st / gcd(st, dil)
+            int nr = 0, ns = 0, i0 = -1, j0 = -1;
+            for (int i = 0; i < s->r; ++i)
+                if (i * dil - pad - st * floordiv_i(i * dil - pad, st) == ry) { if (i0 < 0) i0 = i; ++nr; }
+            for (int j = 0; j < s->s; ++j)
+                if (j * dil - pad - st * floordiv_i(j * dil - pad, st) == rx) { if (j0 < 0) j0 = j; ++ns; }
+            g->nr[g->nph] = nr; g->ns[g->nph] = ns; g->wi0[g->nph] = i0; g->wj0[g->nph] = j0;
+            g->rho_y[g->nph] = ry; g->rho_x[g->nph] = rx; g->ntaps[g->nph] = n;
+            g->max_taps = std::max(g->max_taps, n);
+            ++g->nph;
+        }
+    return g->nph > 0;
+}
+
+static int nb_cap() {   // B ring depth cap (OLLIE_NB_MAX overrides, for experiments)
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("OLLIE_NB_MAX");
+        v = e ? std::max(2, std::min(32, atoi(e))) : 8;
+    }
+    return v;
+}
+
 static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transposed, FusedArgs *out, int64_t OH,
                               int64_t OW) {
     const int es = tf32 ? 4 : 2;
     if ((s->c * es) % 16 != 0) return false;
     if (s->n > INT32_MAX || s->h > 32768 || s->w > 32768 || s->c > 65535 || s->f > 65535) return false;
     FusedArgs base{};
-    int span_y, span_x, max_taps, nclass;
+    int span_y, span_x, max_taps, nclass, taps_item;
     int64_t GH, GW;                               // class-grid (tile space) extent
+    PhaseGeom pg{};
+    // weight-box geometry of every table entry (class x phase): kernel rows / cols it reads
+    int nent = 0, ent_nr[FC_MAX_CLASSES], ent_ns[FC_MAX_CLASSES];
+    int westr = 1;
     if (!transposed) {
-        if (s->stride != 1 || s->r * s->s > FC_MAX_TAPS) return false;
-        span_y = (int)((s->r - 1) * s->dilation);
-        span_x = (int)((s->s - 1) * s->dilation);
-        max_taps = (int)(s->r * s->s);
+        if (!conv_phases(s, &pg)) return false;
+        span_y = pg.span_y;
+        span_x = pg.span_x;
+        max_taps = pg.max_taps;
+        taps_item = (int)(s->r * s->s);             // every tap once per item, over all phases
         nclass = 1;
         GH = OH; GW = OW;
         base.ost = 1;
+        base.ist = s->stride;
+        base.nph = pg.nph;
+        westr = pg.westr;
+        for (int ph = 0; ph < pg.nph; ++ph) {
+            ent_nr[ph] = pg.nr[ph]; ent_ns[ph] = pg.ns[ph];
+        }
+        nent = pg.nph;
     } else {
         const int st = s->stride;
         if (s->dilation != 1 || st * st > FC_MAX_CLASSES) return false;
@@ -300,6 +372,8 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                 ClassGeom g;
                 class_geom(s, a, b, &g);
                 if (g.ntaps_r == 0 || g.ntaps_s == 0) return false;      // class of pure zeros: not fused
+                ent_nr[nent] = g.ntaps_r; ent_ns[nent] = g.ntaps_s;
+                ++nent;
                 kr = std::max(kr, g.ntaps_r);
                 ks = std::max(ks, g.ntaps_s);
                 max_taps = std::max(max_taps, g.ntaps_r * g.ntaps_s);
@@ -308,9 +382,32 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
         span_y = kr - 1;
         span_x = ks - 1;
         nclass = st * st;
+        taps_item = max_taps;
         GH = ceil_div(OH, st); GW = ceil_div(OW, st);
         base.ost = st;
+        base.ist = 1;
+        base.nph = 1;
+        westr = st;
     }
+    const int ist = base.ist, nph = base.nph;
+    int nsb = 0, max_rows = 0;
+    for (int e = 0; e < nent; ++e) { nsb = std::max(nsb, ent_ns[e]); max_rows = std::max(max_rows, ent_nr[e]); }
+    if ((nsb - 1) * westr + 1 > 256 || (max_rows - 1) * westr + 1 > 256) return false;
+    // weight boxes of grb kernel rows: tiles per channel chunk (resident) and boxes per item step
+    auto box_geom = [&](int grb, int *kc_tiles, int *ops_item) {
+        int tiles = 0, ops_max = 0;
+        for (int c0 = 0; c0 < nclass; ++c0) {
+            int ops = 0;
+            for (int ph = 0; ph < nph; ++ph) {
+                const int e = c0 * nph + ph, ng = (ent_nr[e] + grb - 1) / grb;
+                tiles += ng * nsb * grb;
+                ops += ng;
+            }
+            ops_max = std::max(ops_max, ops);
+        }
+        *kc_tiles = tiles;
+        *ops_item = ops_max;
+    };
     const int CI = 16 / es, KI = 32 / es, BKfull = 128 / es;
     base.n = (int)s->n; base.H = (int)s->h; base.W = (int)s->w; base.C = (int)s->c; base.F = (int)s->f;
     base.R = (int)s->r; base.S = (int)s->s; base.pad = s->pad; base.dil = s->dilation;
@@ -321,7 +418,6 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
     const int nchunk = base.BK / CI;
     const bool sw128 = base.BK * es == 128;      // full 128-byte channel chunks: SWIZZLE_128B pixel rows
     const int rowbytes = sw128 ? 128 : 16;
-    const int wtaps = (int)(s->r * s->s);
     const int ksteps = base.BK / KI;
     const int sms = num_sms();
     const int64_t Fp = ceil_div(s->f, 16) * 16;
@@ -335,7 +431,7 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
     std::vector<std::pair<double, FusedArgs>> all;   // every evaluated plan (autotune candidates)
     for (int XB = (int)std::min<int64_t>(GW, 128); XB >= 1; --XB) {
         const int Xb = XB + span_x;
-        if (Xb > 256) continue;
+        if (Xb * ist > 256) continue;                // TMA box: <= 256 traversed elements
         const int Yb = (int)std::min<int64_t>(GH, (128 - XB) / Xb + 1);
         if (Yb < 1) continue;
         if (XB < std::min<int64_t>(GW, 128) && ceil_div(GW, XB) == ceil_div(GW, XB + 1) &&
@@ -345,7 +441,7 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
             if (g_force_mt > 0 && MT != g_force_mt) continue;
             if (MT > 1 && (int64_t)(MT - 1) * Yb >= GH) break;
             const int Yp = MT * Yb + span_y;
-            if (Yp > 256) break;
+            if (Yp * ist > 256) break;
             const int max_off = span_y * Xb + span_x + (MT - 1) * Yb * Xb;
             if (max_off >= 65536) break;
             const int box = 16 * Xb * Yp * nchunk;   // same bytes in both layouts
@@ -363,8 +459,6 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                 const int64_t slices = ceil_div(s->f, FS);
                 const int64_t items = items_sp * slices;
                 if (items > INT32_MAX) continue;
-                const int64_t wbytes = (int64_t)wtaps * base.kchunks * bstage;          // whole slice
-                const int64_t tbytes = (int64_t)max_taps * base.kchunks * bstage;       // per item
                 for (int pair = 0; pair <= 1; ++pair)
                 for (int occ = 1; occ <= 2; ++occ)
                 for (int resident = 0; resident <= 1; ++resident) {
@@ -373,44 +467,59 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                     // pair = 1: a CTA pair computes two spatial tiles with M = 256 cta_group::2 MMAs;
                     // each CTA holds half of every weight tile (FS / 2 rows, SW128 atoms of 8 rows)
                     if (pair && (FS % 16 != 0 || items_sp < 2)) continue;
-                    const int bstage_c = pair ? bstage / 2 : bstage;
-                    const int64_t wbytes_c = pair ? wbytes / 2 : wbytes;
+                    const int btile = pair ? bstage / 2 : bstage;      // one tap's tile in this CTA
                     const int64_t items_c = pair ? nclass * ceil_div(items_sp / nclass, 2) * slices : items;
                     // occ = 2: two CTAs per SM, each with half the smem and 256 TMEM columns
                     const int bud = occ == 1 ? budget : (113 * 1024 - 2048);
                     const int nbuf_o = occ == 1 ? nbuf : (2 * MT * acc_cols <= 256 ? 2 : 1);
                     if (occ == 2 && MT * acc_cols > 256) continue;
-                    int na, nb;
-                    if (resident) {
-                        if (wbytes_c + 2 * astage > bud) continue;
-                        na = (int)std::min<int64_t>(4, (bud - wbytes_c) / astage);
-                        nb = 1;
-                    } else {
-                        na = bud >= 3 * astage + 4 * bstage_c ? 3 : 2;
-                        nb = std::min(8, (bud - na * astage) / bstage_c);
-                        if (nb < 2) continue;
+                    // largest weight box (fewest TMA ops) that fits: grb kernel rows per box
+                    int na = 0, nb = 0, grb = 0, kc_tiles = 0, ops_item = 0;
+                    for (int g = max_rows; g >= 1; --g) {
+                        int kt, oi;
+                        box_geom(g, &kt, &oi);
+                        const int bst = nsb * g * btile;
+                        if (resident) {
+                            const int64_t wb = (int64_t)base.kchunks * kt * btile;
+                            if (wb + 2 * astage > bud) continue;
+                            na = (int)std::min<int64_t>(4, (bud - wb) / astage);
+                            nb = 1;
+                        } else {
+                            na = bud >= 3 * astage + 2 * bst ? 3 : 2;
+                            nb = std::min(nb_cap(), (bud - na * astage) / bst);
+                            if (nb < 2) continue;
+                        }
+                        grb = g; kc_tiles = kt; ops_item = oi;
+                        break;
                     }
+                    if (grb == 0) continue;
+                    const int bstage_c = nsb * grb * btile;
                     // grid in work units: CTAs (single) or CTA pairs
                     const int units = pair ? occ * sms / 2 : occ * sms;
                     int grid = (int)std::min<int64_t>(items_c, (int64_t)units);
                     if (resident) grid = (int)std::max<int64_t>(slices, grid / slices * slices);
                     const double per_cta = (double)ceil_div(items_c, grid);
-                    const double instr = (double)base.kchunks * max_taps * ksteps * MT;
-                    const double mma = instr * std::max(FS / 2.0, 40.0 + FS / 3.0) +
-                                       (resident ? 0.0 : 250.0 * base.kchunks * max_taps);
-                    // TMA issues one request per box row: 16-byte planar rows stream at ~8 B/clk,
-                    // 128-byte pixel rows at ~40 B/clk (tools/trace_fused.py)
-                    const double ld = (double)base.kchunks * box / (sw128 ? 40.0 : 8.0) +
-                                      (resident ? 0.0 : (double)(pair ? tbytes / 2 : tbytes) / 40.0);
+                    // Measured on B200 (tools/mma_bench2.cu, tools/tma_bench.cu): a 128xNx16 MMA costs
+                    // max(61, N/2) cycles; a CTA's TMA ops run ~one at a time at max(275, bytes/103)
+                    // cycles (16-byte planar patch rows: ~8 B/clk); a weight-box handshake ~100 cycles.
+                    const double instr = (double)base.kchunks * taps_item * ksteps * MT;
+                    const double mma = instr * std::max(61.0, FS / 2.0) +
+                                       (resident ? 0.0 : 100.0 * base.kchunks * ops_item);
+                    const double a_op = sw128 ? std::max(275.0, box / 103.0) : std::max(275.0, box / 8.0);
+                    const double b_op = std::max(275.0, bstage_c / 103.0);
+                    const double ld = (double)base.kchunks * nph * a_op + (resident ? 0.0 : (double)base.kchunks * ops_item * b_op);
                     const double epi = nbuf_o == 2 ? 0.0 : MT * (FS / 32.0) * 400.0;
-                    // two co-resident CTAs share the SM's tensor core: count both CTAs' work
-                    double t = per_cta * occ * (std::max(mma, ld) + epi + 600.0) / (occ == 2 ? 1.6 : 1.0);
-                    if (resident) t += (double)wbytes_c / 40.0;
+                    // co-resident CTAs share the SM's tensor core but each has its own TMA stream
+                    double t = per_cta * (std::max(occ * mma, ld) + epi + 600.0);
+                    if (resident) t += (double)base.kchunks * (kc_tiles / (nsb * grb)) * b_op;
+                    if (pair) t *= 1.1;   // measured: pairs rarely beat single CTAs on these layers (autotune decides)
                     {
                         FusedArgs a = base;
                         a.XB = XB; a.Xb = Xb; a.Yb = Yb; a.Yp = Yp; a.MT = MT;
                         a.a_box_bytes = box; a.a_stage_bytes = astage;
                         a.FS = FS; a.acc_cols = acc_cols; a.nbuf = nbuf_o; a.b_stage_bytes = bstage_c;
+                        a.b_tile_bytes = btile; a.nsb = nsb; a.grb = grb; a.westr = westr;
+                        a.box_tiles = nsb * grb; a.kc_tiles = kc_tiles;
                         a.resident = resident; a.na = na; a.nb = nb;
                         a.tmem_cols = occ == 1 ? 512 : 256;
                         a.pair = pair;
@@ -438,17 +547,25 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
     a.num_items = a.pair ? (int)(nclass * ceil_div(a.spatial / nclass, 2) * a.f_slices) : a.num_tiles;
     // class tables
     if (!transposed) {
-        FusedClass &c = a.cls[0];
-        c.ntaps = max_taps;
-        c.oy0 = c.ox0 = 0;
-        c.py = -s->pad;
-        c.px = -s->pad;
-        for (int i = 0; i < s->r; ++i)
-            for (int j = 0; j < s->s; ++j) {
-                const int t = (int)(i * s->s + j);
-                c.tap_off[t] = (uint16_t)((i * a.Xb + j) * s->dilation);
-                c.tap_w[t] = (uint8_t)t;
-            }
+        const int st = s->stride, dil = s->dilation;
+        for (int ph = 0; ph < pg.nph; ++ph) {
+            FusedClass &c = a.cls[ph];
+            c.ntaps = 0;
+            c.oy0 = c.ox0 = 0;
+            c.py = st * pg.qmin_y + pg.rho_y[ph];      // full-resolution input coordinates
+            c.px = st * pg.qmin_x + pg.rho_x[ph];
+            c.wi0 = pg.wi0[ph];
+            c.wj0 = pg.wj0[ph];
+            for (int i = 0; i < s->r; ++i)
+                for (int j = 0; j < s->s; ++j) {
+                    const int ei = (int)(i * dil - s->pad), ej = (int)(j * dil - s->pad);
+                    const int qi = floordiv_i(ei, st), qj = floordiv_i(ej, st);
+                    if (ei - st * qi != pg.rho_y[ph] || ej - st * qj != pg.rho_x[ph]) continue;
+                    c.tap_off[c.ntaps] = (uint16_t)((qi - pg.qmin_y) * a.Xb + (qj - pg.qmin_x));
+                    c.tap_pos[c.ntaps] = (uint8_t)(((i - c.wi0) / a.westr) * a.nsb + (j - c.wj0) / a.westr);
+                    ++c.ntaps;
+                }
+        }
     } else {
         const int st = s->stride;
         for (int ca = 0; ca < st; ++ca)
@@ -461,13 +578,25 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                 c.ox0 = cb;
                 c.py = g.ca - (g.ntaps_r - 1);
                 c.px = g.cb - (g.ntaps_s - 1);
+                c.wi0 = g.i0;
+                c.wj0 = g.j0;
                 for (int k = 0; k < g.ntaps_r; ++k)
                     for (int l = 0; l < g.ntaps_s; ++l) {
                         const int t = k * g.ntaps_s + l;
                         c.tap_off[t] = (uint16_t)((g.ntaps_r - 1 - k) * a.Xb + (g.ntaps_s - 1 - l));
-                        c.tap_w[t] = (uint8_t)((g.i0 + st * k) * s->s + (g.j0 + st * l));
+                        c.tap_pos[t] = (uint8_t)(k * a.nsb + l);
                     }
             }
+    }
+    // weight boxes: groups of grb kernel rows per entry, resident tile offsets
+    {
+        int bres = 0;
+        for (int e = 0; e < nent; ++e) {
+            FusedClass &c = a.cls[e];
+            c.ngroups = (ent_nr[e] + a.grb - 1) / a.grb;
+            c.bres = bres;
+            bres += c.ngroups * a.box_tiles;
+        }
     }
     return a;
     };
@@ -550,8 +679,8 @@ static int fused_grid(const FusedArgs &a) {
 }
 
 static size_t fused_smem_bytes(const FusedArgs &a) {
-    const size_t nbst = a.resident ? (size_t)a.R * a.S * a.kchunks : (size_t)a.nb;
-    return 1024 + (size_t)a.na * a.a_stage_bytes + nbst * a.b_stage_bytes + 1024;
+    const size_t b_region = a.resident ? (size_t)a.kchunks * a.kc_tiles * a.b_tile_bytes : (size_t)a.nb * a.b_stage_bytes;
+    return 1024 + (size_t)a.na * a.a_stage_bytes + b_region + 1024;
 }
 
 static bool out_hw(const ollie_conv_shape *s, int transposed, int64_t *OH, int64_t *OW) {
@@ -615,27 +744,39 @@ static ollie_status run_fused(const ollie_conv_shape *s, bool tf32, int transpos
     const int es = tf32 ? 4 : 2, CI = 16 / es;
     const CUtensorMapDataType dt = tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     CUtensorMap tx, tw;
+    // strided Conv2d: the patch is the subsampled image of one input phase, traversed with element
+    // stride ist along w and h (ist * Xb traversed elements load Xb pixels)
+    const uint32_t ist = (uint32_t)a.ist;
     if (a.sw128) {   // X as 4-D NHWC {c, w, h, n}, box = 128-byte pixel rows, SWIZZLE_128B
-        ollie_status st4 = make_tmap_nhwc(&tx, x, tf32, s->n, s->h, s->w, s->c, (uint32_t)a.BK, (uint32_t)a.Xb,
-                                          (uint32_t)a.Yp, 1);
-        if (st4 != OLLIE_OK) return st4;
+        cuuint64_t dims[4] = {(cuuint64_t)s->c, (cuuint64_t)s->w, (cuuint64_t)s->h, (cuuint64_t)s->n};
+        cuuint64_t strides[3] = {(cuuint64_t)(s->c * es), (cuuint64_t)(s->w * s->c * es),
+                                 (cuuint64_t)(s->h * s->w * s->c * es)};
+        cuuint32_t box[4] = {(cuuint32_t)a.BK, (cuuint32_t)(a.Xb * ist), (cuuint32_t)(a.Yp * ist), 1};
+        cuuint32_t estr[4] = {1, ist, ist, 1};
+        CUresult r = enc(&tx, dt, 4, const_cast<void *>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (patch 4d) failed (%d)", (int)r);
     } else {   // X as 5-D planar view {c_in (16 B), w, h, n, c_out}
         cuuint64_t dims[5] = {(cuuint64_t)CI, (cuuint64_t)s->w, (cuuint64_t)s->h, (cuuint64_t)s->n,
                               (cuuint64_t)(s->c / CI)};
         cuuint64_t strides[4] = {(cuuint64_t)(s->c * es), (cuuint64_t)(s->w * s->c * es),
                                  (cuuint64_t)(s->h * s->w * s->c * es), 16};
-        cuuint32_t box[5] = {(cuuint32_t)CI, (cuuint32_t)a.Xb, (cuuint32_t)a.Yp, 1, (cuuint32_t)(a.BK / CI)};
-        cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+        cuuint32_t box[5] = {(cuuint32_t)CI, (cuuint32_t)(a.Xb * ist), (cuuint32_t)(a.Yp * ist), 1, (cuuint32_t)(a.BK / CI)};
+        cuuint32_t estr[5] = {1, ist, ist, 1, 1};
         CUresult r = enc(&tx, dt, 5, const_cast<void *>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (patch) failed (%d)", (int)r);
     }
-    {   // W' as 3-D {c, f, tap}: f >= F reads are out of bounds -> zero
-        cuuint64_t dims[3] = {(cuuint64_t)s->c, (cuuint64_t)s->f, (cuuint64_t)(s->r * s->s)};
-        cuuint64_t strides[2] = {(cuuint64_t)(s->c * es), (cuuint64_t)(s->f * s->c * es)};
-        cuuint32_t box[3] = {(cuuint32_t)(128 / es), (cuuint32_t)(a.pair ? a.FS / 2 : a.FS), 1};   // pair: this CTA's half
-        cuuint32_t estr[3] = {1, 1, 1};
-        CUresult r = enc(&tw, dt, 3, const_cast<void *>(wp), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    {   // W' as 4-D {c, f, j, i} (tap = i*S + j): one box = nsb x grb taps of an entry, kernel rows /
+        // cols element-strided by westr (ConvT class / strided-conv phase); f >= F and taps past the
+        // kernel are out of bounds -> zero
+        cuuint64_t dims[4] = {(cuuint64_t)s->c, (cuuint64_t)s->f, (cuuint64_t)s->s, (cuuint64_t)s->r};
+        cuuint64_t strides[3] = {(cuuint64_t)(s->c * es), (cuuint64_t)(s->f * s->c * es),
+                                 (cuuint64_t)(s->s * s->f * s->c * es)};
+        cuuint32_t box[4] = {(cuuint32_t)(128 / es), (cuuint32_t)(a.pair ? a.FS / 2 : a.FS),   // pair: this CTA's half
+                             (cuuint32_t)((a.nsb - 1) * a.westr + 1), (cuuint32_t)((a.grb - 1) * a.westr + 1)};
+        cuuint32_t estr[4] = {1, 1, (cuuint32_t)a.westr, (cuuint32_t)a.westr};
+        CUresult r = enc(&tw, dt, 4, const_cast<void *>(wp), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (weights) failed (%d)", (int)r);
     }
@@ -1374,10 +1515,11 @@ extern "C" ollie_status ollie_plan_describe(const ollie_conv_shape *s, ollie_dty
         if (!plan_fused(s, tf32, transposed, &a, OH, OW)) return fail(OLLIE_E_UNSUPPORTED, "no fused plan");
         snprintf(buf, len,
                  "fused XB=%d Yb=%d Xb=%d Yp=%d MT=%d FS=%d f_slices=%d resident=%d nbuf=%d na=%d nb=%d BK=%d "
-                 "kchunks=%d tiles=%d grid=%d smem=%zu classes=%d taps=%d sw128=%d ctas_per_sm=%d pair=%d",
+                 "kchunks=%d tiles=%d grid=%d smem=%zu classes=%d phases=%d ist=%d taps=%d sw128=%d ctas_per_sm=%d "
+                 "pair=%d wbox=%dx%d",
                  a.XB, a.Yb, a.Xb, a.Yp, a.MT, a.FS, a.f_slices, a.resident, a.nbuf, a.na, a.nb, a.BK, a.kchunks,
-                 a.num_tiles, fused_grid(a), fused_smem_bytes(a), a.nclass, a.max_taps, a.sw128,
-                 a.tmem_cols == 256 ? 2 : 1, a.pair);
+                 a.num_tiles, fused_grid(a), fused_smem_bytes(a), a.nclass, a.nph, a.ist, a.max_taps, a.sw128,
+                 a.tmem_cols == 256 ? 2 : 1, a.pair, a.grb, a.nsb);
     } else if (is_identity_offset_add(s, transposed)) {
         snprintf(buf, len, "unfused-identity gemm BN=%d (OffsetAdd eliminated)", choose_bn(s->r * s->s * s->f));
     } else {

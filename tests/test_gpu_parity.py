@@ -161,6 +161,37 @@ def test_derived_layer_random_tolerance(O, lay, plan):
     assert _max_rel(got, _oracle_layer(lay, x, w)) <= TOL[lay.dtype]
 
 
+# NEXT-2: strided Conv2d on the fused path (input-phase split, TMA element strides): zero-waste
+STRIDED = [
+    syn.Layer("s2_3x3_p1", 2, 64, 14, 14, 128, 3, 3, pad=1, stride=2),
+    syn.Layer("s2_3x3_odd", 1, 64, 15, 13, 64, 3, 3, pad=1, stride=2),
+    syn.Layer("s2_1x1_down", 2, 64, 14, 14, 128, 1, 1, pad=0, stride=2),
+    syn.Layer("s2_5x5_p2", 1, 32, 17, 19, 48, 5, 5, pad=2, stride=2),
+    syn.Layer("s3_3x3", 1, 64, 20, 23, 32, 3, 3, pad=1, stride=3),
+    syn.Layer("s2_dil2", 1, 64, 16, 16, 64, 3, 3, pad=2, stride=2, dilation=2),
+    syn.Layer("s2_planar_c16", 2, 16, 21, 18, 40, 3, 3, pad=1, stride=2),
+    syn.Layer("s2_tf32", 1, 36, 12, 10, 24, 3, 3, pad=1, stride=2, dtype="tf32"),
+    syn.Layer("s2_7x7_p3_c8", 1, 8, 32, 30, 64, 7, 7, pad=3, stride=2),
+    syn.Layer("s2_big_c256", 2, 256, 14, 14, 512, 3, 3, pad=1, stride=2),
+]
+
+
+@pytest.mark.parametrize("lay", STRIDED, ids=[l.name for l in STRIDED])
+def test_strided_fused_integer_exact(O, lay):
+    x, w = syn.layer_inputs(lay, 400, exact_int=True)
+    got = _run_layer(O, lay, x, w, O.PLAN_FUSED)
+    ref = _oracle_layer(lay, x, w)
+    assert got.shape == ref.shape
+    assert np.array_equal(got, _round_like(ref, lay.dtype))
+
+
+@pytest.mark.parametrize("lay", STRIDED, ids=[l.name for l in STRIDED])
+def test_strided_fused_random_tolerance(O, lay):
+    x, w = syn.layer_inputs(lay, 401)
+    got = _run_layer(O, lay, x, w, O.PLAN_FUSED)
+    assert _max_rel(got, _oracle_layer(lay, x, w)) <= TOL[lay.dtype]
+
+
 def _configured():
     out = []
     for name in ("motivating", "resnet18", "resnet18_s2", "csrnet", "infogan", "dcgan", "paper_conv3x3"):

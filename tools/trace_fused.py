@@ -19,8 +19,14 @@ from dataclasses import replace as _rep
 from paper_2208_02025_b200.stack import padded_channels
 lay = _rep(lay, c=padded_channels(lay.c, lay.dtype), f=padded_channels(lay.f, lay.dtype) if cfg == 'fsrcnn' and li < 7 else lay.f)
 x, w = syn.layer_inputs(lay, 1)
-conv = DerivedConv.from_layer(lay, plan=1).prepare(w.cuda())
+auto = "auto" in sys.argv[3:]
+kv = dict(a.split("=") for a in sys.argv[3:] if "=" in a and not a.startswith("flags="))
+O._lib.ollie_debug_force_plan(int(kv.get("mt", 0)), int(kv.get("fs", 0)), int(kv.get("res", -1)))
+O._lib.ollie_debug_force_pair(int(kv.get("pair", -1)))
+conv = DerivedConv.from_layer(lay, plan=0 if auto else 1).prepare(w.cuda())
 xd = x.cuda()
+if auto:
+    conv(xd)          # autotune; the trace then follows the tuned plan
 tr = torch.zeros(148 * 32 * 4, dtype=torch.int64, device="cuda")
 O._lib.ollie_debug_set_trace.argtypes = [ctypes.c_void_p]
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
