@@ -49,8 +49,11 @@ struct FusedClass {                   // one (output class, input phase) table e
     int32_t wi0, wj0;                 // first kernel row / col of the entry's taps (weight box origin)
     int32_t ngroups;                  // weight boxes per step: kernel-row groups of grb rows
     int32_t bres;                     // resident layout: tile offset of the entry's boxes in a channel chunk
-    uint16_t tap_off[FC_MAX_TAPS];    // row offset of the tap inside the patch (16-byte rows)
-    uint8_t tap_pos[FC_MAX_TAPS];     // tile position in the entry's box grid: k * nsb + l (sorted)
+    // The entry's taps form a grid (k, l) < (nr, ns): kernel row wi0 + westr*k, col wj0 + westr*l.
+    // Tap (k, l) reads patch row a_base + k*a_dk + l*a_dl and weight tile k*nsb + l of the box grid
+    // (affine, so the MMA issue loop needs no per-tap table lookups).
+    int32_t nr, ns;
+    int32_t a_base, a_dk, a_dl;
 };
 
 struct FusedArgs {
@@ -152,7 +155,7 @@ __device__ __forceinline__ TileCoord fc_work(const FusedArgs &a, int item, int r
     else return fc_tile(a, item);
 }
 
-template <bool kTF32, bool kPair>
+template <bool kTF32, bool kPair, bool kOneEntry>
 __global__ void __launch_bounds__(FC_THREADS, 2)
 fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                   const __grid_constant__ FusedArgs a) {
@@ -175,7 +178,10 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
-    const int warp = threadIdx.x / 32;
+    // warp index via a lane-0 broadcast: ptxas then knows the role branches are warp-uniform and
+    // keeps the MMA issuer on the uniform datapath (plain tid/32 made every issue operand go
+    // through R2UR: ~90 instead of ~48 cycles per N=64 MMA)
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0);
     const int lane = threadIdx.x & 31;
     // pair mode: cid = the pair's index, rank 0 = the MMA leader; work is strided over pairs
     const int rank = kPair ? (int)cluster_ctarank() : 0;
@@ -333,7 +339,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         const uint32_t sA16 = smem_u32(sA) >> 4, sB16 = smem_u32(sB) >> 4;
         const uint32_t astage16 = (uint32_t)a.a_stage_bytes >> 4, bstage16 = (uint32_t)a.b_stage_bytes >> 4;
         const uint32_t btile16 = (uint32_t)a.b_tile_bytes >> 4;
-        const int box_tiles = a.box_tiles, kc_tiles = a.kc_tiles;
+        const int box_tiles = a.box_tiles, kc_tiles = a.kc_tiles, nsb = a.nsb, grb = a.grb;
         const int MT = a.MT, nb = a.nb, na = a.na, kchunks = a.kchunks, nbuf = a.nbuf, BK = a.BK, C = a.C;
         const uint32_t acc_cols = (uint32_t)a.acc_cols;
         const bool resident = a.resident != 0;
@@ -342,72 +348,82 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         int acc = 0;
         uint32_t accp = 0;
         if (resident && cid < a.num_items) {
-            mbar_wait(&b_full[0], 0);
+            mbar_wait_warp(&b_full[0], 0);
             tc_fence_after();
         }
         for (int item = cid; item < a.num_items; item += ncl) {
             const TileCoord tc = fc_work<kPair>(a, item, 0);
-            mbar_wait(&tempty[acc], accp ^ 1);
+            mbar_wait_warp(&tempty[acc], accp ^ 1);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + (uint32_t)acc * (uint32_t)MT * acc_cols;
             const int nph = a.nph, nq = kchunks * nph;
             int q = (cid / a.max_taps) % nq;
             for (int qi = 0; qi < nq; ++qi) {
                 const int kc = q / nph;
-                const FusedClass &cl = a.cls[tc.cls * nph + (q - kc * nph)];
-                const int ntaps = cl.ntaps;
+                // single-entry layers (stride-1 Conv2d) read entry 0 with a constant index: the
+                // table fields then load as uniform constants and the issue loop stays uniform
+                const FusedClass &cl = kOneEntry ? a.cls[0] : a.cls[tc.cls * nph + (q - kc * nph)];
                 const int kvalid = min(BK, C - kc * BK);
                 const int ksteps = (kvalid + KI - 1) / KI;
-                mbar_wait(&a_full[as], ap);
+                mbar_wait_warp(&a_full[as], ap);
                 tc_fence_after();
                 if (item == cid && qi == 0 && lane == 0) FC_TRACE(1);
+                if (item == cid && qi < 6 && lane == 0) FC_TRACE(8 + 3 * qi);     // A landed
                 const uint32_t a16 = sA16 + (uint32_t)as * astage16;
                 {
-                    // the whole (converged) warp walks the taps with warp-uniform values; only the
+                    // the whole (converged) warp walks the tap grid with warp-uniform values; only the
                     // tcgen05.mma / commit instructions are issued by one elected lane.  Taps come in
                     // weight boxes (kernel-row groups): one wait / commit per box.
-                    int t = 0;
                     const bool full_k = ksteps == 4;
+                    const int nr = cl.nr, ns = cl.ns;
+                    const int a_dk = cl.a_dk * (int)rowb16, a_dl = cl.a_dl * (int)rowb16;
+                    const uint64_t adesc_s = adesc_t | (uint64_t)((a16 + (uint32_t)cl.a_base * rowb16) & 0x3FFF);
                     for (int g = 0; g < cl.ngroups; ++g) {
                         uint32_t gb16;
                         if (resident) {
                             gb16 = sB16 + (uint32_t)(kc * kc_tiles + cl.bres + g * box_tiles) * btile16;
                         } else {
-                            mbar_wait(&b_full[bs], bp);
+                            mbar_wait_warp(&b_full[bs], bp);
                             tc_fence_after();
+                            if (item == cid && qi < 6 && g == 0 && lane == 0) FC_TRACE(9 + 3 * qi);   // B landed
                             gb16 = sB16 + (uint32_t)bs * bstage16;
                         }
-                        const int pend = (g + 1) * box_tiles;
-                        for (; t < ntaps && (int)cl.tap_pos[t] < pend; ++t) {
-                            const uint32_t b16 = gb16 + (uint32_t)((int)cl.tap_pos[t] - g * box_tiles) * btile16;
-                            const uint32_t at16 = a16 + (uint32_t)cl.tap_off[t] * rowb16;
-                            const uint64_t bd = bdesc_t | (uint64_t)(b16 & 0x3FFF);
-                            const uint32_t accum = (uint32_t)(qi | t);
-                            for (int m = 0; m < MT; ++m) {
-                                const uint32_t am16 = at16 + (uint32_t)m * mstride16;
-                                // SWIZZLE_128B rows may start anywhere inside a 1024-byte atom: the tensor
-                                // core XORs with absolute smem address bits, exactly as TMA wrote them, so
-                                // the descriptor's base-offset field stays 0 (verified on B200 by parity)
-                                const uint64_t adm = adesc_t | (uint64_t)(am16 & 0x3FFF);
-                                const uint32_t dm = d_tmem + (uint32_t)m * acc_cols;
-                                if (full_k) {
+                        const uint64_t bdesc_g = bdesc_t | (uint64_t)(gb16 & 0x3FFF);
+                        const int k_lo = g * grb, k_hi = min(k_lo + grb, nr);
+                        for (int k = k_lo; k < k_hi; ++k) {
+                            for (int l = 0; l < ns; ++l) {
+                                // descriptor address fields are 16-byte units; offsets stay inside the
+                                // 14-bit field (smem < 256 KB), so plain 64-bit adds are exact
+                                const uint64_t bd = bdesc_g + (uint64_t)((uint32_t)((k - k_lo) * nsb + l) * btile16);
+                                const uint64_t at = adesc_s + (uint64_t)(int64_t)(k * a_dk + l * a_dl);
+                                const uint32_t first = (uint32_t)(qi == 0 && k == 0 && l == 0);
+                                for (int m = 0; m < MT; ++m) {
+                                    // SWIZZLE_128B rows may start anywhere inside a 1024-byte atom: the
+                                    // tensor core XORs with absolute smem address bits, exactly as TMA
+                                    // wrote them, so the descriptor's base-offset field stays 0
+                                    const uint64_t adm = at + (uint64_t)((uint32_t)m * mstride16);
+                                    const uint32_t dm = d_tmem + (uint32_t)m * acc_cols;
+                                    if (full_k) {
 #pragma unroll
-                                    for (int k = 0; k < 4; ++k) {
-                                        if constexpr (kPair)
-                                            umma_pair_elect<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16),
-                                                                   bd + (uint64_t)(2 * k), idesc, accum | (uint32_t)k);
-                                        else
-                                            umma_elect<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16),
-                                                              bd + (uint64_t)(2 * k), idesc, accum | (uint32_t)k);
-                                    }
-                                } else {
-                                    for (int k = 0; k < ksteps; ++k) {
-                                        if constexpr (kPair)
-                                            umma_pair_elect<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16),
-                                                                   bd + (uint64_t)(2 * k), idesc, accum | (uint32_t)k);
-                                        else
-                                            umma_elect<kTF32>(dm, adm + (uint64_t)((uint32_t)k * kstep16),
-                                                              bd + (uint64_t)(2 * k), idesc, accum | (uint32_t)k);
+                                        for (int ks = 0; ks < 4; ++ks) {
+                                            const uint32_t accum = (first && ks == 0) ? 0u : 1u;
+                                            if constexpr (kPair)
+                                                umma_pair_elect<kTF32>(dm, adm + (uint64_t)((uint32_t)ks * kstep16),
+                                                                       bd + (uint64_t)(2 * ks), idesc, accum);
+                                            else
+                                                umma_elect<kTF32>(dm, adm + (uint64_t)((uint32_t)ks * kstep16),
+                                                                  bd + (uint64_t)(2 * ks), idesc, accum);
+                                        }
+                                    } else {
+                                        for (int ks = 0; ks < ksteps; ++ks) {
+                                            const uint32_t accum = (first && ks == 0) ? 0u : 1u;
+                                            if constexpr (kPair)
+                                                umma_pair_elect<kTF32>(dm, adm + (uint64_t)((uint32_t)ks * kstep16),
+                                                                       bd + (uint64_t)(2 * ks), idesc, accum);
+                                            else
+                                                umma_elect<kTF32>(dm, adm + (uint64_t)((uint32_t)ks * kstep16),
+                                                                  bd + (uint64_t)(2 * ks), idesc, accum);
+                                        }
                                     }
                                 }
                             }
@@ -422,6 +438,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                     else umma_commit_elect(&a_empty[as]);
                 }
                 __syncwarp();
+                if (item == cid && qi < 6 && lane == 0) FC_TRACE(10 + 3 * qi);    // step issued
                 if (++as == na) { as = 0; ap ^= 1; }
                 if (++q == nq) q = 0;
             }

@@ -556,15 +556,15 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
             c.px = st * pg.qmin_x + pg.rho_x[ph];
             c.wi0 = pg.wi0[ph];
             c.wj0 = pg.wj0[ph];
-            for (int i = 0; i < s->r; ++i)
-                for (int j = 0; j < s->s; ++j) {
-                    const int ei = (int)(i * dil - s->pad), ej = (int)(j * dil - s->pad);
-                    const int qi = floordiv_i(ei, st), qj = floordiv_i(ej, st);
-                    if (ei - st * qi != pg.rho_y[ph] || ej - st * qj != pg.rho_x[ph]) continue;
-                    c.tap_off[c.ntaps] = (uint16_t)((qi - pg.qmin_y) * a.Xb + (qj - pg.qmin_x));
-                    c.tap_pos[c.ntaps] = (uint8_t)(((i - c.wi0) / a.westr) * a.nsb + (j - c.wj0) / a.westr);
-                    ++c.ntaps;
-                }
+            c.nr = pg.nr[ph];
+            c.ns = pg.ns[ph];
+            c.ntaps = c.nr * c.ns;
+            // kernel row wi0 + westr*k reads subsampled-patch row q(k) - qmin with q(k) = q(0) + k*dil/g
+            const int step = dil / gcd_i(st, dil);
+            const int q0y = floordiv_i((int)(c.wi0 * dil - s->pad), st), q0x = floordiv_i((int)(c.wj0 * dil - s->pad), st);
+            c.a_base = (q0y - pg.qmin_y) * a.Xb + (q0x - pg.qmin_x);
+            c.a_dk = step * a.Xb;
+            c.a_dl = step;
         }
     } else {
         const int st = s->stride;
@@ -580,12 +580,12 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                 c.px = g.cb - (g.ntaps_s - 1);
                 c.wi0 = g.i0;
                 c.wj0 = g.j0;
-                for (int k = 0; k < g.ntaps_r; ++k)
-                    for (int l = 0; l < g.ntaps_s; ++l) {
-                        const int t = k * g.ntaps_s + l;
-                        c.tap_off[t] = (uint16_t)((g.ntaps_r - 1 - k) * a.Xb + (g.ntaps_s - 1 - l));
-                        c.tap_pos[t] = (uint8_t)(k * a.nsb + l);
-                    }
+                c.nr = g.ntaps_r;
+                c.ns = g.ntaps_s;
+                // kernel row i0 + st*k reads input row (tile row) + c_a - k: patch row nr-1-k
+                c.a_base = (g.ntaps_r - 1) * a.Xb + (g.ntaps_s - 1);
+                c.a_dk = -a.Xb;
+                c.a_dl = -1;
             }
     }
     // weight boxes: groups of grb kernel rows per entry, resident tile offsets
@@ -713,9 +713,9 @@ static bool fused_preferred(const ollie_conv_shape *s, bool tf32, int transposed
     return e.ok && e.fused_cost <= e.unfused_cost;
 }
 
-template <bool TF32, bool PAIR>
+template <bool TF32, bool PAIR, bool ONE>
 static ollie_status launch_fused_t(const CUtensorMap &tx, const CUtensorMap &tw, const FusedArgs &a, cudaStream_t stream) {
-    auto kern = fused_conv_kernel<TF32, PAIR>;
+    auto kern = fused_conv_kernel<TF32, PAIR, ONE>;
     static bool attr_done[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -780,8 +780,13 @@ static ollie_status run_fused(const ollie_conv_shape *s, bool tf32, int transpos
                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (weights) failed (%d)", (int)r);
     }
-    if (a.pair) return tf32 ? launch_fused_t<true, true>(tx, tw, a, stream) : launch_fused_t<false, true>(tx, tw, a, stream);
-    return tf32 ? launch_fused_t<true, false>(tx, tw, a, stream) : launch_fused_t<false, false>(tx, tw, a, stream);
+    const bool one = a.nclass * a.nph == 1;
+    if (a.pair) {
+        if (one) return tf32 ? launch_fused_t<true, true, true>(tx, tw, a, stream) : launch_fused_t<false, true, true>(tx, tw, a, stream);
+        return tf32 ? launch_fused_t<true, true, false>(tx, tw, a, stream) : launch_fused_t<false, true, false>(tx, tw, a, stream);
+    }
+    if (one) return tf32 ? launch_fused_t<true, false, true>(tx, tw, a, stream) : launch_fused_t<false, false, true>(tx, tw, a, stream);
+    return tf32 ? launch_fused_t<true, false, false>(tx, tw, a, stream) : launch_fused_t<false, false, false>(tx, tw, a, stream);
 }
 
 // ------------------------------------------------------------------------ shapes

@@ -10,10 +10,12 @@
 
 using namespace ollie;
 
-__global__ void __launch_bounds__(128, 1) bench(int N, int nmma, int arow, int rnd, int m256, long long *out) {
+__device__ __forceinline__ bool lane_is0() { return (threadIdx.x & 31) == 0; }
+__global__ void __launch_bounds__(128, 1) bench(int N, int nmma, int arow, int rnd, int m256, long long *out,
+                                               int taps, int stw) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar, done2, sink2;
     __shared__ uint32_t tslot;
     for (int i = threadIdx.x; i < 160 * 1024 / 4; i += blockDim.x) {
         uint32_t h = (uint32_t)i * 2654435761u + blockIdx.x;
@@ -23,7 +25,9 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int nmma, int arow, int r
         uint32_t hi = (((h >> 10) & 1) << 15) | ((126u + ((h >> 11) % 3)) << 7) | ((h >> 14) & 0x7F);
         reinterpret_cast<uint32_t *>(smem)[i] = rnd ? (lo | (hi << 16)) : 0u;
     }
-    if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&done2, 1); mbar_init(&sink2, 1); fence_barrier_init(); }
+    __syncthreads();
+    if (threadIdx.x == 0) mbar_arrive(&done2);
     __syncthreads();
     if (threadIdx.x < 32) tmem_alloc<512>(&tslot);
     tc_fence_before();
@@ -31,20 +35,72 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int nmma, int arow, int r
     tc_fence_after();
     const uint32_t tmem = tslot;
     const uint32_t idesc = make_idesc(false, 128, N);
-    const uint32_t a0 = smem_u32(smem) + (uint32_t)arow * 128u, b0 = smem_u32(smem + 96 * 1024);
+    const uint32_t a0 = smem_u32(smem) + (uint32_t)arow * 128u, b0 = smem_u32(smem + 48 * 1024);
     long long t0 = 0, t1 = 0;
-    if (threadIdx.x == 0) {
+    __shared__ volatile int stop;
+    if (threadIdx.x == 0) stop = 0;
+    __syncthreads();
+    if (threadIdx.x == 0 && stw < 2) {
         t0 = clock64();
         for (int m = 0; m < nmma; ++m) {
             const int k = m & 3;
-            const uint64_t da = make_sdesc_k_sw128(a0 + k * 32);
-            const uint64_t db = make_sdesc_k_sw128(b0 + k * 32);
+            // "taps": the A start row moves by 1 row per tap (mid-atom), B switches to another tile
+            const int t = taps > 1 ? (m >> 2) % taps : 0;
+            const uint64_t da = make_sdesc_k_sw128(a0 + (uint32_t)t * 128u + k * 32);
+            const uint64_t db = make_sdesc_k_sw128(b0 + (uint32_t)t * (uint32_t)(N * 128) % (48u * 1024u) + k * 32);
             umma<false>(tmem + (uint32_t)((m >> 2) & 1) * (uint32_t)(m256 ? 0 : 256), da, db, idesc, 1);
         }
         umma_commit(&bar);
         mbar_wait(&bar, 0);
         t1 = clock64();
         out[blockIdx.x] = t1 - t0;
+        stop = 1;
+        (void)t1;
+    } else if (threadIdx.x >= 32 && threadIdx.x < 64 && stw >= 2) {
+        // lean issuer (warp 1, converged): stw 2 = same A/B every MMA; 3 = conv-like taps (A row
+        // offsets {0,1,2,16,17,18,32,33,34}, one 8 KB B tile per tap); 4 = 3 + a concurrent smem
+        // writer warp (TMA-like traffic)
+        __syncwarp();
+        long long s0 = clock64();
+        const uint64_t da0 = make_sdesc_k_sw128(a0), db0 = make_sdesc_k_sw128(b0);
+        const uint32_t dcol = tmem;
+        for (int m = 0; m < nmma; m += 36) {
+            if (stw >= 5) {
+                // per-step sync like the conv kernel: wait A, fence, wait B, fence
+                mbar_wait_warp(&done2, 0);
+                tc_fence_after();
+                mbar_wait_warp(&done2, 0);
+                tc_fence_after();
+            }
+            for (int t = 0; t < 9; ++t) {
+                uint64_t da = da0, db = db0;
+                if (stw >= 3) {
+                    da += (uint64_t)(((t / 3) * 16 + (t % 3)) * 8);
+                    db += (uint64_t)(t * N * 8);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) umma_elect<false>(dcol, da + 2 * k, db + 2 * k, idesc, 1);
+            }
+            if (stw >= 6) { umma_commit_elect(&sink2); umma_commit_elect(&sink2); }
+        }
+        umma_commit_elect(&bar);
+        mbar_wait(&bar, 0);
+        if (lane_is0()) out[blockIdx.x] = clock64() - s0;
+        if (lane_is0()) stop = 1;
+    } else if (threadIdx.x >= 64 && threadIdx.x < 96 && stw >= 4) {
+        uint4 *dst = reinterpret_cast<uint4 *>(smem + 180 * 1024);
+        int i = threadIdx.x - 64;
+        while (!stop) {
+#pragma unroll
+            for (int r = 0; r < 8; ++r) dst[(i + r * 32) & 255] = make_uint4(r, i, 0, 0);
+        }
+    } else if (threadIdx.x >= 64 && stw == 1) {
+        // concurrent smem writes (TMA-like traffic) into a region the MMAs do not read
+        uint4 *dst = reinterpret_cast<uint4 *>(smem + 150 * 1024);
+        int i = threadIdx.x - 64;
+        while (!stop) {
+            for (int r = 0; r < 16; ++r) dst[(i + r * 64) & 511] = make_uint4(r, i, 0, 0);
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -55,18 +111,19 @@ int main() {
     long long *d;
     cudaMalloc(&d, 148 * sizeof(long long));
     cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    const int nmma = 4096;
-    for (int rnd = 0; rnd < 2; ++rnd)
-        for (int arow : {0, 1, 3})
-            for (int N : {16, 32, 64, 128, 256}) {
-                bench<<<148, 128, 200 * 1024>>>(N, nmma, arow, rnd, 1, d);
+    const int nmma = 36 * 128;
+    for (int stw = 3; stw < 7; ++stw)
+        for (int taps : {1})
+            for (int N : {32, 64, 128}) {
+                const int rnd = 1, arow = 0;
+                bench<<<148, 128, 200 * 1024>>>(N, nmma, arow, rnd, 1, d, taps, stw);
                 cudaError_t e = cudaDeviceSynchronize();
                 if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
                 long long h[148];
                 cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
                 long long mx = 0;
                 for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
-                printf("data=%s arow=%d N=%3d : %6.1f cyc/mma  (math-bound %5.1f)\n", rnd ? "rand" : "zero", arow, N,
+                printf("smem-writer=%d taps=%d N=%3d : %6.1f cyc/mma  (math-bound %5.1f)\n", stw, taps, N,
                        (double)mx / nmma, 128.0 * N * 16 * 2 / 8192.0);
             }
     return 0;

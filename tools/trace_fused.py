@@ -48,8 +48,12 @@ t = tr.view(-1, 32).cpu()
 t = t[t[:, 30] != 0]
 g0 = t[:, 30].min()
 names = ["setup", "A0", "-", "tile0_mma", "-", "epi0", "epi_end", "end"]
+for q in range(6):
+    names += [f"s{q}_A", f"s{q}_B", f"s{q}_issued"]
+names = names[:8] + names[8:]
 print("CTAs", t.shape[0], "start spread (ns):", int((t[:, 30] - g0).max()))
 for k, nm in enumerate(names):
     if nm == '-': continue
+    if k >= 8 and (t[:, k] == 0).all(): continue
     col = t[:, k].double()
     print(f"{nm:10s} min {col.min():9.0f} med {col.median():9.0f} max {col.max():9.0f}")
