@@ -41,6 +41,8 @@ constexpr uint32_t FC_TMEM_COLS = 512;
 constexpr int FC_SMEM_BUDGET = 225 * 1024;
 constexpr int FC_MAX_CLASSES = 9;            // table entries: ConvT output classes x strided-conv input phases
 constexpr int FC_MAX_TAPS = 32;
+// split-K receive buffer: (ks - 1) senders x (128 / ks) owned rows x FS fp32 (host sizes it)
+__host__ __device__ constexpr int fc_red_bytes(int ks, int FS) { return ks > 1 ? (ks - 1) * (128 / ks) * FS * 4 : 0; }
 
 struct FusedClass {                   // one (output class, input phase) table entry
     int32_t ntaps;
@@ -82,6 +84,7 @@ struct FusedArgs {
     int32_t sw128;                    // 1: patch rows are 128-byte pixel rows, SWIZZLE_128B (BK*es == 128)
     int32_t tmem_cols;                // 512 (1 CTA / SM) or 256 (2 CTAs / SM share the SM's TMEM)
     int32_t pair;                     // 1: CTA pairs (cluster of 2) issue cta_group::2 MMAs with M = 256
+    int32_t ksplit;                   // > 1: split-K over a cluster of ksplit CTAs (DSMEM reduction), MT == 1
     int32_t num_items;                // work items: num_tiles (single) or ceil(spatial / 2) * f_slices (pair)
     int32_t spatial;                  // spatial tiles = nclass * n * tiles_y * tiles_x
     void *y;
@@ -169,14 +172,18 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     const int b_region = a.resident ? a.kchunks * a.kc_tiles * a.b_tile_bytes : a.nb * a.b_stage_bytes;
     uint8_t *sA = smem;
     uint8_t *sB = sA + a.na * a.a_stage_bytes;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sB + b_region);
+    // split-K receive buffer: [sender slot][FS/4 float4 column groups][owned rows]
+    float4 *sRed = reinterpret_cast<float4 *>(sB + b_region);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sB + b_region + fc_red_bytes(a.ksplit, a.FS));
     uint64_t *a_full = bars;
     uint64_t *a_empty = a_full + a.na;
     uint64_t *b_full = a_empty + a.na;      // [nb]   (resident: b_full[0] = "all weights loaded")
     uint64_t *b_empty = b_full + a.nb;
     uint64_t *tfull = b_empty + a.nb;
     uint64_t *tempty = tfull + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint64_t *recv_full = tempty + 2;       // split-K: every peer pushed its partial of my rows
+    uint64_t *peer_done = recv_full + 1;    // split-K: every peer consumed what I pushed to it
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(peer_done + 1);
 
     // warp index via a lane-0 broadcast: ptxas then knows the role branches are warp-uniform and
     // keeps the MMA issuer on the uniform datapath (plain tid/32 made every issue operand go
@@ -184,10 +191,16 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0);
     const int lane = threadIdx.x & 31;
     // pair mode: cid = the pair's index, rank 0 = the MMA leader; work is strided over pairs
+    // split-K: a cluster of ks CTAs shares every item; CTA `krank` takes steps [q_lo, q_lo + q_cnt)
+    const int ks = kPair ? 1 : a.ksplit;
+    const int krank = ks > 1 ? (int)cluster_ctarank() : 0;
     const int rank = kPair ? (int)cluster_ctarank() : 0;
-    const int cid = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-    const int ncl = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    const int cid = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x / ks;
+    const int ncl = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x / ks;
     const bool leader = rank == 0;
+    const int nq_all = a.kchunks * a.nph;
+    const int q_lo = ks > 1 ? krank * nq_all / ks : 0;
+    const int q_cnt = ks > 1 ? (krank + 1) * nq_all / ks - q_lo : nq_all;
     const int fhalf = kPair ? a.FS / 2 : 0;        // B rows this CTA loads start at f0 + rank * fhalf
     const long long t_entry = clock64();
     if (a.trace && threadIdx.x == 0) {
@@ -204,6 +217,10 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         for (int i = 0; i < a.na; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
         for (int i = 0; i < a.nb; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
         for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], kPair ? 8 : 4); }
+        if (ks > 1) {   // arrivals per item: one per (peer CTA, warp covering the relevant rows)
+            mbar_init(recv_full, (ks - 1) * (128 / ks) / 32);
+            mbar_init(peer_done, (ks - 1) * (128 / ks) / 32);
+        }
         fence_barrier_init();
     }
     if (warp == 2) {
@@ -216,7 +233,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         }
     }
     tc_fence_before();
-    if constexpr (kPair) cluster_sync();   // the peer's barriers exist before any TMA / arrive targets them
+    if (kPair || ks > 1) cluster_sync();   // the peers' barriers exist before any TMA / arrive targets them
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
@@ -269,9 +286,9 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                 const TileCoord tc = fc_work<kPair>(a, item, rank);
                 // steps (kc, ph): channel chunk kc of input phase ph -- one patch, that phase's taps.
                 // A per-CTA rotation of the step and tap order spreads identical weight requests in time.
-                const int nq = a.kchunks * a.nph;
-                int q = (cid / a.max_taps) % nq;
-                for (int qi = 0; qi < nq; ++qi) {
+                const int nq = nq_all;
+                int q = ks > 1 ? q_lo : (cid / a.max_taps) % nq;
+                for (int qi = 0; qi < q_cnt; ++qi) {
                     const int kc = q / a.nph;
                     const FusedClass &cl = a.cls[tc.cls * a.nph + (q - kc * a.nph)];
                     const int xin = a.ist * tc.x0 + cl.px, yin = a.ist * tc.y0 + cl.py;
@@ -356,9 +373,9 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             mbar_wait_warp(&tempty[acc], accp ^ 1);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + (uint32_t)acc * (uint32_t)MT * acc_cols;
-            const int nph = a.nph, nq = kchunks * nph;
-            int q = (cid / a.max_taps) % nq;
-            for (int qi = 0; qi < nq; ++qi) {
+            const int nph = a.nph, nq = nq_all;
+            int q = ks > 1 ? q_lo : (cid / a.max_taps) % nq;
+            for (int qi = 0; qi < q_cnt; ++qi) {
                 const int kc = q / nph;
                 // single-entry layers (stride-1 Conv2d) read entry 0 with a constant index: the
                 // table fields then load as uniform constants and the issue loop stays uniform
@@ -459,9 +476,113 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         pdl_wait();   // Y may still be read by the previous kernel: order our stores after it
         // pair mode: the follower's warps release the LEADER's accumulator barrier (count 8)
         const uint32_t tempty_leader0 = kPair ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
+        uint32_t rc = 0;                         // split-K: reduction chunks processed (buffer = rc & 1)
         for (int item = cid; item < a.num_items; item += ncl) {
             const TileCoord tc = fc_work<kPair>(a, item, rank);
             const FusedClass &cl = a.cls[tc.cls * a.nph];
+            if (ks > 1) {
+                // ===== split-K (push): rows [o*rpc, (o+1)*rpc) of the tile belong to CTA o.  A warp whose
+                // rows another CTA owns pushes its fp32 partial into that CTA's receive buffer with
+                // fire-and-forget distributed-shared-memory stores; owner warps add the pushed
+                // partials to their own and run the normal epilogue.  One arrive per warp per item.
+                const int rpc = 128 / ks;
+                const int owner = L / rpc;
+                const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * a.acc_cols);
+                mbar_wait(&tfull[acc], accp);
+                tc_fence_after();
+                if (owner != krank) {
+                    if (rc > 0) mbar_wait_cluster(peer_done, (rc - 1) & 1);   // owner consumed the last push
+                    const int slot = krank < owner ? krank : krank - 1;
+                    const uint32_t dst0 = mapa_shared(smem_u32(sRed), (uint32_t)owner) +
+                                          (uint32_t)((slot * (a.FS / 4) * rpc + (L - owner * rpc)) * 16);
+                    for (int c0 = 0; c0 < a.FS; c0 += 32) {
+                        uint32_t v[32];
+                        tmem_ld_32x32b_x32(tbase + (uint32_t)c0, v);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int g = 0; g < 8; ++g)
+                            if (c0 + 4 * g < a.FS)
+                                st_dsmem_f4(dst0 + (uint32_t)(((c0 / 4 + g) * rpc) * 16),
+                                            make_float4(__uint_as_float(v[4 * g]), __uint_as_float(v[4 * g + 1]),
+                                                        __uint_as_float(v[4 * g + 2]), __uint_as_float(v[4 * g + 3])));
+                    }
+                    tc_fence_before();
+                    fence_acq_rel_cluster();
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(&tempty[acc]);
+                        mbar_arrive_cluster(mapa_shared(smem_u32(recv_full), (uint32_t)owner));
+                    }
+                } else {
+                    mbar_wait_cluster(recv_full, rc & 1);
+                    const int lr = L - krank * rpc;
+                    const int ly = L / a.Xb, lx = L - (L / a.Xb) * a.Xb;
+                    const int oy = (tc.y0 + ly) * a.ost + cl.oy0, ox = (tc.x0 + lx) * a.ost + cl.ox0;
+                    const bool valid = tc.valid && ly < a.Yb && lx < a.XB && oy < a.OH && ox < a.OW;
+                    const int64_t pix = ((int64_t)tc.img * a.OH + oy) * a.OW + ox;
+                    for (int c0 = 0; c0 < a.FS; c0 += 32) {
+                        uint32_t v[32];
+                        tmem_ld_32x32b_x32(tbase + (uint32_t)c0, v);
+                        tmem_ld_wait();
+                        for (int sl = 0; sl < ks - 1; ++sl) {
+#pragma unroll
+                            for (int g = 0; g < 8; ++g)
+                                if (c0 + 4 * g < a.FS) {
+                                    const float4 p4 = sRed[(sl * (a.FS / 4) + c0 / 4 + g) * rpc + lr];
+                                    v[4 * g] = __float_as_uint(__uint_as_float(v[4 * g]) + p4.x);
+                                    v[4 * g + 1] = __float_as_uint(__uint_as_float(v[4 * g + 1]) + p4.y);
+                                    v[4 * g + 2] = __float_as_uint(__uint_as_float(v[4 * g + 2]) + p4.z);
+                                    v[4 * g + 3] = __float_as_uint(__uint_as_float(v[4 * g + 3]) + p4.w);
+                                }
+                        }
+                        const int f = tc.f0 + c0;
+                        if (!valid || f >= a.F) continue;
+                        const int nf = min(min(32, a.FS - c0), a.F - f);
+                        if (a.epi.on) epi_apply_bits<!kTF32, 32>(a.epi, v, pix * a.F + f, f, nf);
+                        if constexpr (kTF32) {
+                            float *yp = reinterpret_cast<float *>(a.y) + pix * a.F + f;
+                            const int nv = vec ? (nf & ~3) : 0;
+#pragma unroll
+                            for (int e = 0; e < 32; e += 4)
+                                if (e < nv)
+                                    *reinterpret_cast<float4 *>(yp + e) =
+                                        make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]),
+                                                    __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
+#pragma unroll
+                            for (int e = 0; e < 32; ++e)
+                                if (e >= nv && e < nf) yp[e] = __uint_as_float(v[e]);
+                        } else {
+                            uint16_t *yp = reinterpret_cast<uint16_t *>(a.y) + pix * a.F + f;
+                            const int nv = vec ? (nf & ~7) : 0;
+#pragma unroll
+                            for (int e = 0; e < 32; e += 8)
+                                if (e < nv) {
+                                    uint4 pk;
+                                    pk.x = pack_bf16x2_rn(__uint_as_float(v[e]), __uint_as_float(v[e + 1]));
+                                    pk.y = pack_bf16x2_rn(__uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
+                                    pk.z = pack_bf16x2_rn(__uint_as_float(v[e + 4]), __uint_as_float(v[e + 5]));
+                                    pk.w = pack_bf16x2_rn(__uint_as_float(v[e + 6]), __uint_as_float(v[e + 7]));
+                                    *reinterpret_cast<uint4 *>(yp + e) = pk;
+                                }
+#pragma unroll
+                            for (int e = 0; e < 32; ++e)
+                                if (e >= nv && e < nf) yp[e] = float_to_bf16_rne(__uint_as_float(v[e]));
+                        }
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(&tempty[acc]);
+                        // my receive buffer is free again: tell every peer
+                        for (int k = 0; k < ks; ++k)
+                            if (k != krank) mbar_arrive_cluster(mapa_shared(smem_u32(peer_done), (uint32_t)k));
+                    }
+                }
+                ++rc;
+                if (threadIdx.x == 128 && item == cid) FC_TRACE(5);
+                if (++acc == a.nbuf) { acc = 0; accp ^= 1; }
+                continue;
+            }
             mbar_wait(&tfull[acc], accp);
             tc_fence_after();
             for (int m = 0; m < a.MT; ++m) {
@@ -522,11 +643,15 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             if (threadIdx.x == 128 && item == cid) FC_TRACE(5);
             if (++acc == a.nbuf) { acc = 0; accp ^= 1; }
         }
+        if (ks > 1 && rc > 0 && (L / (128 / ks)) != krank) {
+            // pusher warps: the owners' last "consumed" arrives must land before this CTA may leave
+            mbar_wait_cluster(peer_done, (rc - 1) & 1);
+        }
         if (threadIdx.x == 128) FC_TRACE(6);
     }
 
     tc_fence_before();
-    if constexpr (kPair) cluster_sync();   // neither CTA leaves while the pair's MMAs / arrives may target it
+    if (kPair || ks > 1) cluster_sync();   // no CTA leaves while a peer's MMAs / arrives / reads may target it
     else __syncthreads();
     if (threadIdx.x == 0) FC_TRACE(7);
     if (warp == 2) {

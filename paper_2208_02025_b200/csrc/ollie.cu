@@ -15,6 +15,8 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <tuple>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -255,6 +257,7 @@ extern "C" ollie_status ollie_merged_gemm(int64_t M, int64_t N, int64_t K, ollie
 // Tile geometry + f-slice choice for fused_conv_kernel; see fused_conv.cuh for the design.
 static int g_force_mt = 0, g_force_fs = 0, g_force_res = -1;   // debug plan overrides (0 / -1 = auto)
 static int g_force_pair = -1;                                   // debug: -1 auto, 0 single CTAs, 1 CTA pairs
+static int g_force_ks = -1;                                     // debug: -1 auto, else the split-K factor
 static thread_local double g_last_fused_cost = 0, g_last_unfused_cost = 0;
 static thread_local std::vector<FusedArgs> g_last_cands;
 
@@ -459,18 +462,23 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                 const int64_t slices = ceil_div(s->f, FS);
                 const int64_t items = items_sp * slices;
                 if (items > INT32_MAX) continue;
+                for (int ksp : {1, 2, 4})
                 for (int pair = 0; pair <= 1; ++pair)
                 for (int occ = 1; occ <= 2; ++occ)
                 for (int resident = 0; resident <= 1; ++resident) {
                     if (g_force_res >= 0 && resident != g_force_res) continue;
                     if (g_force_pair >= 0 && pair != g_force_pair) continue;
+                    if (g_force_ks >= 0 && ksp != g_force_ks) continue;
+                    // split-K over a cluster of ksp CTAs (DSMEM reduction): single CTAs, streamed
+                    // weights, one M-tile, at least one (chunk, phase) step per CTA
+                    if (ksp > 1 && (pair || resident || MT != 1 || base.kchunks * nph < ksp)) continue;
                     // pair = 1: a CTA pair computes two spatial tiles with M = 256 cta_group::2 MMAs;
                     // each CTA holds half of every weight tile (FS / 2 rows, SW128 atoms of 8 rows)
                     if (pair && (FS % 16 != 0 || items_sp < 2)) continue;
                     const int btile = pair ? bstage / 2 : bstage;      // one tap's tile in this CTA
                     const int64_t items_c = pair ? nclass * ceil_div(items_sp / nclass, 2) * slices : items;
                     // occ = 2: two CTAs per SM, each with half the smem and 256 TMEM columns
-                    const int bud = occ == 1 ? budget : (113 * 1024 - 2048);
+                    const int bud = (occ == 1 ? budget : (113 * 1024 - 2048)) - fc_red_bytes(ksp, FS);
                     const int nbuf_o = occ == 1 ? nbuf : (2 * MT * acc_cols <= 256 ? 2 : 1);
                     if (occ == 2 && MT * acc_cols > 256) continue;
                     // largest weight box (fewest TMA ops) that fits: grb kernel rows per box
@@ -494,8 +502,8 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                     }
                     if (grb == 0) continue;
                     const int bstage_c = nsb * grb * btile;
-                    // grid in work units: CTAs (single) or CTA pairs
-                    const int units = pair ? occ * sms / 2 : occ * sms;
+                    // grid in work units: CTAs (single), CTA pairs, or split-K clusters
+                    const int units = pair ? occ * sms / 2 : occ * sms / ksp;
                     int grid = (int)std::min<int64_t>(items_c, (int64_t)units);
                     if (resident) grid = (int)std::max<int64_t>(slices, grid / slices * slices);
                     const double per_cta = (double)ceil_div(items_c, grid);
@@ -510,7 +518,8 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                     const double ld = (double)base.kchunks * nph * a_op + (resident ? 0.0 : (double)base.kchunks * ops_item * b_op);
                     const double epi = nbuf_o == 2 ? 0.0 : MT * (FS / 32.0) * 400.0;
                     // co-resident CTAs share the SM's tensor core but each has its own TMA stream
-                    double t = per_cta * (std::max(occ * mma, ld) + epi + 600.0);
+                    double t = per_cta * (std::max(occ * mma / ksp, ld / ksp) + epi + 600.0);
+                    if (ksp > 1) t += per_cta * (1500.0 + FS * 4.0);   // push + one cluster round trip per item
                     if (resident) t += (double)base.kchunks * (kc_tiles / (nsb * grb)) * b_op;
                     if (pair) t *= 1.1;   // measured: pairs rarely beat single CTAs on these layers (autotune decides)
                     {
@@ -523,6 +532,7 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                         a.resident = resident; a.na = na; a.nb = nb;
                         a.tmem_cols = occ == 1 ? 512 : 256;
                         a.pair = pair;
+                        a.ksplit = ksp;
                         all.emplace_back(t, a);
                         if (t < best * 0.995) {
                             best = t;
@@ -608,11 +618,11 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
     // the model's best geometry for every (MT, FS, residency, CTAs-per-SM) family, cheapest first:
     // structurally different plans the cost model cannot rank reliably are measured instead
     for (auto &c : all) {
-        if ((int)g_last_cands.size() >= 32) break;
+        if ((int)g_last_cands.size() >= 40) break;
         bool dup = false;
         for (auto &d : g_last_cands)
             dup |= d.MT == c.second.MT && d.FS == c.second.FS && d.resident == c.second.resident &&
-                   d.tmem_cols == c.second.tmem_cols && d.pair == c.second.pair;
+                   d.tmem_cols == c.second.tmem_cols && d.pair == c.second.pair && d.ksplit == c.second.ksplit;
         if (!dup && c.first < 4.0 * best) g_last_cands.push_back(finalize(c.second));
     }
     // the cost of the same layer unfused (GEMM writes T, OffsetAdd reads it back): AUTO only fuses
@@ -644,7 +654,7 @@ static std::map<PlanKey, PlanEntry> g_plan_cache;
 static PlanEntry *plan_entry_mut(const ollie_conv_shape *s, bool tf32, int transposed, int64_t OH, int64_t OW) {
     PlanKey k{{s->n, s->c, s->h, s->w, s->f, s->r * 65536 + s->s, s->pad, s->stride * 65536 + s->dilation,
                (int64_t)tf32 * 2 + transposed + 4 * (int64_t)s->output_padding, num_sms(),
-               g_force_mt * 1000 + g_force_fs, g_force_res * 16 + g_force_pair}};
+               g_force_mt * 1000 + g_force_fs, (g_force_res * 16 + g_force_pair) * 16 + g_force_ks}};
     {
         std::lock_guard<std::mutex> g(g_plan_mu);
         auto it = g_plan_cache.find(k);
@@ -669,18 +679,21 @@ static bool plan_fused(const ollie_conv_shape *s, bool tf32, int transposed, Fus
     return e.ok;
 }
 
-// CTAs launched: work units (CTAs, or CTA pairs in pair mode) x units' CTA count.
-static int fused_grid(const FusedArgs &a) {
+// CTAs launched: work units (CTAs, CTA pairs, or split-K clusters) x CTAs per unit.  max_units
+// caps the units at what can be co-resident (clusters: cudaOccupancyMaxActiveClusters).
+static int fused_grid(const FusedArgs &a, int max_units = 0) {
     const int occ = a.tmem_cols == 256 ? 2 : 1;
-    const int units = a.pair ? occ * num_sms() / 2 : occ * num_sms();
+    const int csz = a.pair ? 2 : (a.ksplit > 1 ? a.ksplit : 1);     // CTAs per work unit (cluster)
+    int units = occ * num_sms() / csz;
+    if (max_units > 0) units = std::min(units, max_units);
     int grid = (int)std::min<int64_t>(a.num_items, (int64_t)units);
     if (a.resident) grid = std::max(a.f_slices, grid / a.f_slices * a.f_slices);   // fixed f-slice per unit
-    return a.pair ? 2 * grid : grid;
+    return csz * grid;
 }
 
 static size_t fused_smem_bytes(const FusedArgs &a) {
     const size_t b_region = a.resident ? (size_t)a.kchunks * a.kc_tiles * a.b_tile_bytes : (size_t)a.nb * a.b_stage_bytes;
-    return 1024 + (size_t)a.na * a.a_stage_bytes + b_region + 1024;
+    return 1024 + (size_t)a.na * a.a_stage_bytes + b_region + (size_t)fc_red_bytes(a.ksplit, a.FS) + 1024;
 }
 
 static bool out_hw(const ollie_conv_shape *s, int transposed, int64_t *OH, int64_t *OW) {
@@ -723,9 +736,40 @@ static ollie_status launch_fused_t(const CUtensorMap &tx, const CUtensorMap &tw,
         CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr_done[dev & 63] = true;
     }
-    if (PAIR)
-        CUDA_TRY(launch_cluster(kern, dim3(fused_grid(a)), dim3(FC_THREADS), fused_smem_bytes(a), stream, 2, tx, tw, a));
-    else
+    const int csz = PAIR ? 2 : a.ksplit;
+    if (csz > 1) {
+        // clusters must all be co-resident for one wave: cap the grid at the active-cluster limit
+        static std::mutex mu;
+        static std::map<std::tuple<const void *, size_t, int>, int> cache;
+        const size_t smem = fused_smem_bytes(a);
+        int maxc = 0;
+        {
+            std::lock_guard<std::mutex> g(mu);
+            auto key = std::make_tuple((const void *)kern, smem, csz);
+            auto it = cache.find(key);
+            if (it != cache.end()) {
+                maxc = it->second;
+            } else {
+                cudaLaunchConfig_t cfg{};
+                cfg.gridDim = dim3(csz * 64);
+                cfg.blockDim = dim3(FC_THREADS);
+                cfg.dynamicSmemBytes = smem;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = (unsigned)csz;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                if (cudaOccupancyMaxActiveClusters(&maxc, kern, &cfg) != cudaSuccess) {
+                    cudaGetLastError();
+                    maxc = 0;
+                }
+                cache[key] = maxc;
+            }
+        }
+        CUDA_TRY(launch_cluster(kern, dim3(fused_grid(a, maxc)), dim3(FC_THREADS), smem, stream, csz, tx, tw, a));
+    } else
         CUDA_TRY(launch(kern, dim3(fused_grid(a)), dim3(FC_THREADS), fused_smem_bytes(a), stream, tx, tw, a));
     return OLLIE_OK;
 }
@@ -1521,10 +1565,10 @@ extern "C" ollie_status ollie_plan_describe(const ollie_conv_shape *s, ollie_dty
         snprintf(buf, len,
                  "fused XB=%d Yb=%d Xb=%d Yp=%d MT=%d FS=%d f_slices=%d resident=%d nbuf=%d na=%d nb=%d BK=%d "
                  "kchunks=%d tiles=%d grid=%d smem=%zu classes=%d phases=%d ist=%d taps=%d sw128=%d ctas_per_sm=%d "
-                 "pair=%d wbox=%dx%d",
+                 "pair=%d wbox=%dx%d ksplit=%d",
                  a.XB, a.Yb, a.Xb, a.Yp, a.MT, a.FS, a.f_slices, a.resident, a.nbuf, a.na, a.nb, a.BK, a.kchunks,
                  a.num_tiles, fused_grid(a), fused_smem_bytes(a), a.nclass, a.nph, a.ist, a.max_taps, a.sw128,
-                 a.tmem_cols == 256 ? 2 : 1, a.pair, a.grb, a.nsb);
+                 a.tmem_cols == 256 ? 2 : 1, a.pair, a.grb, a.nsb, a.ksplit);
     } else if (is_identity_offset_add(s, transposed)) {
         snprintf(buf, len, "unfused-identity gemm BN=%d (OffsetAdd eliminated)", choose_bn(s->r * s->s * s->f));
     } else {
@@ -1546,6 +1590,8 @@ extern "C" void ollie_debug_force_plan(int mt, int fs, int resident) {
 }
 // Debug hook (not part of include/ollie.h): -1 auto, 0 single-CTA plans only, 1 CTA-pair plans only.
 extern "C" void ollie_debug_force_pair(int pair) { g_force_pair = pair; }
+// Debug hook (not part of include/ollie.h): -1 auto, else only plans with this split-K factor.
+extern "C" void ollie_debug_force_ksplit(int ks) { g_force_ks = ks; }
 
 // ------------------------------------------------------------------------ autotune
 extern "C" ollie_status ollie_autotune_derived(const ollie_conv_shape *s, ollie_dtype dtype, int transposed,

@@ -13,12 +13,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("cfg", nargs="?", default="resnet18")
 ap.add_argument("--pair", type=int, default=-1, help="-1 auto, 0 single-CTA plans, 1 CTA-pair plans")
 ap.add_argument("--no-cudnn", action="store_true")
+ap.add_argument("--ks", type=int, default=-1, help="-1 auto, else force the split-K factor")
 ap.add_argument("--describe", action="store_true")
 args = ap.parse_args()
 cfg = args.cfg
 REPS = 10
 from paper_2208_02025_b200 import ollie as O
 O._lib.ollie_debug_force_pair(args.pair)
+O._lib.ollie_debug_force_ksplit(args.ks)
 
 
 def graph_time(fn):

@@ -23,6 +23,7 @@ auto = "auto" in sys.argv[3:]
 kv = dict(a.split("=") for a in sys.argv[3:] if "=" in a and not a.startswith("flags="))
 O._lib.ollie_debug_force_plan(int(kv.get("mt", 0)), int(kv.get("fs", 0)), int(kv.get("res", -1)))
 O._lib.ollie_debug_force_pair(int(kv.get("pair", -1)))
+O._lib.ollie_debug_force_ksplit(int(kv.get("ks", -1)))
 conv = DerivedConv.from_layer(lay, plan=0 if auto else 1).prepare(w.cuda())
 xd = x.cuda()
 if auto:
