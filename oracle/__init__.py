@@ -219,3 +219,31 @@ def epilogue(y, bias=None, residual=None, act: str = "none", alpha=None) -> np.n
     elif act != "none":
         raise ValueError(f"unknown activation {act!r}")
     return v
+
+
+# ----------------------------------------------------------------------------- NEXT-1 derivation
+def conv2d_dilated_as_dense(x_nhwc, w_fcrs, pad: int, dilation: int) -> np.ndarray:
+    """The dilated -> non-dilated derivation ("transforms the dilated convolution into
+    non-dilated convolution by expression derivation"), written out step by step: for pad = d*k,
+    output rows d*u + a read input rows d*(u + i - k) + a only, so
+        X_ab = X[:, a::d, b::d, :]                     (space-to-batch, residue class (a, b))
+        Y[:, a::d, b::d, :] = conv2d(X_ab, W, pad=k)   (dense 3x3, same weights)
+    Stride 1; pad must be a multiple of the dilation (reading R3)."""
+    x = _f64(x_nhwc)
+    d = int(dilation)
+    if pad % d:
+        raise ValueError("pad must be a multiple of the dilation")
+    n, h, w, _ = x.shape
+    f = np.asarray(w_fcrs).shape[0]
+    oh = conv_out_size(h, np.asarray(w_fcrs).shape[2], pad, 1, d)
+    ow = conv_out_size(w, np.asarray(w_fcrs).shape[3], pad, 1, d)
+    y = np.zeros((n, oh, ow, f))
+    for a in range(d):
+        for b in range(d):
+            xab = x[:, a::d, b::d, :]
+            if xab.shape[1] == 0 or xab.shape[2] == 0:
+                continue
+            yab = conv2d(xab, w_fcrs, pad=pad // d)
+            rows, cols = y[:, a::d, b::d, :].shape[1:3]
+            y[:, a::d, b::d, :] = yab[:, :rows, :cols, :]
+    return y

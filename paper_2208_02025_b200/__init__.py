@@ -8,5 +8,6 @@ CPU fallback and the oracle (../oracle) is never imported from here.
 """
 from . import ollie  # noqa: F401  (loads libollie.so)
 from .layers import DerivedConv  # noqa: F401
+from .dilated import DilatedAsDense  # noqa: F401
 
-__all__ = ["ollie", "DerivedConv"]
+__all__ = ["ollie", "DerivedConv", "DilatedAsDense"]

@@ -117,7 +117,11 @@ static cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t 
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
-// Same, with thread-block clusters of `cluster_x` CTAs along x (CTA pairs for cta_group::2).
+// Same, with thread-block clusters of `cluster_x` CTAs along x (CTA pairs for cta_group::2,
+// split-K clusters).  Launched WITHOUT programmatic stream serialization: a cluster kernel launched
+// early behind a running grid deadlocked on B200 (eOperator -> CTA-pair conv chain on a side
+// stream, tools/next1_hang.py); it now starts after its predecessor completes (its
+// griddepcontrol.wait is then a no-op), and may still let its own dependents start early.
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                                   int cluster_x, Args &&...args) {
@@ -134,7 +138,7 @@ static cudaError_t launch_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block,
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
