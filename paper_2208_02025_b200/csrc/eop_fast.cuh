@@ -111,10 +111,18 @@ __global__ void __launch_bounds__(256) eop_affine_gather_kernel(const __grid_con
         const int64_t obase = (int64_t)row0 * e.inner + j0;
         if constexpr (!std::is_void<E>::value) {
             E v[VEC];
+            const E *src = reinterpret_cast<const E *>(e.in) + (off + j0);
+            if (VEC * sizeof(E) == 16 && sl == 1 && j0 >= jlo && j0 + VEC <= jhi &&
+                (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+                // contiguous, in-bounds, aligned: one 16-byte load (layout DLTs, space <-> batch)
+                const uint4 pk = __ldg(reinterpret_cast<const uint4 *>(src));
+                memcpy(v, &pk, 16);
+            } else {
 #pragma unroll
-            for (int q = 0; q < VEC; ++q) {
-                const int32_t j = j0 + q;
-                v[q] = (j >= jlo && j < jhi) ? raw_ld<E>(e.in, off + sl * j) : E(0);
+                for (int q = 0; q < VEC; ++q) {
+                    const int32_t j = j0 + q;
+                    v[q] = (j >= jlo && j < jhi) ? raw_ld<E>(e.in, off + sl * j) : E(0);
+                }
             }
             E *o = reinterpret_cast<E *>(e.out) + obase;
             if (j0 + VEC <= e.inner && ((obase * (int64_t)sizeof(E)) & 15) == 0 && VEC * sizeof(E) == 16) {
