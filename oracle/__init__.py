@@ -65,6 +65,7 @@ def _load():
             lib.oracle_weight_dlt_conv2d.argtypes = [I] * 4 + [_dp] * 2
             lib.oracle_weight_dlt_convt.argtypes = [I] * 4 + [_dp] * 2
             lib.oracle_offset_add.argtypes = [I] * 9 + [_dp] * 2
+            lib.oracle_g2bmm.argtypes = [I] * 5 + [_dp] * 3
             lib.oracle_selective_add.argtypes = [I] * 10 + [_dp] * 2
             lib.oracle_num_threads.restype = ctypes.c_int
             _lib = lib
@@ -247,3 +248,30 @@ def conv2d_dilated_as_dense(x_nhwc, w_fcrs, pad: int, dilation: int) -> np.ndarr
             rows, cols = y[:, a::d, b::d, :].shape[1:3]
             y[:, a::d, b::d, :] = yab[:, :rows, :cols, :]
     return y
+
+
+# ----------------------------------------------------------------------------- NEXT-4 G2BMM
+def g2bmm(a_blk, b_blk, W: int, d: int) -> np.ndarray:
+    """General-to-band matrix multiplication (P:1109-1118 iterator table; LongFormer),
+    reading R4: out[b, m, w] = sum_k A[b, m, k] * B[b, m + d*(w - W), k] for w in [0, 2W],
+    0 where the B row leaves [0, L).  fp64 C loops (conv_oracle.c)."""
+    lib = _load()
+    a, b = _f64(a_blk), _f64(b_blk)
+    nb, L, K = a.shape
+    out = np.zeros((nb, L, 2 * W + 1))
+    lib.oracle_g2bmm(ctypes.c_int64(nb), ctypes.c_int64(L), ctypes.c_int64(K), ctypes.c_int64(W),
+                     ctypes.c_int64(d), _p(a), _p(b), _p(out))
+    return out
+
+
+def g2bmm_residue_split(a_blk, b_blk, W: int, d: int) -> np.ndarray:
+    """The paper's dilated -> non-dilated derivation of G2BMM, step by step: rows of
+    residue r (m = d*u + r) only meet B rows of the same residue, m + d*(w - W) = d*(u + w - W) + r,
+    so out[:, r::d] = G2BMM_{d=1}(A[:, r::d], B[:, r::d]) -- a non-dilated band product per class."""
+    a, b = _f64(a_blk), _f64(b_blk)
+    nb, L, _ = a.shape
+    out = np.zeros((nb, L, 2 * W + 1))
+    for r in range(d):
+        if r < L:
+            out[:, r::d] = g2bmm(a[:, r::d], b[:, r::d], W, 1)
+    return out

@@ -197,6 +197,24 @@ void oracle_selective_add(i64 N, i64 H, i64 W, i64 F, i64 R, i64 S,
                 }
 }
 
+/* NEXT-4 G2BMM, general-to-band matrix multiplication (iterator mapping table, P:1109-1118;
+ * LongFormer dilated attention), the definition written out (reading R4):
+ *   out[b][m][w] = sum_k A[b][m][k] * B[b][m + d*(w - W)][k],  w in [0, 2W],
+ * and 0 when the B row m + d*(w - W) lies outside [0, L).  A, B: [batch][L][K]; out: [batch][L][2W+1]. */
+void oracle_g2bmm(i64 batch, i64 L, i64 K, i64 W, i64 d, const double *A, const double *B, double *out) {
+    const i64 NW = 2 * W + 1;
+#pragma omp parallel for collapse(2) schedule(static)
+    for (i64 b = 0; b < batch; b++)
+        for (i64 m = 0; m < L; m++)
+            for (i64 w = 0; w < NW; w++) {
+                const i64 j = m + d * (w - W);
+                double acc = 0.0;
+                if (j >= 0 && j < L)
+                    for (i64 k = 0; k < K; k++) acc += A[(b * L + m) * K + k] * B[(b * L + j) * K + k];
+                out[(b * L + m) * NW + w] = acc;
+            }
+}
+
 /* Number of OpenMP threads the oracle will use (reported as cpu_baseline.cores). */
 #ifdef _OPENMP
 #include <omp.h>
