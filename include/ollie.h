@@ -254,6 +254,23 @@ ollie_status ollie_eop_analyze(const ollie_eop *eop, ollie_eop_info *info);
 ollie_status ollie_eop_eval(const ollie_eop *eop, const void *const *inputs, void *output,
                             ollie_stream_t stream);
 
+/* ---------------------------------------------------------------------------------
+ * NEXT-4 -- G2BMM, general-to-band matrix multiplication (iterator mapping table, P:1109-1118;
+ * LongFormer dilated attention; band width / dilation reading R4 in DESIGN.md):
+ *     out[b][m][w] = sum_k A[b][m][k] * B[b][m + d*(w - W)][k],   w in [0, 2W],
+ * and 0 where the B row m + d*(w - W) lies outside [0, L).
+ *   A, B : [batch][L][K] dtype elements, 16-byte aligned (device); K*sizeof(elem) == 128
+ *          (K = 64 bf16 / 32 tf32), else E_UNSUPPORTED
+ *   out  : [batch][L][ldo], ldo >= 2W+1; bf16 (BF16) or fp32 (TF32); columns >= 2W+1 untouched
+ *   form : OLLIE_G2BMM_DERIVED -- the paper's dilated -> non-dilated rewrite: tiles of one
+ *          residue class m = r + d*u, a dense band product per class (TMA element stride d);
+ *          OLLIE_G2BMM_DIRECT -- dilated tiles over contiguous rows (band columns d apart), d <= 4.
+ * fp32 accumulation; errors before any launch.
+ * --------------------------------------------------------------------------------- */
+enum { OLLIE_G2BMM_DERIVED = 0, OLLIE_G2BMM_DIRECT = 1 };
+ollie_status ollie_g2bmm(int64_t batch, int64_t L, int64_t K, int64_t W, int64_t d, ollie_dtype dtype,
+                         const void *A, const void *B, void *out, int64_t ldo, int form, ollie_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -147,3 +147,49 @@ def config_seed(config_name: str, layer_index: int) -> int:
     """seed = 1000 + row index (stable per config / layer)."""
     base = sorted(CONFIGS).index(config_name) * 100
     return 1000 + base + layer_index
+
+
+# --------------------------------------------------------------------------- NEXT-4 G2BMM workload
+@dataclass(frozen=True)
+class G2:
+    """LongFormer dilated sliding-window attention scores as G2BMM:
+    A = queries, B = keys, [batch, L, K]; band half-width W and dilation d (reading R4)."""
+    name: str
+    batch: int
+    L: int
+    K: int
+    W: int
+    d: int
+    dtype: str = "bf16"
+
+    @property
+    def flops(self) -> float:        # multiply-adds inside the sequence count, x2
+        n = 0
+        for w in range(2 * self.W + 1):
+            off = self.d * (w - self.W)
+            n += max(0, self.L - abs(off))
+        return 2.0 * self.batch * self.K * n
+
+    @property
+    def bytes(self) -> float:        # |A| + |B| + |out|
+        es = 2 if self.dtype == "bf16" else 4
+        return es * (2 * self.batch * self.L * self.K + self.batch * self.L * (2 * self.W + 1))
+
+
+G2_CONFIGS = {
+    "longformer": [G2("longformer_8x10000x64_w256_d4", 8, 10000, 64, 256, 4)],
+}
+
+
+def g2bmm_inputs(g: G2, seed: int, exact_int: bool = False):
+    """A, B ~ U(-1, 1) rounded to the storage dtype (or integers in [-4, 4]), [batch, L, K]."""
+    gen = torch.Generator().manual_seed(seed)
+    shp = (g.batch, g.L, g.K)
+    if exact_int:
+        a = torch.randint(-4, 5, shp, generator=gen).float()
+        b = torch.randint(-4, 5, shp, generator=gen).float()
+    else:
+        a = torch.rand(shp, generator=gen) * 2 - 1
+        b = torch.rand(shp, generator=gen) * 2 - 1
+    dt = torch_dtype(g.dtype)
+    return a.to(dt), b.to(dt)

@@ -25,6 +25,7 @@
 #include "eop_fast.cuh"
 #include "eop_kernels.cuh"
 #include "fused_conv.cuh"
+#include "g2bmm.cuh"
 #include "merged_gemm.cuh"
 
 using namespace ollie;
@@ -1667,4 +1668,87 @@ extern "C" ollie_status ollie_autotune_derived(const ollie_conv_shape *s, ollie_
     if (best_k < 0 && !unfused_ok) return fail(OLLIE_E_UNSUPPORTED, "no runnable plan to tune");
     // leave y holding the chosen plan's result
     return derived_layer(s, dtype, x, wp, y, ws, ws_bytes, OLLIE_PLAN_AUTO, stream, transposed);
+}
+
+
+// ------------------------------------------------------------------------ NEXT-4 G2BMM
+static int g_g2_dbg = 0;
+// Debug hook (not part of include/ollie.h): G2BMM epilogue ablations (bit 0 skip stores, bit 1 skip staging).
+extern "C" void ollie_debug_g2bmm_flags(int f) { g_g2_dbg = f; }
+template <bool TF32, int CS>
+static ollie_status launch_g2bmm_t(const CUtensorMap &ta, const CUtensorMap &tb, const G2Args &g, size_t smem,
+                                   cudaStream_t stream) {
+    auto kern = g2bmm_kernel<TF32, CS>;
+    static bool attr_done[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_done[dev & 63]) {
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_done[dev & 63] = true;
+    }
+    const int grid = (int)std::min<int64_t>(g.num_items, num_sms());
+    CUDA_TRY(launch(kern, dim3(grid), dim3(G2_THREADS), smem, stream, ta, tb, g));
+    return OLLIE_OK;
+}
+
+extern "C" ollie_status ollie_g2bmm(int64_t batch, int64_t L, int64_t K, int64_t W, int64_t d, ollie_dtype dtype,
+                                    const void *A, const void *B, void *out, int64_t ldo, int form,
+                                    ollie_stream_t stream_) {
+    if (batch <= 0 || L <= 0 || K <= 0 || W < 0 || d < 1) return fail(OLLIE_E_INVALID, "G2BMM: batch, L, K > 0, W >= 0, d >= 1");
+    if (dtype != OLLIE_BF16 && dtype != OLLIE_TF32) return fail(OLLIE_E_UNSUPPORTED, "G2BMM dtype must be BF16 or TF32");
+    if (form != OLLIE_G2BMM_DERIVED && form != OLLIE_G2BMM_DIRECT) return fail(OLLIE_E_INVALID, "unknown G2BMM form %d", form);
+    if (!A || !B || !out) return fail(OLLIE_E_INVALID, "null pointer");
+    if (ldo < 2 * W + 1) return fail(OLLIE_E_INVALID, "ldo < 2W + 1");
+    const bool tf32 = dtype == OLLIE_TF32;
+    const int es = tf32 ? 4 : 2;
+    if (K * es != 128) return fail(OLLIE_E_UNSUPPORTED, "G2BMM implemented for K*sizeof(elem) == 128 (K = 64 bf16 / 32 tf32)");
+    if (!aligned16(A) || !aligned16(B)) return fail(OLLIE_E_ALIGN, "A / B must be 16-byte aligned");
+    if (batch * L * (2 * W + 1) >= (1ll << 40) || L >= (1ll << 30)) return fail(OLLIE_E_UNSUPPORTED, "G2BMM extents too large");
+    // derived: tiles over one residue class (rows r + d*u, stride d), band columns dense (cs = 1);
+    // direct: contiguous rows, band columns d apart (cs = d)
+    const bool derived = form == OLLIE_G2BMM_DERIVED || d == 1;
+    const int stride = derived ? (int)d : 1;
+    const int cs = derived ? 1 : (int)d;
+    if (cs > 4) return fail(OLLIE_E_UNSUPPORTED, "direct G2BMM form implemented for d <= 4 (use the derived form)");
+    if (stride > 8) return fail(OLLIE_E_UNSUPPORTED, "G2BMM derived form implemented for d <= 8 (TMA element stride)");
+    G2Args g{};
+    g.batch = (int)batch; g.L = (int)L; g.W = (int)W; g.d = (int)d;
+    g.stride = stride; g.cs = cs;
+    g.nw = (int)(2 * W + 1);
+    g.nwb = (g.nw + 31) / 32;
+    const int last_col = 96 + cs * 32 * (g.nwb - 1) + 32 * (cs + 1);
+    g.nchunks = (last_col + G2_BN - 1) / G2_BN;
+    g.rpb = 128;                              // rows per TMA box: a power of two with rpb * stride <= 256
+    while (g.rpb * stride > 256) g.rpb /= 2;
+    g.nres = derived ? (int)d : 1;
+    const int64_t rows_per_res = derived ? ceil_div(L, d) : L;
+    g.tiles_r = (int)ceil_div(rows_per_res, 128);
+    g.num_items = (int)(batch * g.nres * g.tiles_r);
+    g.ldo = ldo;
+    g.out = out;
+    g.dbg = g_g2_dbg;
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
+    const CUtensorMapDataType dt = tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    CUtensorMap ta, tb;
+    cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)L, (cuuint64_t)batch};
+    cuuint64_t strides[2] = {(cuuint64_t)(K * es), (cuuint64_t)(L * K * es)};
+    cuuint32_t box[3] = {(cuuint32_t)K, (cuuint32_t)(g.rpb * stride), 1};   // rpb rows, element stride `stride`
+    cuuint32_t estr[3] = {1, (cuuint32_t)stride, 1};
+    for (int t = 0; t < 2; ++t) {
+        CUresult r = enc(t == 0 ? &ta : &tb, dt, 3, const_cast<void *>(t == 0 ? A : B), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (G2BMM) failed (%d)", (int)r);
+    }
+    const size_t smem = 1024 + 128 * 128 + 2 * G2_BN * 128 + G2_EPI_WARPS * 32 * 32 * 4 + 256;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    ollie_status st;
+    switch (cs) {
+        case 1: st = tf32 ? launch_g2bmm_t<true, 1>(ta, tb, g, smem, stream) : launch_g2bmm_t<false, 1>(ta, tb, g, smem, stream); break;
+        case 2: st = tf32 ? launch_g2bmm_t<true, 2>(ta, tb, g, smem, stream) : launch_g2bmm_t<false, 2>(ta, tb, g, smem, stream); break;
+        case 3: st = tf32 ? launch_g2bmm_t<true, 3>(ta, tb, g, smem, stream) : launch_g2bmm_t<false, 3>(ta, tb, g, smem, stream); break;
+        default: st = tf32 ? launch_g2bmm_t<true, 4>(ta, tb, g, smem, stream) : launch_g2bmm_t<false, 4>(ta, tb, g, smem, stream); break;
+    }
+    return st == OLLIE_OK ? ok() : st;
 }

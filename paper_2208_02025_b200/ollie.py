@@ -28,6 +28,7 @@ ATOM_ITER, ATOM_FLOORDIV, ATOM_MOD = 0, 1, 2
 OP_PUSH_ACCESS, OP_PUSH_CONST, OP_ADD, OP_MUL, OP_SUB, OP_NEG, OP_MAX, OP_MIN = range(8)
 MAX_DIMS, MAX_TERMS, MAX_ACCESS, MAX_INSTR, MAX_INPUTS = 8, 8, 8, 32, 8
 ACT_NONE, ACT_RELU, ACT_PRELU = 0, 1, 2
+G2BMM_DERIVED, G2BMM_DIRECT = 0, 1
 
 
 class ConvShape(Structure):
@@ -104,6 +105,8 @@ _sig = {
                                   c_void_p]),
     "ollie_offset_add": (c_int, [_P(ConvShape), c_int, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
     "ollie_eop_analyze": (c_int, [_P(Eop), _P(EopInfo)]),
+    "ollie_g2bmm": (c_int, [c_int64, c_int64, c_int64, c_int64, c_int64, c_int, c_void_p, c_void_p, c_void_p, c_int64,
+                            c_int, c_void_p]),
     "ollie_eop_eval": (c_int, [_P(Eop), _P(c_void_p), c_void_p, c_void_p]),
 }
 for _name, (_res, _args) in _sig.items():
@@ -311,3 +314,10 @@ def eop_analyze(eop: Eop) -> dict:
 def eop_eval(eop: Eop, inputs, output, stream=None):
     arr = (c_void_p * max(1, len(inputs)))(*[_ptr(t) for t in inputs])
     _check(_lib.ollie_eop_eval(ctypes.byref(eop), arr, _ptr(output), _stream(stream)), "ollie_eop_eval")
+
+
+def g2bmm(batch: int, L: int, K: int, W: int, d: int, dtype: int, A, B, out, ldo: int | None = None,
+          form: int = G2BMM_DERIVED, stream=None):
+    """NEXT-4 G2BMM: out[b, m, w] = sum_k A[b, m, k] B[b, m + d(w - W), k], w in [0, 2W] (include/ollie.h)."""
+    _check(_lib.ollie_g2bmm(batch, L, K, W, d, dtype, _ptr(A), _ptr(B), _ptr(out),
+                            2 * W + 1 if ldo is None else ldo, form, _stream(stream)), "ollie_g2bmm")
