@@ -200,9 +200,9 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         for (int i = 0; i < a.na; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
         for (int i = 0; i < a.nb; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
         for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], kPair ? 8 : 4); }
-        if (ks > 1) {   // arrivals per item: one per (peer CTA, warp covering the relevant rows)
-            mbar_init(recv_full, (ks - 1) * (128 / ks) / 32);
-            mbar_init(peer_done, (ks - 1) * (128 / ks) / 32);
+        if (ks > 1) {   // arrivals per item: one per (peer CTA, thread of the relevant rows), each a release
+            mbar_init(recv_full, (ks - 1) * (128 / ks));
+            mbar_init(peer_done, (ks - 1) * (128 / ks));
         }
         fence_barrier_init();
     }
@@ -490,12 +490,10 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                                                         __uint_as_float(v[4 * g + 2]), __uint_as_float(v[4 * g + 3])));
                     }
                     tc_fence_before();
-                    fence_acq_rel_cluster();
+                    // every pushing thread publishes its own stores (release.cluster arrive)
+                    mbar_arrive_cluster(mapa_shared(smem_u32(recv_full), (uint32_t)owner));
                     __syncwarp();
-                    if (lane == 0) {
-                        mbar_arrive(&tempty[acc]);
-                        mbar_arrive_cluster(mapa_shared(smem_u32(recv_full), (uint32_t)owner));
-                    }
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
                 } else {
                     mbar_wait_cluster(recv_full, rc & 1);
                     const int lr = L - krank * rpc;
@@ -553,13 +551,12 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                         }
                     }
                     tc_fence_before();
+                    // my receive buffer is free again: every owner thread tells every peer (its reads
+                    // are ordered before the peers' next pushes by its own release)
+                    for (int k = 0; k < ks; ++k)
+                        if (k != krank) mbar_arrive_cluster(mapa_shared(smem_u32(peer_done), (uint32_t)k));
                     __syncwarp();
-                    if (lane == 0) {
-                        mbar_arrive(&tempty[acc]);
-                        // my receive buffer is free again: tell every peer
-                        for (int k = 0; k < ks; ++k)
-                            if (k != krank) mbar_arrive_cluster(mapa_shared(smem_u32(peer_done), (uint32_t)k));
-                    }
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
                 }
                 ++rc;
                 if (threadIdx.x == 128 && item == cid) FC_TRACE(5);

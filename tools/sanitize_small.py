@@ -3,6 +3,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import ollie_synth as syn
+STAGE = os.environ.get("SAN_STAGE", "all")
 from paper_2208_02025_b200 import ollie as O, eops
 from paper_2208_02025_b200.layers import DerivedConv
 from tests import eop_cases as ec
@@ -26,5 +27,36 @@ for spec, shapes in ((ec.transpose_nchw_to_nhwc(2, 33, 5, 7), [(2, 33, 5, 7)]),
     ins = [torch.randn(s, device="cuda") for s in shapes]
     out = torch.empty([hi - lo for lo, hi in spec["scopes"][0]["trav"]], device="cuda")
     O.eop_eval(e, ins, out)
+# CTA pairs, split-K clusters, strided phases, the NEXT-3 epilogue
+lay = syn.Layer("p", 2, 256, 14, 14, 128, 3, 3, pad=1)
+x, w = syn.layer_inputs(lay, 4)
+for pair, ks in (((1, -1),) if STAGE in ("all", "pair") else ()) + (((0, 2), (0, 4)) if STAGE != "pair" else ()):
+    O._lib.ollie_debug_force_pair(pair)
+    O._lib.ollie_debug_force_ksplit(ks)
+    try:
+        conv = DerivedConv.from_layer(lay, plan=O.PLAN_FUSED, autotune=False).prepare(w.cuda())
+        conv(x.cuda(), bias=torch.randn(lay.f, device="cuda"), residual=torch.randn(lay.n, lay.oh, lay.ow, lay.f, device="cuda").bfloat16(), act=O.ACT_PRELU, alpha=torch.rand(lay.f, device="cuda"))
+        torch.cuda.synchronize()
+        print("ran pair", pair, "ks", ks, O.plan_describe(conv.shape, conv.code, O.PLAN_FUSED, False)[-40:], flush=True)
+    except O.OllieError as e:
+        if e.status != O.E_UNSUPPORTED:
+            raise
+        print("no plan for pair", pair, "ks", ks, flush=True)
+O._lib.ollie_debug_force_pair(-1)
+O._lib.ollie_debug_force_ksplit(-1)
+lay = syn.Layer("s", 1, 64, 13, 11, 64, 3, 3, pad=1, stride=2)
+x, w = syn.layer_inputs(lay, 5)
+DerivedConv.from_layer(lay, plan=O.PLAN_FUSED, autotune=False).prepare(w.cuda())(x.cuda())
+# NEXT-1 and NEXT-4
+from paper_2208_02025_b200 import DilatedAsDense
+lay = syn.Layer("dd", 1, 16, 10, 12, 16, 3, 3, pad=2, dilation=2)
+x, w = syn.layer_inputs(lay, 6)
+DilatedAsDense(1, 16, 10, 12, 16, 3, 3, 2, 2, plan=O.PLAN_FUSED).prepare(w.cuda())(x.cuda())
+for form in (0, 1):
+    g = syn.G2("g", 1, 300, 64, 20, 3)
+    a, b = syn.g2bmm_inputs(g, 7)
+    for ldo in (41, 48):
+        out = torch.empty(1, 300, ldo, dtype=torch.bfloat16, device="cuda")
+        O.g2bmm(1, 300, 64, 20, 3, O.BF16, a.cuda(), b.cuda(), out, ldo, form)
 torch.cuda.synchronize()
 print("sanitize run ok")
