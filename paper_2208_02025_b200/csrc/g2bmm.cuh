@@ -20,9 +20,12 @@
 
 namespace ollie {
 
-constexpr int G2_THREADS = 384;            // warps 0 TMA, 1 MMA, 2 TMEM alloc, 4-11 epilogue
-constexpr int G2_EPI_WARPS = 8;
-constexpr int G2_BN = 256;                 // B rows (S columns) per MMA chunk / TMEM buffer
+// warps 0 TMA, 1 MMA, 2 TMEM alloc, 4.. epilogue: 12 epilogue warps for the derived form (cs = 1,
+// 64-register windows), 8 for the direct form's wider windows
+__host__ __device__ constexpr int g2_epi_warps(int cs) { return cs == 1 ? 12 : 8; }
+__host__ __device__ constexpr int g2_threads(int cs) { return 128 + 32 * g2_epi_warps(cs); }
+constexpr int G2_BN = 128;                 // B rows (S columns) per MMA chunk / TMEM buffer
+constexpr int G2_NBUF = 4;                 // TMEM chunk buffers (4 x 128 = 512 columns) = B ring stages
 
 struct G2Args {
     int32_t batch, L, W, d;
@@ -41,21 +44,23 @@ struct G2Args {
 };
 
 template <bool kTF32, int kCS>
-__global__ void __launch_bounds__(G2_THREADS, 1)
+__global__ void __launch_bounds__(g2_threads(kCS), 1)
 g2bmm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
              const __grid_constant__ G2Args a) {
     constexpr int ES = kTF32 ? 4 : 2;
     constexpr int WIN = 32 * (kCS + 1);    // TMEM window per band block
+    constexpr int EPI = g2_epi_warps(kCS);
+    constexpr int PERQ = EPI / 4;          // epilogue warps per TMEM lane quadrant
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem;                                   // 128 rows x 128 B
-    uint8_t *sB = sA + 128 * 128;                         // 2 stages x 256 rows x 128 B
-    float *sStage = reinterpret_cast<float *>(sB + 2 * G2_BN * 128);   // 8 warps x 32 x 32 fp32
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sStage + G2_EPI_WARPS * 32 * 32);
+    uint8_t *sB = sA + 128 * 128;                         // G2_NBUF stages x G2_BN rows x 128 B
+    float *sStage = reinterpret_cast<float *>(sB + G2_NBUF * G2_BN * 128);   // EPI warps x 32 x 32 fp32
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sStage + EPI * 32 * 32);
     uint64_t *a_full = bars, *a_empty = bars + 1;
-    uint64_t *b_full = bars + 2, *b_empty = bars + 4;
-    uint64_t *tfull = bars + 6, *tempty = bars + 8;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 10);
+    uint64_t *b_full = bars + 2, *b_empty = b_full + G2_NBUF;
+    uint64_t *tfull = b_empty + G2_NBUF, *tempty = tfull + G2_NBUF;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + G2_NBUF);
 
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0);
     const int lane = threadIdx.x & 31;
@@ -65,8 +70,8 @@ g2bmm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
     }
     if (warp == 1 && lane == 0) {
         mbar_init(a_full, 1); mbar_init(a_empty, 1);
-        for (int i = 0; i < 2; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], G2_EPI_WARPS); }
+        for (int i = 0; i < G2_NBUF; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
+        for (int i = 0; i < G2_NBUF; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], EPI); }
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -107,7 +112,7 @@ g2bmm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
                     for (int r0 = 0; r0 < G2_BN; r0 += a.rpb)
                         tma_load_3d(sB + bs * (G2_BN * 128) + r0 * 128, &tm_b, &b_full[bs], 0,
                                     mA0 + a.stride * (c * G2_BN + r0) - dW, bb);
-                    if (++bs == 2) { bs = 0; bp ^= 1; }
+                    if (++bs == G2_NBUF) { bs = 0; bp ^= 1; }
                 }
             }
         }
@@ -125,8 +130,8 @@ g2bmm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
             mbar_wait_warp(a_full, ap);
             tc_fence_after();
             for (int c = 0; c < a.nchunks; ++c, ++cg) {
-                const uint32_t buf = cg & 1;
-                mbar_wait_warp(&tempty[buf], ((cg >> 1) & 1) ^ 1);
+                const uint32_t buf = cg % G2_NBUF;
+                mbar_wait_warp(&tempty[buf], ((cg / G2_NBUF) & 1) ^ 1);
                 mbar_wait_warp(&b_full[bs], bp);
                 tc_fence_after();
                 const uint64_t bdesc = desc_t | (uint64_t)((sB16 + (uint32_t)bs * (G2_BN * 128 / 16)) & 0x3FFF);
@@ -137,7 +142,7 @@ g2bmm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
                 umma_commit_elect(&b_empty[bs]);
                 umma_commit_elect(&tfull[buf]);
                 __syncwarp();
-                if (++bs == 2) { bs = 0; bp ^= 1; }
+                if (++bs == G2_NBUF) { bs = 0; bp ^= 1; }
             }
             umma_commit_elect(a_empty);
             __syncwarp();
@@ -148,7 +153,7 @@ g2bmm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
         // Two warps per TMEM lane quadrant (q = warp % 4) take alternate band blocks. =====
         const int e = warp - 4;
         const int q = warp & 3;
-        const int half = e >> 2;
+        const int half = e >> 2;                  // which of the quadrant's PERQ warps
         const int R0 = 32 * q;
         float *stg = sStage + e * (32 * 32);
         const uint32_t stg_addr = smem_u32(stg);
@@ -158,14 +163,14 @@ g2bmm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
             int bb, mA0;
             item_rows(item, bb, mA0);
             int c_ready = -1, c_freed = -1;
-            for (int bi = half; bi < a.nwb; bi += 2) {
+            for (int bi = half; bi < a.nwb; bi += PERQ) {
                 const int w0 = 32 * bi;
                 const int s = R0 + kCS * w0;                       // window start column in S
                 const int need = (s + WIN - 1) / G2_BN;
                 while (c_ready < need) {
                     ++c_ready;
                     const uint32_t cgc = cg0 + (uint32_t)c_ready;
-                    mbar_wait(&tfull[cgc & 1], (cgc >> 1) & 1);
+                    mbar_wait(&tfull[cgc % G2_NBUF], (cgc / G2_NBUF) & 1);
                     tc_fence_after();
                 }
                 uint32_t v[WIN];
@@ -173,7 +178,7 @@ g2bmm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
                 for (int p = 0; p <= kCS; ++p) {
                     const int col = s + 32 * p;
                     const uint32_t cgc = cg0 + (uint32_t)(col / G2_BN);
-                    const uint32_t taddr = tmem_base + ((uint32_t)R0 << 16) + (cgc & 1) * G2_BN + (uint32_t)(col % G2_BN);
+                    const uint32_t taddr = tmem_base + ((uint32_t)R0 << 16) + (cgc % G2_NBUF) * G2_BN + (uint32_t)(col % G2_BN);
                     tmem_ld_32x32b_x32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&v[32 * p]));
                 }
                 tmem_ld_wait();
@@ -256,17 +261,17 @@ g2bmm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
                 }
                 __syncwarp();
                 // chunks below the next window are no longer needed by this warp
-                const int fmin = (bi + 2 < a.nwb) ? (s + 64 * kCS) / G2_BN : a.nchunks;
+                const int fmin = (bi + PERQ < a.nwb) ? (s + 32 * PERQ * kCS) / G2_BN : a.nchunks;
                 while (c_freed + 1 < fmin) {
                     ++c_freed;
                     while (c_ready < c_freed) {   // never release a chunk before it was produced
                         ++c_ready;
                         const uint32_t cgc = cg0 + (uint32_t)c_ready;
-                        mbar_wait(&tfull[cgc & 1], (cgc >> 1) & 1);
+                        mbar_wait(&tfull[cgc % G2_NBUF], (cgc / G2_NBUF) & 1);
                     }
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[(cg0 + (uint32_t)c_freed) & 1]);
+                    if (lane == 0) mbar_arrive(&tempty[(cg0 + (uint32_t)c_freed) % G2_NBUF]);
                 }
             }
             cg0 += (uint32_t)a.nchunks;

@@ -1687,7 +1687,7 @@ static ollie_status launch_g2bmm_t(const CUtensorMap &ta, const CUtensorMap &tb,
         attr_done[dev & 63] = true;
     }
     const int grid = (int)std::min<int64_t>(g.num_items, num_sms());
-    CUDA_TRY(launch(kern, dim3(grid), dim3(G2_THREADS), smem, stream, ta, tb, g));
+    CUDA_TRY(launch(kern, dim3(grid), dim3(g2_threads(CS)), smem, stream, ta, tb, g));
     return OLLIE_OK;
 }
 
@@ -1741,7 +1741,7 @@ extern "C" ollie_status ollie_g2bmm(int64_t batch, int64_t L, int64_t K, int64_t
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (G2BMM) failed (%d)", (int)r);
     }
-    const size_t smem = 1024 + 128 * 128 + 2 * G2_BN * 128 + G2_EPI_WARPS * 32 * 32 * 4 + 256;
+    const size_t smem = 1024 + 128 * 128 + G2_NBUF * G2_BN * 128 + (size_t)g2_epi_warps(cs) * 32 * 32 * 4 + 512;
     cudaStream_t stream = (cudaStream_t)stream_;
     ollie_status st;
     switch (cs) {
