@@ -144,6 +144,84 @@ __global__ void __launch_bounds__(256) eop_affine_gather_kernel(const __grid_con
     }
 }
 
+// Narrow output rows (inner <= 64 elements, same dtype in and out): one thread per output row,
+// one decode per row, the row's input run read element by element inside its valid interval and
+// written back as 16-byte vectors (channel pads / crops of NHWC rows: FSRCNN's 1 -> 16, 12 -> 16).
+// Row decode + valid interval of the innermost output dim (shared by the row kernels).
+__device__ __forceinline__ void affine_row(const AffineEop &e, int32_t row, int32_t &off, int32_t &jlo, int32_t &jhi) {
+    const int dl = e.nd_out - 1;
+    off = e.base;
+    int32_t idx[FAST_MAX_D];
+#pragma unroll
+    for (int k = 0; k < FAST_MAX_D; ++k) idx[k] = e.b[k];
+    for (int d = e.nd_out - 2; d >= 0; --d) {
+        const int32_t q = row / e.w[d];
+        const int32_t od = row - q * e.w[d];
+        row = q;
+        off += e.s[d] * od;
+#pragma unroll
+        for (int k = 0; k < FAST_MAX_D; ++k) idx[k] += e.a[k][d] * od;
+    }
+    jlo = 0;
+    jhi = e.inner;
+    if (e.chk) {
+#pragma unroll
+        for (int k = 0; k < FAST_MAX_D; ++k)
+            if (e.chk & (1 << k)) {
+                const int32_t c = e.a[k][dl], b = idx[k], n = e.shape[k];
+                if (c == 0) {
+                    if (b < 0 || b >= n) jhi = 0;
+                } else if (c == 1) {
+                    jlo = max(jlo, -b);
+                    jhi = min(jhi, n - b);
+                } else if (c == -1) {
+                    jlo = max(jlo, b - n + 1);
+                    jhi = min(jhi, b + 1);
+                } else if (c > 0) {
+                    jlo = max(jlo, cdiv32(-b, c));
+                    jhi = min(jhi, fdiv32(n - 1 - b, c) + 1);
+                } else {
+                    jlo = max(jlo, cdiv32(n - 1 - b, c));
+                    jhi = min(jhi, fdiv32(-b, c) + 1);
+                }
+            }
+    }
+}
+
+template <typename E>
+__global__ void __launch_bounds__(256) eop_affine_rows_kernel(const __grid_constant__ AffineEop e) {
+    pdl_launch_dependents();
+    pdl_wait();
+    constexpr int VEC = 16 / (int)sizeof(E);
+    const int dl = e.nd_out - 1;
+    const int nvec = (e.inner + VEC - 1) / VEC;
+    for (int32_t row0 = blockIdx.x * blockDim.x + threadIdx.x; row0 < e.rows; row0 += gridDim.x * blockDim.x) {
+        int32_t off, jlo, jhi;
+        affine_row(e, row0, off, jlo, jhi);
+        const int32_t sl = e.s[dl];
+        const E *src = reinterpret_cast<const E *>(e.in) + off;
+        E *o = reinterpret_cast<E *>(e.out) + (int64_t)row0 * e.inner;
+        const bool vec_ok = (e.inner % VEC) == 0;    // rows start 16-byte aligned (host: out aligned)
+        for (int vv = 0; vv < nvec; ++vv) {
+            E v[VEC];
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) {
+                const int32_t j = vv * VEC + q;
+                v[q] = (j >= jlo && j < jhi) ? __ldg(src + sl * j) : E(0);
+            }
+            if (vec_ok) {
+                uint4 pk;
+                memcpy(&pk, v, 16);
+                *reinterpret_cast<uint4 *>(o + vv * VEC) = pk;
+            } else {
+#pragma unroll
+                for (int q = 0; q < VEC; ++q)
+                    if (vv * VEC + q < e.inner) o[vv * VEC + q] = v[q];
+            }
+        }
+    }
+}
+
 // Tiled transpose: the output's innermost dim (dl) is strided in the input and dim dt has input
 // stride 1.  A block moves a 32 (dt) x 128 (dl) strip as four 32 x 32 tiles through shared
 // memory, so both the reads (along dt) and the writes (along dl) are coalesced; same-dtype moves
@@ -188,6 +266,62 @@ __global__ void __launch_bounds__(256) eop_affine_transpose_kernel(const __grid_
             if (ol < e.w[dl] && ot < e.w[dt]) out[obase + ostr[dt] * ot + ol] = tile[tx][r];
         }
         __syncthreads();
+    }
+}
+
+// 2-byte transpose with 16-byte global accesses: a block moves a 64 (dt) x 64 (dl) tile.  Reads:
+// 8 lanes cover one 128-byte run along dt (input stride 1) with uint4 loads; writes: 8 lanes cover
+// one 128-byte run along dl (output stride 1) with uint4 stores; the tile goes through shared
+// memory as 16-bit elements (row pitch 66 halves the bank conflicts of the column gathers).
+// Used when both dims are multiples of 8 and both base offsets are 16-byte aligned (host-checked).
+__global__ void __launch_bounds__(256) eop_affine_transpose16_kernel(const __grid_constant__ AffineEop e) {
+    pdl_launch_dependents();
+    pdl_wait();
+    __shared__ uint16_t tile[64][66];
+    const int dl = e.nd_out - 1, dt = e.dt;
+    const int32_t ns_l = (e.w[dl] + 63) / 64;
+    const int32_t sl = (int32_t)(blockIdx.x % ns_l), tt = (int32_t)(blockIdx.x / ns_l);
+    int32_t rest = (int32_t)blockIdx.y;
+    int32_t off = e.base;
+    int64_t obase = 0, ostride = 1;
+    int64_t ostr[FAST_MAX_D];
+    for (int d = e.nd_out - 1; d >= 0; --d) {
+        ostr[d] = ostride;
+        ostride *= e.w[d];
+    }
+    for (int d = e.nd_out - 1; d >= 0; --d) {
+        if (d == dl || d == dt) continue;
+        const int32_t q = rest / e.w[d];
+        const int32_t od = rest - q * e.w[d];
+        rest = q;
+        off += e.s[d] * od;
+        obase += ostr[d] * od;
+    }
+    const uint16_t *in = reinterpret_cast<const uint16_t *>(e.in);
+    uint16_t *out = reinterpret_cast<uint16_t *>(e.out);
+    const int c8 = threadIdx.x & 7, r = threadIdx.x >> 3;    // 8 lanes x 16 B = one 128-byte run; 32 runs
+    const int32_t l0 = sl * 64, t0 = tt * 64;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {                           // read 64 runs along dt: rows ol = l0 + rr
+        const int rr = r + 32 * h;
+        const int32_t ol = l0 + rr, ot = t0 + 8 * c8;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (ol < e.w[dl] && ot < e.w[dt]) v = __ldg(reinterpret_cast<const uint4 *>(in + off + e.s[dl] * ol + ot));
+        const uint16_t *hv = reinterpret_cast<const uint16_t *>(&v);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) tile[8 * c8 + k][rr] = hv[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {                           // write 64 runs along dl: rows ot = t0 + rr
+        const int rr = r + 32 * h;
+        const int32_t ot = t0 + rr, ol = l0 + 8 * c8;
+        if (ot >= e.w[dt] || ol >= e.w[dl]) continue;
+        uint4 v;
+        uint16_t *hv = reinterpret_cast<uint16_t *>(&v);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) hv[k] = tile[rr][8 * c8 + k];
+        *reinterpret_cast<uint4 *>(out + obase + ostr[dt] * ot + ol) = v;
     }
 }
 

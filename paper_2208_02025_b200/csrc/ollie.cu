@@ -1525,7 +1525,16 @@ extern "C" ollie_status ollie_eop_eval(const ollie_eop *eop, const void *const *
             const int64_t vec_per_row = (fe.inner + 7) / 8;
             const int64_t blocks = std::min<int64_t>(ceil_div((int64_t)fe.rows * vec_per_row, 256), (int64_t)num_sms() * 32);
             const unsigned gb = (unsigned)std::max<int64_t>(blocks, 1);
-            if (fe.in_bf16 == fe.out_bf16) {
+            if (fe.in_bf16 == fe.out_bf16 && fe.inner <= 64 && fe.inner * (fe.in_bf16 ? 2 : 4) % 16 == 0 && aligned16(fe.out)) {
+                // narrow 16-byte-multiple rows: one thread per row
+                const int64_t rb = std::min<int64_t>(ceil_div((int64_t)fe.rows, 256), (int64_t)num_sms() * 32);
+                const unsigned g = (unsigned)std::max<int64_t>(rb, 1);
+                if (fe.in_bf16) {
+                    CUDA_TRY(launch(eop_affine_rows_kernel<uint16_t>, dim3(g), dim3(256), 0, s, fe));
+                } else {
+                    CUDA_TRY(launch(eop_affine_rows_kernel<uint32_t>, dim3(g), dim3(256), 0, s, fe));
+                }
+            } else if (fe.in_bf16 == fe.out_bf16) {
                 if (fe.in_bf16) CUDA_TRY(launch(eop_affine_gather_kernel<8, uint16_t>, dim3(gb), dim3(256), 0, s, fe));
                 else CUDA_TRY(launch(eop_affine_gather_kernel<4, uint32_t>, dim3(gb), dim3(256), 0, s, fe));
             } else {
@@ -1538,6 +1547,17 @@ extern "C" ollie_status ollie_eop_eval(const ollie_eop *eop, const void *const *
             int64_t others = 1;
             for (int d = 0; d < fe.nd_out; ++d)
                 if (d != fe.dt && d != fe.nd_out - 1) others *= fe.w[d];
+            const int dl = fe.nd_out - 1;
+            bool v16 = fe.in_bf16 && fe.out_bf16 && fe.w[dl] % 8 == 0 && fe.w[fe.dt] % 8 == 0 && fe.base % 8 == 0 &&
+                       aligned16(fe.in) && aligned16(fe.out);
+            for (int d = 0; d < fe.nd_out && v16; ++d)
+                if (d != fe.dt && fe.s[d] % 8 != 0) v16 = false;
+            if (v16) {   // 64 x 64 tiles, 16-byte loads and stores
+                const int64_t strips16 = ceil_div(fe.w[dl], 64) * ceil_div(fe.w[fe.dt], 64);
+                CUDA_TRY(launch(eop_affine_transpose16_kernel, dim3((unsigned)strips16, (unsigned)others), dim3(256), 0, s, fe));
+                CHECK_LAUNCH();
+                return ok();
+            }
             const int64_t strips = ceil_div(fe.w[fe.nd_out - 1], 128) * ceil_div(fe.w[fe.dt], 32);
             dim3 grid((unsigned)strips, (unsigned)others);
             if (fe.in_bf16 && fe.out_bf16) CUDA_TRY(launch(eop_affine_transpose_kernel<uint16_t>, grid, dim3(256), 0, s, fe));

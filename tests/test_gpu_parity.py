@@ -233,6 +233,9 @@ EOPS = {
     "affine_mix": lambda: (ec.affine_mix(2, 3, 5, 6), [(2, 3, 5, 6), (5, 6)]),
     # fast paths: tiled transpose (inner output dim strided in the input) and affine gather
     "transpose_big": lambda: (ec.transpose_nchw_to_nhwc(2, 70, 33, 45), [(2, 70, 33, 45)]),
+    # 16-byte transpose path (bf16, every dim a multiple of 8, partial 64 x 64 tiles)
+    "transpose_v16": lambda: (ec.transpose_nchw_to_nhwc(2, 72, 16, 40), [(2, 72, 16, 40)]),
+    "transpose_v16_partial": lambda: (ec.transpose_nchw_to_nhwc(1, 136, 24, 104), [(1, 136, 24, 104)]),
     "channel_pad_big": lambda: (ec.channel_pad(3, 17, 40, 12, 16), [(3, 17, 40, 12)]),
     "flip_pad": lambda: ({"inputs": [{"shape": [5, 37], "pad": [[2, 1], [0, 3]]}],
                           "scopes": [{"trav": [[0, 8], [0, 40]], "sum": [],
