@@ -340,16 +340,48 @@ def gpu_main(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    with torch.cuda.stream(stream):
+    if not chained and gather_bufs is None:
+        # independent layers: pipeline the transfers with the compute -- H2D of layer i's input on
+        # one copy stream, layer i on the compute stream, D2H of its output on the other copy
+        # stream (both copy engines and the SMs busy at once); every step still moves every input
+        # and output through pinned host memory inside the timed region
+        h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        nl = len(stack.layers)
+        ev_in = [torch.cuda.Event() for _ in range(nl)]
+        ev_done = [torch.cuda.Event() for _ in range(nl)]
+        ev_out = [torch.cuda.Event() for _ in range(nl)]
         e2e_s.record(stream)
+        h2d_s.wait_stream(stream)
+        d2h_s.wait_stream(stream)
         for k in range(args.steps):
-            for hd, dd in zip(in_host, in_dev):
-                dd.copy_(hd, non_blocking=True)
-            step()
-            gather()
-            for dd, hh in zip(out_dev, out_host):
-                hh.copy_(dd, non_blocking=True)
+            for i, sl in enumerate(stack.layers):
+                if k > 0:
+                    h2d_s.wait_event(ev_done[i])          # the previous step consumed in_dev[i]
+                with torch.cuda.stream(h2d_s):
+                    in_dev[i].copy_(in_host[i], non_blocking=True)
+                    ev_in[i].record(h2d_s)
+                stream.wait_event(ev_in[i])
+                if k > 0:
+                    stream.wait_event(ev_out[i])          # the previous step's D2H read out_dev[i]
+                sl(in_dev[i], stream.cuda_stream)
+                ev_done[i].record(stream)
+                d2h_s.wait_event(ev_done[i])
+                with torch.cuda.stream(d2h_s):
+                    out_host[i].copy_(out_dev[i], non_blocking=True)
+                    ev_out[i].record(d2h_s)
+        stream.wait_stream(d2h_s)
         e2e_e.record(stream)
+    else:
+        with torch.cuda.stream(stream):
+            e2e_s.record(stream)
+            for k in range(args.steps):
+                for hd, dd in zip(in_host, in_dev):
+                    dd.copy_(hd, non_blocking=True)
+                step()
+                gather()
+                for dd, hh in zip(out_dev, out_host):
+                    hh.copy_(dd, non_blocking=True)
+            e2e_e.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e2e_s.elapsed_time(e2e_e) / args.steps
     if world > 1:

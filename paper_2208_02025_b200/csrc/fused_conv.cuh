@@ -141,7 +141,7 @@ __device__ __forceinline__ TileCoord fc_work(const FusedArgs &a, int item, int r
     else return fc_tile(a, item);
 }
 
-template <bool kTF32, bool kPair, bool kOneEntry>
+template <bool kTF32, bool kPair, bool kOneEntry, bool kSplit>
 __global__ void __launch_bounds__(FC_THREADS, 2)
 fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                   const __grid_constant__ FusedArgs a) {
@@ -157,7 +157,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     uint8_t *sB = sA + a.na * a.a_stage_bytes;
     // split-K receive buffer: [sender slot][FS/4 float4 column groups][owned rows]
     float4 *sRed = reinterpret_cast<float4 *>(sB + b_region);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sB + b_region + fc_red_bytes(a.ksplit, a.FS));
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sB + b_region + (kSplit ? fc_red_bytes(a.ksplit, a.FS) : 0));
     uint64_t *a_full = bars;
     uint64_t *a_empty = a_full + a.na;
     uint64_t *b_full = a_empty + a.na;      // [nb]   (resident: b_full[0] = "all weights loaded")
@@ -175,7 +175,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     const int lane = threadIdx.x & 31;
     // pair mode: cid = the pair's index, rank 0 = the MMA leader; work is strided over pairs
     // split-K: a cluster of ks CTAs shares every item; CTA `krank` takes steps [q_lo, q_lo + q_cnt)
-    const int ks = kPair ? 1 : a.ksplit;
+    const int ks = kSplit ? a.ksplit : 1;    // compile-time 1 unless this is the split-K variant
     const int krank = ks > 1 ? (int)cluster_ctarank() : 0;
     const int rank = kPair ? (int)cluster_ctarank() : 0;
     const int cid = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x / ks;
@@ -463,7 +463,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         for (int item = cid; item < a.num_items; item += ncl) {
             const TileCoord tc = fc_work<kPair>(a, item, rank);
             const FusedClass &cl = a.cls[tc.cls * a.nph];
-            if (ks > 1) {
+            if (kSplit) {
                 // ===== split-K (push): rows [o*rpc, (o+1)*rpc) of the tile belong to CTA o.  A warp whose
                 // rows another CTA owns pushes its fp32 partial into that CTA's receive buffer with
                 // fire-and-forget distributed-shared-memory stores; owner warps add the pushed
