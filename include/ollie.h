@@ -79,7 +79,16 @@ typedef struct {
     int32_t output_padding; /* ConvTranspose2d only (PyTorch semantics, reading Q9)  */
 } ollie_conv_shape;
 
-enum { OLLIE_PLAN_AUTO = 0, OLLIE_PLAN_FUSED = 1, OLLIE_PLAN_UNFUSED = 2 };
+/* Plans of the derived layer:
+ *   AUTO     -- measured choice (first call per shape: ollie_autotune_derived) or the cost model
+ *   FUSED    -- a8: OffsetAdd / selective add fused into the GEMM, T only in TMEM / smem
+ *   UNFUSED  -- the literal two-kernel program: merged GEMM writes T (workspace), then a3 / a4
+ *   GEMM_RED -- merged GEMM over full n*h*w rows whose epilogue adds every T element into its
+ *               output pixel as fp32 L2 reductions (red.global.add.v4.f32; "the L2 reduction",
+ *               P:1580), then Y = epilogue(acc): the workspace holds the fp32 accumulator
+ *               [n][OH][OW][f] (zeroed by the call); f % 4 == 0; summation order is not fixed
+ *               (fp32 atomics: results are deterministic only up to rounding, reading Q12). */
+enum { OLLIE_PLAN_AUTO = 0, OLLIE_PLAN_FUSED = 1, OLLIE_PLAN_UNFUSED = 2, OLLIE_PLAN_GEMM_RED = 3 };
 
 /* ---------------------------------------------------------------------------------
  * Versioning and errors

@@ -175,6 +175,21 @@ __global__ void __launch_bounds__(256) selective_add_kernel(OffsetAddArgs a) {
     }
 }
 
+// GEMM_RED plan, last step: Y = epilogue(acc) in Y's dtype (acc is the fp32 sum the GEMM's
+// reductions produced; 4 channels per thread).
+template <bool kOutBF16>
+__global__ void __launch_bounds__(256) red_finish_kernel(const float *__restrict__ acc, void *y, int64_t n4, int32_t F,
+                                                         EpiArgs epi) {
+    pdl_launch_dependents();
+    pdl_wait();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 s4 = *reinterpret_cast<const float4 *>(acc + 4 * i);
+        float v[4] = {s4.x, s4.y, s4.z, s4.w};
+        if (epi.on) epi_apply<kOutBF16, 4>(epi, v, 4 * i, (int)((4 * i) % F), 4);
+        store_y<4, kOutBF16>(y, 4 * i, v);
+    }
+}
+
 // a0: weight DLT  wp[(ij)*F + f][c] = src[f*sz + c*sc + ij]   (ij = i*S+j)
 //   Conv2d  W[f][c][i][j]: sz = C*RS, sc = RS;   ConvT W[c][f][i][j]: sz = RS, sc = F*RS.
 // Per f a [C x RS] -> [RS x C] transpose through a 32x33 smem tile; pure data movement.

@@ -33,15 +33,28 @@ constexpr size_t gemm_smem_bytes() {
            4 * GEMM_STG_FLOATS * sizeof(float) + 256 /* barriers */;
 }
 
+// GEMM_RED plan: the epilogue performs the OffsetAdd (Conv2d) / selective addition (ConvT) itself
+// as fp32 reductions into L2 -- T[m, (i,j,f)] is added to acc[output pixel of (m, i, j), f] with
+// red.global.add.v4.f32 -- so T never reaches HBM ("the L2 reduction").
+struct RedArgs {
+    float *acc;          // [n][OH][OW][F] fp32, zeroed before the GEMM
+    int32_t H, W, F, S, pad, stride, dil, OH, OW, transposed;
+};
+
 struct GemmArgs {
     int64_t M, N, K;
     int32_t BN;          // UMMA N of a tile
     void *out;           // fp32 or bf16, row-major with leading dimension ldo
     int64_t ldo;
     EpiArgs epi;         // element-wise epilogue (identity plan only: out is Y, column = channel)
+    RedArgs red;         // GEMM_RED plan (kRed kernels only)
 };
 
-template <bool kTF32, bool kOutBF16>
+__device__ __forceinline__ void red_add_v4(float *addr, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
+template <bool kTF32, bool kOutBF16, bool kRed = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 merged_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
     constexpr int ES = kTF32 ? 4 : 2;
@@ -171,6 +184,40 @@ merged_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
                 tmem_ld_wait();
                 if (row >= M) continue;
                 const int nc = (int)min((int64_t)64, col_end - (col_base + c0));
+                if constexpr (kRed) {
+                    // column n = tap*F + f of input pixel `row`: add it at the tap's output pixel
+                    const RedArgs &rd = args.red;
+                    const int HW = rd.H * rd.W;
+                    const int img = (int)(row / HW), rem = (int)(row - (int64_t)img * HW);
+                    const int ih = rem / rd.W, iw = rem - (rem / rd.W) * rd.W;
+                    int n = (int)(col_base + c0);
+                    int tap = n / rd.F, f = n - tap * rd.F;
+                    float *accb = rd.acc + (int64_t)img * rd.OH * rd.OW * rd.F;
+#pragma unroll
+                    for (int e = 0; e < 64; e += 4) {
+                        if (e < nc) {
+                            const int ti = tap / rd.S, tj = tap - (tap / rd.S) * rd.S;
+                            int oh, ow;
+                            bool ok;
+                            if (rd.transposed) {           // selective addition: scatter form
+                                oh = ih * rd.stride - rd.pad + ti * rd.dil;
+                                ow = iw * rd.stride - rd.pad + tj * rd.dil;
+                                ok = true;
+                            } else {                       // OffsetAdd: ih = oh*st - pad + i*dil
+                                const int a0 = ih + rd.pad - ti * rd.dil, b0 = iw + rd.pad - tj * rd.dil;
+                                oh = a0 / rd.stride;
+                                ow = b0 / rd.stride;
+                                ok = a0 >= 0 && b0 >= 0 && oh * rd.stride == a0 && ow * rd.stride == b0;
+                            }
+                            if (ok && oh >= 0 && oh < rd.OH && ow >= 0 && ow < rd.OW)
+                                red_add_v4(accb + ((int64_t)oh * rd.OW + ow) * rd.F + f, __uint_as_float(v[e]),
+                                           __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
+                            f += 4;
+                            if (f >= rd.F) { f -= rd.F; ++tap; }
+                        }
+                    }
+                    continue;
+                }
                 if (args.epi.on)
                     epi_apply_bits<kOutBF16, 64>(args.epi, v, row * args.ldo + col_base + c0, (int)(col_base + c0), nc);
                 if constexpr (kOutBF16) {

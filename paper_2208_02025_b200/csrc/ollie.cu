@@ -209,10 +209,10 @@ static int choose_bn(int64_t N) {
     return best;
 }
 
-template <bool TF32, bool OUTBF16>
+template <bool TF32, bool OUTBF16, bool RED = false>
 static ollie_status launch_gemm_t(const CUtensorMap &ta, const CUtensorMap &tb, const GemmArgs &ga,
                                   cudaStream_t stream) {
-    auto kern = merged_gemm_kernel<TF32, OUTBF16>;
+    auto kern = merged_gemm_kernel<TF32, OUTBF16, RED>;
     static bool attr_done[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -228,7 +228,8 @@ static ollie_status launch_gemm_t(const CUtensorMap &ta, const CUtensorMap &tb, 
 
 // out = A[M,K] * B[N,K]^T ; out fp32 (out_bf16 = false) or bf16, leading dim ldo.
 static ollie_status run_gemm(int64_t M, int64_t N, int64_t K, bool tf32, const void *A, const void *B, void *out,
-                             int64_t ldo, bool out_bf16, cudaStream_t stream, const EpiArgs *epi = nullptr) {
+                             int64_t ldo, bool out_bf16, cudaStream_t stream, const EpiArgs *epi = nullptr,
+                             const RedArgs *red = nullptr) {
     const size_t es = tf32 ? 4 : 2;
     if ((K * es) % 16 != 0)
         return fail(OLLIE_E_ALIGN, "K*sizeof(elem) = %lld is not a multiple of 16 (TMA rule); pad channels",
@@ -243,7 +244,8 @@ static ollie_status run_gemm(int64_t M, int64_t N, int64_t K, bool tf32, const v
     if (st != OLLIE_OK) return st;
     st = make_tmap_2d(&tb, B, tf32, (uint64_t)K, (uint64_t)N, (uint64_t)(K * es), BK, (uint32_t)BN);
     if (st != OLLIE_OK) return st;
-    GemmArgs ga{M, N, K, BN, out, ldo, epi ? *epi : EpiArgs{}};
+    GemmArgs ga{M, N, K, BN, out, ldo, epi ? *epi : EpiArgs{}, red ? *red : RedArgs{}};
+    if (red) return tf32 ? launch_gemm_t<true, false, true>(ta, tb, ga, stream) : launch_gemm_t<false, false, true>(ta, tb, ga, stream);
     if (tf32) return out_bf16 ? launch_gemm_t<true, true>(ta, tb, ga, stream) : launch_gemm_t<true, false>(ta, tb, ga, stream);
     return out_bf16 ? launch_gemm_t<false, true>(ta, tb, ga, stream) : launch_gemm_t<false, false>(ta, tb, ga, stream);
 }
@@ -661,7 +663,7 @@ struct PlanEntry {
     FusedArgs args;                 // the plan in use (model's best, or the autotuned winner)
     std::vector<FusedArgs> cands;   // autotune candidates (cands[0] = model's best)
     double fused_cost, unfused_cost;
-    int tuned;                      // 0: model decides; 1: autotuned fused; 2: autotuned unfused
+    int tuned;                      // 0: model decides; 1: autotuned fused; 2: autotuned unfused; 3: GEMM_RED
 };
 static std::mutex g_plan_mu;
 static std::map<PlanKey, PlanEntry> g_plan_cache;
@@ -732,6 +734,14 @@ static bool fused_supported(const ollie_conv_shape *s, bool tf32, int transposed
 // OLLIE_PLAN_AUTO picks the fused kernel when it can run the layer and its cost estimate beats
 // the unfused GEMM + OffsetAdd estimate (small-F, many-tap layers such as FSRCNN's 9x9 deconv
 // keep the literal merged-GEMM form, where N = r*s*f stays wide).
+static int tuned_choice(const ollie_conv_shape *s, bool tf32, int transposed) {
+    int64_t OH, OW;
+    if (!out_hw(s, transposed, &OH, &OW)) return 0;
+    const PlanEntry &e = plan_entry(s, tf32, transposed, OH, OW);
+    std::lock_guard<std::mutex> g(g_plan_mu);
+    return e.tuned;
+}
+
 static bool fused_preferred(const ollie_conv_shape *s, bool tf32, int transposed) {
     int64_t OH, OW;
     if (!out_hw(s, transposed, &OH, &OW)) return false;
@@ -977,15 +987,29 @@ static bool is_identity_offset_add(const ollie_conv_shape *s, int transposed) {
     return s->r == 1 && s->s == 1 && s->pad == 0 && s->stride == 1 && (!transposed || s->output_padding == 0);
 }
 
+static int tuned_choice(const ollie_conv_shape *s, bool tf32, int transposed);   // autotune result (0 none)
+
 static int resolve_plan(const ollie_conv_shape *s, ollie_dtype dtype, int plan, int transposed) {
-    if (plan == OLLIE_PLAN_FUSED || plan == OLLIE_PLAN_UNFUSED) return plan;
+    if (plan == OLLIE_PLAN_FUSED || plan == OLLIE_PLAN_UNFUSED || plan == OLLIE_PLAN_GEMM_RED) return plan;
     if (is_identity_offset_add(s, transposed)) return OLLIE_PLAN_UNFUSED;
+    if (tuned_choice(s, dtype == OLLIE_TF32, transposed) == 3) return OLLIE_PLAN_GEMM_RED;
     return fused_preferred(s, dtype == OLLIE_TF32, transposed) ? OLLIE_PLAN_FUSED : OLLIE_PLAN_UNFUSED;
 }
 
+// GEMM_RED plan: fp32 output accumulator [n][OH][OW][F] in the workspace.
+static size_t red_acc_bytes(const ollie_conv_shape *s, int64_t OH, int64_t OW) {
+    return (size_t)(s->n * OH * OW * s->f) * sizeof(float);
+}
+static bool red_supported(const ollie_conv_shape *s, int transposed) {
+    return s->f % 4 == 0 && !is_identity_offset_add(s, transposed) && s->h * s->w < (1ll << 30);
+}
+
 extern "C" size_t ollie_workspace_bytes(const ollie_conv_shape *s, ollie_dtype dtype, int plan, int transposed) {
-    if (!s || check_shape(s, transposed, nullptr, nullptr) != OLLIE_OK) return 0;
-    if (resolve_plan(s, dtype, plan, transposed) != OLLIE_PLAN_UNFUSED) return 0;
+    int64_t OH = 0, OW = 0;
+    if (!s || check_shape(s, transposed, &OH, &OW) != OLLIE_OK) return 0;
+    const int rp = resolve_plan(s, dtype, plan, transposed);
+    if (rp == OLLIE_PLAN_GEMM_RED) return red_supported(s, transposed) ? red_acc_bytes(s, OH, OW) : 0;
+    if (rp != OLLIE_PLAN_UNFUSED) return 0;
     if (is_identity_offset_add(s, transposed)) return 0;
     return (size_t)(s->n * s->h * s->w) * (size_t)ldT_of(s) * sizeof(float);
 }
@@ -1001,6 +1025,24 @@ static ollie_status make_epi(const ollie_epilogue *e, EpiArgs *out) {
     out->alpha = e->alpha;
     out->act = e->act;
     out->on = (e->bias || e->residual || e->act != OLLIE_ACT_NONE) ? 1 : 0;
+    return OLLIE_OK;
+}
+
+// GEMM_RED: zero the fp32 accumulator, merged GEMM whose epilogue reduces every T element into
+// its output pixel (L2 atomics), then Y = epilogue(acc) in Y's dtype.  Three stream operations.
+static ollie_status run_gemm_red(const ollie_conv_shape *s, int transposed, bool tf32, const void *x, const void *wp,
+                                 float *acc, void *y, int64_t OH, int64_t OW, cudaStream_t stream, const EpiArgs *epi) {
+    CUDA_TRY(cudaMemsetAsync(acc, 0, red_acc_bytes(s, OH, OW), stream));
+    RedArgs rd{acc, (int)s->h, (int)s->w, (int)s->f, (int)s->s, s->pad, s->stride, s->dilation, (int)OH, (int)OW,
+               transposed};
+    const int64_t M = s->n * s->h * s->w, N = s->r * s->s * s->f;
+    ollie_status st = run_gemm(M, N, s->c, tf32, x, wp, nullptr, 0, false, stream, nullptr, &rd);
+    if (st != OLLIE_OK) return st;
+    const int64_t n4 = s->n * OH * OW * s->f / 4;
+    const unsigned g = (unsigned)std::max<int64_t>(std::min<int64_t>(ceil_div(n4, 256), (int64_t)num_sms() * 16), 1);
+    const EpiArgs e = epi ? *epi : EpiArgs{};
+    if (tf32) CUDA_TRY(launch(red_finish_kernel<false>, dim3(g), dim3(256), 0, stream, (const float *)acc, y, n4, (int32_t)s->f, e));
+    else CUDA_TRY(launch(red_finish_kernel<true>, dim3(g), dim3(256), 0, stream, (const float *)acc, y, n4, (int32_t)s->f, e));
     return OLLIE_OK;
 }
 
@@ -1027,6 +1069,15 @@ static ollie_status derived_layer(const ollie_conv_shape *s, ollie_dtype dtype, 
         if (!fused_supported(s, tf32, transposed))
             return fail(OLLIE_E_UNSUPPORTED, "fused plan not available for this shape/dtype");
         st = run_fused(s, tf32, transposed, x, wp, y, OH, OW, stream, &epi);
+        return st == OLLIE_OK ? ok() : st;
+    }
+    if (rp == OLLIE_PLAN_GEMM_RED) {
+        if (!red_supported(s, transposed))
+            return fail(OLLIE_E_UNSUPPORTED, "GEMM_RED plan needs f %% 4 == 0 and a non-identity OffsetAdd");
+        const size_t need = red_acc_bytes(s, OH, OW);
+        if (!ws || ws_bytes < need) return fail(OLLIE_E_WORKSPACE, "GEMM_RED plan needs %zu workspace bytes (got %zu)", need, ws_bytes);
+        if (!aligned16(ws)) return fail(OLLIE_E_ALIGN, "workspace must be 16-byte aligned");
+        st = run_gemm_red(s, transposed, tf32, x, wp, (float *)ws, y, OH, OW, stream, &epi);
         return st == OLLIE_OK ? ok() : st;
     }
     if (is_identity_offset_add(s, transposed)) {
@@ -1608,6 +1659,9 @@ extern "C" ollie_status ollie_plan_describe(const ollie_conv_shape *s, ollie_dty
                  a.XB, a.Yb, a.Xb, a.Yp, a.MT, a.FS, a.f_slices, a.resident, a.nbuf, a.na, a.nb, a.BK, a.kchunks,
                  a.num_tiles, fused_grid(a), fused_smem_bytes(a), a.nclass, a.nph, a.ist, a.max_taps, a.sw128,
                  a.tmem_cols == 256 ? 2 : 1, a.pair, a.grb, a.nsb, a.ksplit);
+    } else if (rp == OLLIE_PLAN_GEMM_RED) {
+        snprintf(buf, len, "gemm_red BN=%d (%s as fp32 L2 reductions in the GEMM epilogue) + finish",
+                 choose_bn(s->r * s->s * s->f), transposed ? "selective add" : "OffsetAdd");
     } else if (is_identity_offset_add(s, transposed)) {
         snprintf(buf, len, "unfused-identity gemm BN=%d (OffsetAdd eliminated)", choose_bn(s->r * s->s * s->f));
     } else {
@@ -1696,15 +1750,20 @@ extern "C" ollie_status ollie_autotune_derived(const ollie_conv_shape *s, ollie_
             return run_offset_add(s, transposed, (const float *)ws, ldT_of(s), !tf32, y, OH, OW, stream);
         });
     }
+    float t_red = 1e30f;
+    const bool red_ok = red_supported(s, transposed) && ws && ws_bytes >= red_acc_bytes(s, OH, OW) && aligned16(ws);
+    if (red_ok)
+        t_red = time_it([&] { return run_gemm_red(s, transposed, tf32, x, wp, (float *)ws, y, OH, OW, stream, nullptr); });
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     {
         std::lock_guard<std::mutex> g(g_plan_mu);
         if (best_k >= 0) e->args = cands[best_k];
-        e->tuned = (t_unf < best || best_k < 0) ? 2 : 1;
+        if (t_red < best && t_red <= t_unf) e->tuned = 3;
+        else e->tuned = (t_unf < best || best_k < 0) ? 2 : 1;
     }
-    if (best_us) *best_us = 1e3f * std::min(best, t_unf);
-    if (best_k < 0 && !unfused_ok) return fail(OLLIE_E_UNSUPPORTED, "no runnable plan to tune");
+    if (best_us) *best_us = 1e3f * std::min(std::min(best, t_unf), t_red);
+    if (best_k < 0 && !unfused_ok && !red_ok) return fail(OLLIE_E_UNSUPPORTED, "no runnable plan to tune");
     // leave y holding the chosen plan's result
     return derived_layer(s, dtype, x, wp, y, ws, ws_bytes, OLLIE_PLAN_AUTO, stream, transposed);
 }

@@ -28,10 +28,13 @@ class DerivedConv:
         nbytes = _o.workspace_bytes(self.shape, self.code, plan, self.transposed)
         self.autotune = autotune and plan == _o.PLAN_AUTO
         if self.autotune:
-            # the unfused plan is an autotune candidate when its T fits a modest workspace
+            # the unfused and GEMM_RED plans are autotune candidates when their workspaces are modest
             unf = _o.workspace_bytes(self.shape, self.code, _o.PLAN_UNFUSED, self.transposed)
             if unf <= (1 << 30):
                 nbytes = max(nbytes, unf)
+            red = _o.workspace_bytes(self.shape, self.code, _o.PLAN_GEMM_RED, self.transposed)
+            if red <= (1 << 30):
+                nbytes = max(nbytes, red)
         self.ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device) if nbytes else None
         self.ws_bytes = nbytes
         self._tuned = False
@@ -51,7 +54,7 @@ class DerivedConv:
         return self
 
     def resolved_plan(self) -> str:
-        """'fused', 'unfused' or 'identity' (unfused GEMM writing Y; OffsetAdd eliminated)."""
+        """'fused', 'unfused', 'gemm_red' or 'identity' (unfused GEMM writing Y; OffsetAdd eliminated)."""
         d = _o.plan_describe(self.shape, self.code, self.plan, self.transposed)
         return "identity" if d.startswith("unfused-identity") else d.split()[0]
 

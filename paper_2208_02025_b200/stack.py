@@ -86,9 +86,10 @@ class StackLayer:
         return self.conv(x, self.y, stream)
 
     def launches(self) -> int:
-        """Kernels one call launches (pad eOp + 1 fused / identity-eliminated, or 2 unfused)."""
+        """Kernels one call launches (pad eOp + 1 fused / identity-eliminated, 2 unfused, or 3 for
+        GEMM_RED: memset node, GEMM with reductions, finish)."""
         n = 1 if self.pad_eop is not None else 0
-        return n + (2 if self.conv.resolved_plan() == "unfused" else 1)
+        return n + {"unfused": 2, "gemm_red": 3}.get(self.conv.resolved_plan(), 1)
 
 
 class DerivedStack:

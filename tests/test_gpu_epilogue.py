@@ -45,7 +45,7 @@ def _run(O, lay, x, w, plan, bias, res, act, alpha, in_place=False):
         y = conv(_dev(x), y, None, bias=_dev(bias) if bias is not None else None, residual=rd,
                  act=ACTS[act], alpha=_dev(alpha))
     except O.OllieError as e:
-        if plan == O.PLAN_FUSED and e.status == O.E_UNSUPPORTED:
+        if plan in (O.PLAN_FUSED, O.PLAN_GEMM_RED) and e.status == O.E_UNSUPPORTED:
             pytest.skip("no fused plan for this layer")
         raise
     torch.cuda.synchronize()
@@ -53,7 +53,7 @@ def _run(O, lay, x, w, plan, bias, res, act, alpha, in_place=False):
 
 
 @pytest.mark.parametrize("act", ["none", "relu", "prelu"])
-@pytest.mark.parametrize("plan", [0, 1, 2])
+@pytest.mark.parametrize("plan", [0, 1, 2, 3])
 @pytest.mark.parametrize("lay", SMALL, ids=[l.name for l in SMALL])
 def test_epilogue_integer_exact(O, lay, plan, act):
     x, w = syn.layer_inputs(lay, 100, exact_int=True)
@@ -63,7 +63,7 @@ def test_epilogue_integer_exact(O, lay, plan, act):
     assert np.array_equal(got, _round_like(want, lay.dtype))
 
 
-@pytest.mark.parametrize("plan", [0, 1, 2])
+@pytest.mark.parametrize("plan", [0, 1, 2, 3])
 @pytest.mark.parametrize("lay", SMALL, ids=[l.name for l in SMALL])
 def test_epilogue_random_tolerance(O, lay, plan):
     x, w = syn.layer_inputs(lay, 200)
@@ -73,7 +73,7 @@ def test_epilogue_random_tolerance(O, lay, plan):
     assert _max_rel(got, want) <= TOL[lay.dtype]
 
 
-@pytest.mark.parametrize("plan", [0, 1, 2])
+@pytest.mark.parametrize("plan", [0, 1, 2, 3])
 def test_epilogue_bias_only_and_in_place_residual(O, plan):
     lay = syn.Layer("r18_64_tiny", 2, 64, 12, 13, 64, 3, 3, pad=1)
     x, w = syn.layer_inputs(lay, 101, exact_int=True)

@@ -33,7 +33,7 @@ def _ref(lay, x, w):
     return oracle.conv2d(x, w, pad=lay.pad, dilation=lay.dilation)
 
 
-@pytest.mark.parametrize("plan", [0, 1, 2])
+@pytest.mark.parametrize("plan", [0, 1, 2, 3])
 @pytest.mark.parametrize("lay", LAYERS, ids=[l.name for l in LAYERS])
 def test_next1_integer_exact(lay, plan):
     x, w = syn.layer_inputs(lay, 600, exact_int=True)

@@ -42,7 +42,7 @@ def _run_layer(O, lay, x, w, plan):
     try:
         y = conv(_dev(x))
     except O.OllieError as e:
-        if plan == O.PLAN_FUSED and e.status == O.E_UNSUPPORTED:
+        if plan in (O.PLAN_FUSED, O.PLAN_GEMM_RED) and e.status == O.E_UNSUPPORTED:
             pytest.skip("no fused plan for this layer")
         raise
     torch.cuda.synchronize()
@@ -143,7 +143,7 @@ SMALL = [
 ]
 
 
-@pytest.mark.parametrize("plan", [0, 1, 2])
+@pytest.mark.parametrize("plan", [0, 1, 2, 3])
 @pytest.mark.parametrize("lay", SMALL, ids=[l.name for l in SMALL])
 def test_derived_layer_integer_exact(O, lay, plan):
     x, w = syn.layer_inputs(lay, 100, exact_int=True)
@@ -153,7 +153,7 @@ def test_derived_layer_integer_exact(O, lay, plan):
     assert np.array_equal(got, _round_like(ref, lay.dtype))
 
 
-@pytest.mark.parametrize("plan", [0, 1, 2])
+@pytest.mark.parametrize("plan", [0, 1, 2, 3])
 @pytest.mark.parametrize("lay", SMALL, ids=[l.name for l in SMALL])
 def test_derived_layer_random_tolerance(O, lay, plan):
     x, w = syn.layer_inputs(lay, 200)

@@ -15,6 +15,7 @@ ap.add_argument("--pair", type=int, default=-1, help="-1 auto, 0 single-CTA plan
 ap.add_argument("--no-cudnn", action="store_true")
 ap.add_argument("--ks", type=int, default=-1, help="-1 auto, else force the split-K factor")
 ap.add_argument("--describe", action="store_true")
+ap.add_argument("--plan", type=int, default=0, help="0 auto, 1 fused, 2 unfused, 3 gemm_red")
 args = ap.parse_args()
 cfg = args.cfg
 REPS = 10
@@ -44,7 +45,7 @@ def graph_time(fn):
 tot_o = tot_c = 0.0
 for i, lay in enumerate(syn.CONFIGS[cfg]):
     x, w = syn.layer_inputs(lay, 1000 + i)
-    conv = DerivedConv.from_layer(lay).prepare(w.cuda())
+    conv = DerivedConv.from_layer(lay, plan=args.plan).prepare(w.cuda())
     xd = x.cuda(); y = conv.new_output()
     conv(xd, y)
     t_o = graph_time(lambda s: conv(xd, y, s.cuda_stream))
