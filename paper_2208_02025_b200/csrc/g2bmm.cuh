@@ -24,6 +24,9 @@ namespace ollie {
 // 64-register windows), 8 for the direct form's wider windows
 __host__ __device__ constexpr int g2_epi_warps(int cs) { return cs == 1 ? 12 : 8; }
 __host__ __device__ constexpr int g2_threads(int cs) { return 128 + 32 * g2_epi_warps(cs); }
+// per-warp staging tile: 32 rows x pitch floats (cs = 1: whole 64-column windows, pitch 68 keeps the
+// 16-byte row writes conflict-free; otherwise a 32 x 32 band tile)
+__host__ __device__ constexpr int g2_stage_pitch(int cs) { return cs == 1 ? 68 : 32; }
 constexpr int G2_BN = 128;                 // B rows (S columns) per MMA chunk / TMEM buffer
 constexpr int G2_NBUF = 4;                 // TMEM chunk buffers (4 x 128 = 512 columns) = B ring stages
 
@@ -55,8 +58,9 @@ g2bmm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem;                                   // 128 rows x 128 B
     uint8_t *sB = sA + 128 * 128;                         // G2_NBUF stages x G2_BN rows x 128 B
-    float *sStage = reinterpret_cast<float *>(sB + G2_NBUF * G2_BN * 128);   // EPI warps x 32 x 32 fp32
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sStage + EPI * 32 * 32);
+    constexpr int SP = g2_stage_pitch(kCS);
+    float *sStage = reinterpret_cast<float *>(sB + G2_NBUF * G2_BN * 128);   // EPI warps x 32 x SP fp32
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sStage + EPI * 32 * SP);
     uint64_t *a_full = bars, *a_empty = bars + 1;
     uint64_t *b_full = bars + 2, *b_empty = b_full + G2_NBUF;
     uint64_t *tfull = b_empty + G2_NBUF, *tempty = tfull + G2_NBUF;
@@ -155,7 +159,7 @@ g2bmm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
         const int q = warp & 3;
         const int half = e >> 2;                  // which of the quadrant's PERQ warps
         const int R0 = 32 * q;
-        float *stg = sStage + e * (32 * 32);
+        float *stg = sStage + e * (32 * SP);
         const uint32_t stg_addr = smem_u32(stg);
         pdl_wait();
         uint32_t cg0 = 0;
@@ -182,13 +186,58 @@ g2bmm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
                     tmem_ld_32x32b_x32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&v[32 * p]));
                 }
                 tmem_ld_wait();
+                if constexpr (kCS == 1 && !kTF32) {
+                    if ((a.ldo & 7) == 0) {
+                        // whole windows into smem (16-byte stores, pitch 68: conflict-free), the skew is
+                        // taken on the read side: lane (r, x0) gathers stg[r][r + x0 .. r + x0 + 7]
+                        // (bank 5r + x0 + k: all 32 distinct)
+                        if (!(a.dbg & 2)) {
+#pragma unroll
+                            for (int t4 = 0; t4 < 16; ++t4)
+                                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                                 stg_addr + (uint32_t)((lane * SP + 4 * t4) * 4)),
+                                             "f"(__uint_as_float(v[4 * t4])), "f"(__uint_as_float(v[4 * t4 + 1])),
+                                             "f"(__uint_as_float(v[4 * t4 + 2])), "f"(__uint_as_float(v[4 * t4 + 3])));
+                        }
+                        __syncwarp();
+                        const int x = 8 * (lane & 3);
+                        float g8[4][8];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int r = 8 * i + (lane >> 2);
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) g8[i][k] = stg[r * SP + r + x + k];
+                        }
+                        const int w = w0 + x;
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int m = mA0 + a.stride * (R0 + 8 * i + (lane >> 2));
+                            if (m >= a.L || w >= a.nw || (a.dbg & 1)) continue;
+                            uint16_t *o = reinterpret_cast<uint16_t *>(a.out) + (((int64_t)bb * a.L + m) * a.ldo + w);
+                            if (w + 8 <= a.nw) {
+                                uint4 pk;
+                                pk.x = pack_bf16x2_rn(g8[i][0], g8[i][1]);
+                                pk.y = pack_bf16x2_rn(g8[i][2], g8[i][3]);
+                                pk.z = pack_bf16x2_rn(g8[i][4], g8[i][5]);
+                                pk.w = pack_bf16x2_rn(g8[i][6], g8[i][7]);
+                                *reinterpret_cast<uint4 *>(o) = pk;
+                            } else {
+#pragma unroll
+                                for (int k = 0; k < 8; ++k)
+                                    if (w + k < a.nw) o[k] = float_to_bf16_rne(g8[i][k]);
+                            }
+                        }
+                        __syncwarp();
+                        goto block_done;
+                    }
+                }
                 // lane l's band value x (w = w0 + x) sits at window column l + kCS*x
                 if (!(a.dbg & 2))
 #pragma unroll
                 for (int t = 0; t < WIN; ++t) {
                     const int e = t - lane;
                     if (e >= 0 && e < 32 * kCS && (kCS == 1 || e % kCS == 0))
-                        asm volatile("st.shared.f32 [%0], %1;" ::"r"(stg_addr + (uint32_t)((lane * 32 + e / kCS) * 4)),
+                        asm volatile("st.shared.f32 [%0], %1;" ::"r"(stg_addr + (uint32_t)((lane * SP + e / kCS) * 4)),
                                      "f"(__uint_as_float(v[t])));
                 }
                 __syncwarp();
@@ -197,7 +246,7 @@ g2bmm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
                 if constexpr (kTF32) {
                     float f[32];
 #pragma unroll
-                    for (int rl = 0; rl < 32; ++rl) f[rl] = stg[rl * 32 + lane];
+                    for (int rl = 0; rl < 32; ++rl) f[rl] = stg[rl * SP + lane];
 #pragma unroll
                     for (int rl = 0; rl < 32; ++rl) {
                         const int m = mA0 + a.stride * (R0 + rl), w = w0 + lane;
@@ -210,7 +259,7 @@ g2bmm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
                     float4 f[8];
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        const float *src = &stg[(8 * i + (lane >> 2)) * 32 + x];
+                        const float *src = &stg[(8 * i + (lane >> 2)) * SP + x];
                         f[2 * i] = *reinterpret_cast<const float4 *>(src);
                         f[2 * i + 1] = *reinterpret_cast<const float4 *>(src + 4);
                     }
@@ -239,7 +288,7 @@ g2bmm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
                     const int x = 2 * (lane & 15);
                     float2 f[16];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) f[i] = *reinterpret_cast<const float2 *>(&stg[(2 * i + (lane >> 4)) * 32 + x]);
+                    for (int i = 0; i < 16; ++i) f[i] = *reinterpret_cast<const float2 *>(&stg[(2 * i + (lane >> 4)) * SP + x]);
                     const int w = w0 + x;
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
@@ -260,6 +309,7 @@ g2bmm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
                     }
                 }
                 __syncwarp();
+            block_done:
                 // chunks below the next window are no longer needed by this warp
                 const int fmin = (bi + PERQ < a.nwb) ? (s + 32 * PERQ * kCS) / G2_BN : a.nchunks;
                 while (c_freed + 1 < fmin) {

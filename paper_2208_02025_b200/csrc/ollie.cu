@@ -1839,7 +1839,7 @@ extern "C" ollie_status ollie_g2bmm(int64_t batch, int64_t L, int64_t K, int64_t
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (G2BMM) failed (%d)", (int)r);
     }
-    const size_t smem = 1024 + 128 * 128 + G2_NBUF * G2_BN * 128 + (size_t)g2_epi_warps(cs) * 32 * 32 * 4 + 512;
+    const size_t smem = 1024 + 128 * 128 + G2_NBUF * G2_BN * 128 + (size_t)g2_epi_warps(cs) * 32 * g2_stage_pitch(cs) * 4 + 512;
     cudaStream_t stream = (cudaStream_t)stream_;
     ollie_status st;
     switch (cs) {
