@@ -26,6 +26,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [nvcc, *NVCC_FLAGS, "-o", tmp, os.path.join(CSRC, "ollie.cu")]
+    if os.environ.get("OLLIE_FC_DEBUG"):      # debug-switch build for tools/dbgrun.sh experiments only
+        cmd.insert(1, "-DOLLIE_FC_DEBUG=1")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)

@@ -36,6 +36,12 @@
 
 namespace ollie {
 
+// Debug switches (FusedArgs::dbg, env OLLIE_FC_DBG) exist only in builds with -DOLLIE_FC_DEBUG=1:
+// production code is compiled without them.
+#ifndef OLLIE_FC_DEBUG
+#define OLLIE_FC_DEBUG 0
+#endif
+
 constexpr int FC_THREADS = 256;
 constexpr uint32_t FC_TMEM_COLS = 512;
 constexpr int FC_SMEM_BUDGET = 225 * 1024;
@@ -90,13 +96,20 @@ struct FusedArgs {
     void *y;
     EpiArgs epi;                      // NEXT-3 element-wise epilogue (bias / residual / ReLU / PReLU)
     long long *trace;                 // debug only (nullptr in production): per-CTA timestamps
+    int32_t dbg;                      // debug only (0 in production): 1 skip MMAs, 2 tap offsets 0, 4 skip Y stores, 8 B tile 0
     FusedClass cls[FC_MAX_CLASSES];
 };
 
-// Debug timeline: slot k of CTA b at trace[b * 32 + k] (clock64 relative to kernel entry).
+// Debug timeline: slot k of CTA b at trace[b * 32 + k] = %globaltimer (ns) when the point was
+// reached; slot 30 = CTA entry, 31 = CTA exit.  (clock64 deltas proved unreliable for this.)
+__device__ __forceinline__ long long fc_gtimer() {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    return (long long)gt;
+}
 #define FC_TRACE(k)                                                              \
     do {                                                                         \
-        if (a.trace) a.trace[blockIdx.x * 32 + (k)] = clock64() - t_entry;       \
+        if (a.trace) a.trace[blockIdx.x * 32 + (k)] = fc_gtimer();               \
     } while (0)
 
 struct TileCoord {
@@ -185,12 +198,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     const int q_lo = ks > 1 ? krank * nq_all / ks : 0;
     const int q_cnt = ks > 1 ? (krank + 1) * nq_all / ks - q_lo : nq_all;
     const int fhalf = kPair ? a.FS / 2 : 0;        // B rows this CTA loads start at f0 + rank * fhalf
-    const long long t_entry = clock64();
-    if (a.trace && threadIdx.x == 0) {
-        unsigned long long gt;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        a.trace[blockIdx.x * 32 + 30] = (long long)gt;
-    }
+    if (threadIdx.x == 0) FC_TRACE(30);
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmX);
@@ -219,7 +227,10 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     if (kPair || ks > 1) cluster_sync();   // the peers' barriers exist before any TMA / arrive targets them
     else __syncthreads();
     tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
+    // lane-0 broadcast: ptxas then treats the TMEM base as warp-uniform, so the MMA issuer's
+    // accumulator address stays in uniform registers (a plain smem load left it in a vector
+    // register and cost an R2UR per tcgen05.mma, ~110 cycles each at N <= 64)
+    const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
     if (threadIdx.x == 0) FC_TRACE(0);
     if (threadIdx.x == 0) pdl_launch_dependents();   // the next layer may start its prologue
 
@@ -246,6 +257,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                     }
             }
             pdl_wait();
+            FC_TRACE(2);
             if (a.resident && cid < a.num_items) {
                 // the CTA's f-slice is fixed (pair count is a multiple of f_slices): load it once
                 const TileCoord tc0 = fc_work<kPair>(a, cid, rank);
@@ -343,6 +355,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         const int MT = a.MT, nb = a.nb, na = a.na, kchunks = a.kchunks, nbuf = a.nbuf, BK = a.BK, C = a.C;
         const uint32_t acc_cols = (uint32_t)a.acc_cols;
         const bool resident = a.resident != 0;
+        const int dbg = OLLIE_FC_DEBUG ? a.dbg : 0;
         int as = 0, bs = 0;
         uint32_t ap = 0, bp = 0;
         int acc = 0;
@@ -390,44 +403,84 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                         }
                         const uint64_t bdesc_g = bdesc_t | (uint64_t)(gb16 & 0x3FFF);
                         const int k_lo = g * grb, k_hi = min(k_lo + grb, nr);
-                        for (int k = k_lo; k < k_hi; ++k) {
-                            for (int l = 0; l < ns; ++l) {
-                                // descriptor address fields are 16-byte units; offsets stay inside the
-                                // 14-bit field (smem < 256 KB), so plain 64-bit adds are exact
-                                const uint64_t bd = bdesc_g + (uint64_t)((uint32_t)((k - k_lo) * nsb + l) * btile16);
-                                const uint64_t at = adesc_s + (uint64_t)(int64_t)(k * a_dk + l * a_dl);
-                                const uint32_t first = (uint32_t)(qi == 0 && k == 0 && l == 0);
-                                for (int m = 0; m < MT; ++m) {
-                                    // SWIZZLE_128B rows may start anywhere inside a 1024-byte atom: the
-                                    // tensor core XORs with absolute smem address bits, exactly as TMA
-                                    // wrote them, so the descriptor's base-offset field stays 0
-                                    const uint64_t adm = at + (uint64_t)((uint32_t)m * mstride16);
-                                    const uint32_t dm = d_tmem + (uint32_t)m * acc_cols;
-                                    if (full_k) {
+                        // One elected thread walks the whole box (a single divergent region per box):
+                        // per-MMA elect / reconvergence inside the tap loop cost ~2x in MMA issue rate.
+                        if (elect_one()) {
+                          if (full_k && ns <= 3 && !(dbg & 32)) {
+                            // Kernel rows of <= 3 taps: the (tap, k-step) walk of a row is unrolled (12 MMAs
+                            // with distinct descriptor registers).  Rewriting the registers an in-flight
+                            // tcgen05.mma still has to read stalls the issue (WAR on its uniform operands):
+                            // a rolled 4-MMA loop ran at ~100 cycles per MMA, the unrolled row at the
+                            // tensor pipe's own rate.
+                            for (int rep = 0; rep < ((dbg & 16) ? 8 : 1); ++rep)
+                            for (int m = 0; m < ((dbg & 1) ? 0 : MT); ++m) {
+                                const uint32_t dm = d_tmem + (uint32_t)m * acc_cols;
+                                const uint64_t atm = adesc_s + (uint64_t)((uint32_t)m * mstride16);
+                                for (int k = k_lo; k < k_hi; ++k) {
+                                    const uint64_t ak = atm + (uint64_t)(int64_t)(k * a_dk);
+                                    const uint64_t bk = bdesc_g + (uint64_t)((uint32_t)((k - k_lo) * nsb) * btile16);
+                                    const uint32_t first = (uint32_t)(qi == 0 && k == 0);
 #pragma unroll
-                                        for (int ks = 0; ks < 4; ++ks) {
-                                            const uint32_t accum = (first && ks == 0) ? 0u : 1u;
-                                            if constexpr (kPair)
-                                                umma_pair_elect<kTF32>(dm, adm + (uint64_t)((uint32_t)ks * kstep16),
-                                                                       bd + (uint64_t)(2 * ks), idesc, accum);
-                                            else
-                                                umma_elect<kTF32>(dm, adm + (uint64_t)((uint32_t)ks * kstep16),
-                                                                  bd + (uint64_t)(2 * ks), idesc, accum);
+                                    for (int l = 0; l < 3; ++l) {
+                                        if (l < ns) {
+                                            const uint64_t al = ak + (uint64_t)(int64_t)(l * a_dl);
+                                            const uint64_t bl = bk + (uint64_t)((uint32_t)l * btile16);
+#pragma unroll
+                                            for (int ks = 0; ks < 4; ++ks) {
+                                                const uint32_t accum = (first && l == 0 && ks == 0) ? 0u : 1u;
+                                                if constexpr (kPair)
+                                                    umma_pair<kTF32>(dm, al + (uint64_t)((uint32_t)ks * kstep16),
+                                                                     bl + (uint64_t)(2 * ks), idesc, accum);
+                                                else
+                                                    umma<kTF32>(dm, al + (uint64_t)((uint32_t)ks * kstep16),
+                                                                bl + (uint64_t)(2 * ks), idesc, accum);
+                                            }
                                         }
-                                    } else {
-                                        for (int ks = 0; ks < ksteps; ++ks) {
-                                            const uint32_t accum = (first && ks == 0) ? 0u : 1u;
-                                            if constexpr (kPair)
-                                                umma_pair_elect<kTF32>(dm, adm + (uint64_t)((uint32_t)ks * kstep16),
-                                                                       bd + (uint64_t)(2 * ks), idesc, accum);
-                                            else
-                                                umma_elect<kTF32>(dm, adm + (uint64_t)((uint32_t)ks * kstep16),
-                                                                  bd + (uint64_t)(2 * ks), idesc, accum);
+                                    }
+                                }
+                            }
+                          } else
+                            for (int rep = 0; rep < ((dbg & 16) ? 8 : 1); ++rep)
+                            for (int k = k_lo; k < k_hi; ++k) {
+                                for (int l = 0; l < ns; ++l) {
+                                    // descriptor address fields are 16-byte units; offsets stay inside the
+                                    // 14-bit field (smem < 256 KB), so plain 64-bit adds are exact
+                                    const uint64_t bd = bdesc_g + ((dbg & 8) ? 0ull : (uint64_t)((uint32_t)((k - k_lo) * nsb + l) * btile16));
+                                    const uint64_t at = adesc_s + ((dbg & 2) ? 0ull : (uint64_t)(int64_t)(k * a_dk + l * a_dl));
+                                    const uint32_t first = (uint32_t)(qi == 0 && k == 0 && l == 0);
+                                    for (int m = 0; m < ((dbg & 1) ? 0 : MT); ++m) {
+                                        // SWIZZLE_128B rows may start anywhere inside a 1024-byte atom: the
+                                        // tensor core XORs with absolute smem address bits, exactly as TMA
+                                        // wrote them, so the descriptor's base-offset field stays 0
+                                        const uint64_t adm = at + (uint64_t)((uint32_t)m * mstride16);
+                                        const uint32_t dm = d_tmem + (uint32_t)m * acc_cols;
+                                        if (full_k) {
+#pragma unroll
+                                            for (int ks = 0; ks < 4; ++ks) {
+                                                const uint32_t accum = (first && ks == 0) ? 0u : 1u;
+                                                if constexpr (kPair)
+                                                    umma_pair<kTF32>(dm, adm + (uint64_t)((uint32_t)ks * kstep16),
+                                                                     bd + (uint64_t)(2 * ks), idesc, accum);
+                                                else
+                                                    umma<kTF32>(dm, adm + (uint64_t)((uint32_t)ks * kstep16),
+                                                                bd + (uint64_t)(2 * ks), idesc, accum);
+                                            }
+                                        } else {
+                                            for (int ks = 0; ks < ksteps; ++ks) {
+                                                const uint32_t accum = (first && ks == 0) ? 0u : 1u;
+                                                if constexpr (kPair)
+                                                    umma_pair<kTF32>(dm, adm + (uint64_t)((uint32_t)ks * kstep16),
+                                                                     bd + (uint64_t)(2 * ks), idesc, accum);
+                                                else
+                                                    umma<kTF32>(dm, adm + (uint64_t)((uint32_t)ks * kstep16),
+                                                                bd + (uint64_t)(2 * ks), idesc, accum);
+                                            }
                                         }
                                     }
                                 }
                             }
                         }
+                        __syncwarp();
                         if (!resident) {
                             if constexpr (kPair) umma_commit_pair_elect(&b_empty[bs], 3);
                             else umma_commit_elect(&b_empty[bs]);
@@ -448,6 +501,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             if (item == cid && lane == 0) FC_TRACE(3);
             if (++acc == nbuf) { acc = 0; accp ^= 1; }
         }
+        if (lane == 0) FC_TRACE(4);
     } else if (warp >= 4) {
         // ===== epilogue: TMEM -> registers -> Y (bf16 RNE or fp32), one output pixel per thread =====
         const int q = warp - 4;
@@ -563,7 +617,16 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                 if (++acc == a.nbuf) { acc = 0; accp ^= 1; }
                 continue;
             }
-            mbar_wait(&tfull[acc], accp);
+            if (OLLIE_FC_DEBUG && (a.dbg & 64)) {   // debug: poll with back-off instead of a blocking try_wait
+                uint32_t ok = 0;
+                while (true) {
+                    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                                 "selp.u32 %0, 1, 0, P1;\n}" : "=r"(ok) : "r"(smem_u32(&tfull[acc])), "r"(accp) : "memory");
+                    if (ok) break;
+                    __nanosleep(500);
+                }
+            } else
+                mbar_wait(&tfull[acc], accp);
             tc_fence_after();
             for (int m = 0; m < a.MT; ++m) {
                 const int oy = (tc.y0 + m * a.Yb + ly) * a.ost + cl.oy0, ox = (tc.x0 + lx) * a.ost + cl.ox0;
@@ -578,7 +641,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                     if (two) tmem_ld_32x32b_x32(tbase + (uint32_t)(c0 + 32), *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
                     tmem_ld_wait();
                     const int f = tc.f0 + c0;
-                    if (!valid || f >= a.F) continue;
+                    if (!valid || f >= a.F || (OLLIE_FC_DEBUG && (a.dbg & 4))) continue;
                     const int nf = min(min(64, a.FS - c0), a.F - f);
                     if (a.epi.on) epi_apply_bits<!kTF32, 64>(a.epi, v, pix * a.F + f, f, nf);
                     if constexpr (kTF32) {
@@ -628,12 +691,15 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             mbar_wait_cluster(peer_done, (rc - 1) & 1);
         }
         if (threadIdx.x == 128) FC_TRACE(6);
+        if (a.trace && threadIdx.x == 128) *reinterpret_cast<volatile uint32_t *>(tmem_slot + 1) = 0xD0E;
     }
 
     tc_fence_before();
     if (kPair || ks > 1) cluster_sync();   // no CTA leaves while a peer's MMAs / arrives / reads may target it
     else __syncthreads();
-    if (threadIdx.x == 0) FC_TRACE(7);
+    if (threadIdx.x == 0) FC_TRACE(31);
+    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 32 + 28] = *reinterpret_cast<volatile uint32_t *>(tmem_slot + 1);
+    if (a.trace && threadIdx.x == 128) FC_TRACE(29);
     if (warp == 2) {
         tc_fence_after();
         if constexpr (kPair) {

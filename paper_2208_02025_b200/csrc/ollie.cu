@@ -808,6 +808,14 @@ static ollie_status run_fused(const ollie_conv_shape *s, bool tf32, int transpos
     a.y = y;
     a.epi = epi ? *epi : EpiArgs{};
     a.trace = g_fc_trace;
+    {   // debug-only kernel switches (OLLIE_FC_DBG, see FusedArgs::dbg); 0 in production
+        static int dbg = -1;
+        if (dbg < 0) {
+            const char *e = getenv("OLLIE_FC_DBG");
+            dbg = e ? atoi(e) : 0;
+        }
+        a.dbg = dbg;
+    }
     PFN_encodeTiled enc = get_encode();
     if (!enc) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
     const int es = tf32 ? 4 : 2, CI = 16 / es;

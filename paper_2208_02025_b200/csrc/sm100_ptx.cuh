@@ -154,6 +154,25 @@ __device__ __forceinline__ void umma_elect(uint32_t d_tmem, uint64_t a_desc, uin
             "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
     }
 }
+// Same, with each descriptor given as (lo, hi) 32-bit words: the issue loop only adds 16-byte
+// address offsets to the low words (32-bit uniform adds instead of 64-bit add-with-carry chains).
+template <bool kTF32>
+__device__ __forceinline__ void umma_elect_lohi(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi, uint32_t b_lo,
+                                                uint32_t b_hi, uint32_t idesc, uint32_t accumulate) {
+    if constexpr (kTF32) {
+        asm volatile(
+            "{\n\t.reg .pred e, p;\n\t.reg .b64 da, db;\n\tmov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+            "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %6, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, p;\n}" ::"r"(d_tmem),
+            "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate));
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred e, p;\n\t.reg .b64 da, db;\n\tmov.b64 da, {%1, %2};\n\tmov.b64 db, {%3, %4};\n\t"
+            "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %6, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n}" ::"r"(d_tmem),
+            "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate));
+    }
+}
 template <bool kTF32>
 __device__ __forceinline__ void umma_pair_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                                 uint32_t accumulate) {

@@ -12,7 +12,7 @@ using namespace ollie;
 
 __device__ __forceinline__ bool lane_is0() { return (threadIdx.x & 31) == 0; }
 __global__ void __launch_bounds__(128, 1) bench(int N, int nmma, int arow, int rnd, int m256, long long *out,
-                                               int taps, int stw) {
+                                               int taps, int stw, int xb = 16) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t bar, done2, sink2;
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int nmma, int arow, int r
             for (int t = 0; t < 9; ++t) {
                 uint64_t da = da0, db = db0;
                 if (stw >= 3) {
-                    da += (uint64_t)(((t / 3) * 16 + (t % 3)) * 8);
+                    da += (uint64_t)(((t / 3) * xb + (t % 3)) * 8);
                     db += (uint64_t)(t * N * 8);
                 }
 #pragma unroll
@@ -107,11 +107,25 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int nmma, int arow, int r
     if (threadIdx.x < 32) { tc_fence_after(); tmem_dealloc<512>(tmem); }
 }
 
-int main() {
+int main(int argc, char **argv) {
     long long *d;
     cudaMalloc(&d, 148 * sizeof(long long));
     cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     const int nmma = 36 * 128;
+    if (argc > 1) {   // row-pitch sweep: conv tap offsets (t/3)*xb + t%3 (the fused kernel's patch width)
+        for (int xb : {16, 8, 9, 10, 13, 18, 30})
+            for (int N : {32, 64, 128}) {
+                bench<<<148, 128, 200 * 1024>>>(N, nmma, 0, 1, 1, d, 1, 3, xb);
+                cudaDeviceSynchronize();
+                long long h[148];
+                cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+                long long mx = 0;
+                for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+                printf("xb=%2d N=%3d : %6.1f cyc/mma\n", xb, N, (double)mx / nmma);
+            }
+        return 0;
+    }
+
     for (int stw = 3; stw < 7; ++stw)
         for (int taps : {1})
             for (int N : {32, 64, 128}) {
