@@ -24,13 +24,13 @@ constexpr int GEMM_STAGES = 4;
 constexpr int GEMM_MAX_BN = 256;
 constexpr int GEMM_A_STAGE_BYTES = GEMM_BM * GEMM_BK_BYTES;          // 16 KB
 constexpr int GEMM_B_STAGE_BYTES = GEMM_MAX_BN * GEMM_BK_BYTES;      // 32 KB (max)
-constexpr int GEMM_STG_FLOATS = 32 * 33;                             // per epilogue warp
+constexpr int GEMM_STG_BYTES = 2 * 32 * 128;                         // per epilogue warp: 2 x (32 rows x 128 B)
 constexpr int GEMM_THREADS = 256;
 constexpr uint32_t GEMM_TMEM_COLS = 512;
 
 constexpr size_t gemm_smem_bytes() {
     return 1024 /* alignment slack */ + (size_t)GEMM_STAGES * (GEMM_A_STAGE_BYTES + GEMM_B_STAGE_BYTES) +
-           4 * GEMM_STG_FLOATS * sizeof(float) + 256 /* barriers */;
+           4 * GEMM_STG_BYTES + 256 /* barriers */;
 }
 
 // GEMM_RED plan: the epilogue performs the OffsetAdd (Conv2d) / selective addition (ConvT) itself
@@ -46,6 +46,7 @@ struct GemmArgs {
     int32_t BN;          // UMMA N of a tile
     void *out;           // fp32 or bf16, row-major with leading dimension ldo
     int64_t ldo;
+    int32_t tma_out;     // 1: fp32 output tiles leave through smem staging + TMA stores (tmO)
     EpiArgs epi;         // element-wise epilogue (identity plan only: out is Y, column = channel)
     RedArgs red;         // GEMM_RED plan (kRed kernels only)
 };
@@ -56,7 +57,8 @@ __device__ __forceinline__ void red_add_v4(float *addr, float a, float b, float 
 
 template <bool kTF32, bool kOutBF16, bool kRed = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-merged_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
+merged_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmO, GemmArgs args) {
     constexpr int ES = kTF32 ? 4 : 2;
     constexpr int BK = GEMM_BK_BYTES / ES;       // 64 bf16 / 32 tf32 elements
     constexpr int UMMA_K_BYTES = 32;             // 16 bf16 / 8 tf32 per tcgen05.mma
@@ -66,8 +68,8 @@ merged_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem;
     uint8_t *sB = sA + GEMM_STAGES * GEMM_A_STAGE_BYTES;
-    float *stg = reinterpret_cast<float *>(sB + GEMM_STAGES * GEMM_B_STAGE_BYTES);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(stg + 4 * GEMM_STG_FLOATS);
+    uint8_t *stg = sB + GEMM_STAGES * GEMM_B_STAGE_BYTES;         // 1024-aligned (SWIZZLE_128B staging)
+    uint64_t *bars = reinterpret_cast<uint64_t *>(stg + 4 * GEMM_STG_BYTES);
     uint64_t *full = bars;                       // [STAGES]
     uint64_t *empty = bars + GEMM_STAGES;        // [STAGES]
     uint64_t *tfull = bars + 2 * GEMM_STAGES;    // [2]
@@ -167,10 +169,47 @@ merged_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         uint32_t acc_phase = 0;
         const bool vec = kOutBF16 ? (args.ldo % 8 == 0) : (args.ldo % 4 == 0);
         pdl_wait();
+        if (lane == 0 && !kOutBF16 && !kRed && args.tma_out) tma_prefetch_desc(&tmO);
+        uint32_t nst = 0;                        // TMA-store path: staging buffers used (buffer = nst & 1)
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             const int m_blk = tile / num_n, n_blk = tile % num_n;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
+            if constexpr (!kOutBF16 && !kRed) {
+                if (args.tma_out && !args.epi.on) {
+                    // fp32 tile -> 32 x 32 SWIZZLE_128B smem blocks -> TMA stores: full 128-byte lines
+                    // (thread-per-row 16-byte stores wrote half sectors and throttled the LSU)
+                    const uint32_t tb0 = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * GEMM_MAX_BN);
+                    const int ncols = (int)min((int64_t)BN, N - (int64_t)n_blk * BN);
+                    for (int c0 = 0; c0 < ncols; c0 += 32) {
+                        uint32_t v[32];
+                        tmem_ld_32x32b_x32(tb0 + (uint32_t)c0, v);
+                        tmem_ld_wait();
+                        if (c0 + 32 >= ncols) {          // accumulator drained: the MMA warp may reuse it
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&tempty[acc]);
+                        }
+                        uint8_t *buf = stg + ew * GEMM_STG_BYTES + (nst & 1) * (32 * 128);
+                        if (lane == 0) bulk_wait_read<1>();      // this buffer's previous store has read it
+                        __syncwarp();
+#pragma unroll
+                        for (int c = 0; c < 8; ++c)
+                            *reinterpret_cast<uint4 *>(buf + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                                make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&tmO, buf, n_blk * BN + c0, m_blk * GEMM_BM + ew * 32);
+                            bulk_commit();
+                        }
+                        ++nst;
+                    }
+                    acc ^= 1;
+                    if (acc == 0) acc_phase ^= 1;
+                    continue;
+                }
+            }
             const int64_t row = (int64_t)m_blk * GEMM_BM + ew * 32 + lane;
             const int64_t col_base = (int64_t)n_blk * BN;
             const int64_t col_end = col_base + BN < N ? col_base + BN : N;   // this tile's columns only
@@ -262,6 +301,7 @@ merged_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         }
     }
 
+    if (warp >= 4 && lane == 0) bulk_wait<0>();   // TMA stores complete before the CTA (and its smem) retire
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {

@@ -195,6 +195,10 @@ static ollie_status make_tmap_nhwc(CUtensorMap *m, const void *base, bool tf32, 
 }
 
 // ------------------------------------------------------------------------ merged GEMM launch
+static const bool g_gemm_no_tma_out = [] {   // OLLIE_GEMM_NO_TMA_OUT=1: thread-per-row stores (A/B switch)
+    const char *e = getenv("OLLIE_GEMM_NO_TMA_OUT");
+    return e && e[0] == '1';
+}();
 // UMMA N per tile: multiple of 16 in [16, 256] minimising the padded N, larger on ties.
 static int choose_bn(int64_t N) {
     int best = 256;
@@ -210,7 +214,7 @@ static int choose_bn(int64_t N) {
 }
 
 template <bool TF32, bool OUTBF16, bool RED = false>
-static ollie_status launch_gemm_t(const CUtensorMap &ta, const CUtensorMap &tb, const GemmArgs &ga,
+static ollie_status launch_gemm_t(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &to, const GemmArgs &ga,
                                   cudaStream_t stream) {
     auto kern = merged_gemm_kernel<TF32, OUTBF16, RED>;
     static bool attr_done[64] = {false};
@@ -222,7 +226,7 @@ static ollie_status launch_gemm_t(const CUtensorMap &ta, const CUtensorMap &tb, 
     }
     const int64_t tiles = ceil_div(ga.M, GEMM_BM) * ceil_div(ga.N, ga.BN);
     const int grid = (int)std::min<int64_t>(tiles, num_sms());
-    CUDA_TRY(launch(kern, dim3(grid), dim3(GEMM_THREADS), gemm_smem_bytes(), stream, ta, tb, ga));
+    CUDA_TRY(launch(kern, dim3(grid), dim3(GEMM_THREADS), gemm_smem_bytes(), stream, ta, tb, to, ga));
     return OLLIE_OK;
 }
 
@@ -244,10 +248,18 @@ static ollie_status run_gemm(int64_t M, int64_t N, int64_t K, bool tf32, const v
     if (st != OLLIE_OK) return st;
     st = make_tmap_2d(&tb, B, tf32, (uint64_t)K, (uint64_t)N, (uint64_t)(K * es), BK, (uint32_t)BN);
     if (st != OLLIE_OK) return st;
-    GemmArgs ga{M, N, K, BN, out, ldo, epi ? *epi : EpiArgs{}, red ? *red : RedArgs{}};
-    if (red) return tf32 ? launch_gemm_t<true, false, true>(ta, tb, ga, stream) : launch_gemm_t<false, false, true>(ta, tb, ga, stream);
-    if (tf32) return out_bf16 ? launch_gemm_t<true, true>(ta, tb, ga, stream) : launch_gemm_t<true, false>(ta, tb, ga, stream);
-    return out_bf16 ? launch_gemm_t<false, true>(ta, tb, ga, stream) : launch_gemm_t<false, false>(ta, tb, ga, stream);
+    GemmArgs ga{M, N, K, BN, out, ldo, 0, epi ? *epi : EpiArgs{}, red ? *red : RedArgs{}};
+    // fp32 output without an element-wise epilogue (the unfused plan's T): staged TMA stores
+    CUtensorMap to = tb;   // placeholder when unused
+    if (!red && !out_bf16 && !(epi && epi->on) && BN % 32 == 0 && aligned16(out) && (ldo * 4) % 16 == 0 &&
+        !g_gemm_no_tma_out) {   // (32-column store boxes must not cross into the next tile)
+        st = make_tmap_2d(&to, out, true, (uint64_t)N, (uint64_t)M, (uint64_t)(ldo * 4), 32, 32);
+        if (st != OLLIE_OK) return st;
+        ga.tma_out = 1;
+    }
+    if (red) return tf32 ? launch_gemm_t<true, false, true>(ta, tb, to, ga, stream) : launch_gemm_t<false, false, true>(ta, tb, to, ga, stream);
+    if (tf32) return out_bf16 ? launch_gemm_t<true, true>(ta, tb, to, ga, stream) : launch_gemm_t<true, false>(ta, tb, to, ga, stream);
+    return out_bf16 ? launch_gemm_t<false, true>(ta, tb, to, ga, stream) : launch_gemm_t<false, false>(ta, tb, to, ga, stream);
 }
 
 extern "C" ollie_status ollie_merged_gemm(int64_t M, int64_t N, int64_t K, ollie_dtype dtype, const void *A,
