@@ -123,7 +123,10 @@ size_t ollie_workspace_bytes(const ollie_conv_shape *shape, ollie_dtype dtype, i
  * selective addition (ConvTranspose2d), unfused (T through `ws`) or fused (a8, T lives
  * only in TMEM / shared memory).
  *   x_nhwc : [n][h][w][c]            dtype elements (device)
- *   w_prep : [r*s*f][c]              from ollie_prepare_weight_* (device)
+ *   w_prep : [r*s*f][c]              from ollie_prepare_weight_* (device); read-only for the
+ *                                    layer's lifetime: the fused kernel loads it before waiting
+ *                                    on the previous kernel of the stream (programmatic dependent
+ *                                    launch), which the weight DLT allows by never triggering early
  *   y_nhwc : [n][OH][OW][f]          dtype elements, fully overwritten (device)
  *   ws     : ollie_workspace_bytes() bytes (device), may be NULL if that is 0
  *   plan   : OLLIE_PLAN_AUTO / FUSED / UNFUSED

@@ -196,7 +196,8 @@ __global__ void __launch_bounds__(256) red_finish_kernel(const float *__restrict
 template <typename E>
 __global__ void __launch_bounds__(256) weight_dlt_kernel(const E *__restrict__ src, E *__restrict__ dst, int64_t F,
                                                          int64_t C, int64_t RS, int64_t sz, int64_t sc) {
-    pdl_launch_dependents();
+    // no early trigger: kernels after this one may load the prepared weights before their own
+    // griddepcontrol.wait (fused_conv), so they must not start until W' is complete
     pdl_wait();
     __shared__ E tile[32][33];
     const int64_t f = blockIdx.z;

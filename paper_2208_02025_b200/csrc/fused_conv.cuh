@@ -256,8 +256,9 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                             tma_prefetch_4d(&tmW, kc * (128 / ES), tc0.f0 + rank * fhalf, en.wj0, en.wi0 + g * a.grb * a.westr);
                     }
             }
-            pdl_wait();
-            FC_TRACE(2);
+            // Weights are read-only for the whole stream (the weight DLT never triggers its dependents
+            // early, ollie.h), so their smem loads go out BEFORE griddepcontrol.wait and overlap the
+            // previous kernel's tail: the resident slice, or the first step's weight boxes.
             if (a.resident && cid < a.num_items) {
                 // the CTA's f-slice is fixed (pair count is a multiple of f_slices): load it once
                 const TileCoord tc0 = fc_work<kPair>(a, cid, rank);
@@ -277,6 +278,27 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                         }
                     }
             }
+            int pre_b = 0;                   // weight boxes of the first step already issued
+            if (!a.resident && cid < a.num_items) {
+                const TileCoord tc = fc_work<kPair>(a, cid, rank);
+                const int q = ks > 1 ? q_lo : (cid / a.max_taps) % nq_all;
+                const int kc = q / a.nph;
+                const FusedClass &cl = a.cls[tc.cls * a.nph + (q - kc * a.nph)];
+                for (int g = 0; g < cl.ngroups && g < a.nb; ++g) {
+                    mbar_wait(&b_empty[bs], bp ^ 1);
+                    if (leader) mbar_arrive_expect_tx(&b_full[bs], xmul * (uint32_t)a.b_stage_bytes);
+                    uint8_t *dstB = sB + bs * a.b_stage_bytes;
+                    const int wi = cl.wi0 + g * a.grb * a.westr;
+                    if constexpr (kPair)
+                        tma_load_4d_pair(dstB, &tmW, &b_full[bs], kc * (128 / ES), tc.f0 + rank * fhalf, cl.wj0, wi);
+                    else
+                        tma_load_4d(dstB, &tmW, &b_full[bs], kc * (128 / ES), tc.f0, cl.wj0, wi);
+                    if (++bs == a.nb) { bs = 0; bp ^= 1; }
+                    ++pre_b;
+                }
+            }
+            pdl_wait();
+            FC_TRACE(2);
             for (int item = cid; item < a.num_items; item += ncl) {
                 const TileCoord tc = fc_work<kPair>(a, item, rank);
                 // steps (kc, ph): channel chunk kc of input phase ph -- one patch, that phase's taps.
@@ -301,7 +323,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                     }
                     if (++as == a.na) { as = 0; ap ^= 1; }
                     if (!a.resident) {
-                        for (int g = 0; g < cl.ngroups; ++g) {
+                        for (int g = (item == cid && qi == 0) ? pre_b : 0; g < cl.ngroups; ++g) {
                             mbar_wait(&b_empty[bs], bp ^ 1);
                             if (leader) mbar_arrive_expect_tx(&b_full[bs], xmul * (uint32_t)a.b_stage_bytes);
                             uint8_t *dstB = sB + bs * a.b_stage_bytes;
