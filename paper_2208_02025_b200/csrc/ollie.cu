@@ -213,6 +213,15 @@ static int choose_bn(int64_t N) {
     return best;
 }
 
+// Few tiles (small M): narrower N tiles spread the GEMM over more SMs -- a CTA's TMA ops and MMAs
+// are serial, so 18 CTAs x 256 columns lose to 72 x 64 (ResNet-18 512x7 batch 1).
+static int gemm_bn(int64_t M, int64_t N) {
+    int BN = choose_bn(N);
+    const int64_t mt = ceil_div(M, GEMM_BM);
+    while (BN % 64 == 0 && BN > 64 && mt * ceil_div(N, BN / 2) <= num_sms()) BN /= 2;
+    return BN;
+}
+
 template <bool TF32, bool OUTBF16, bool RED = false>
 static ollie_status launch_gemm_t(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &to, const GemmArgs &ga,
                                   cudaStream_t stream) {
@@ -241,7 +250,7 @@ static ollie_status run_gemm(int64_t M, int64_t N, int64_t K, bool tf32, const v
     if (!aligned16(A) || !aligned16(B)) return fail(OLLIE_E_ALIGN, "GEMM operand base not 16-byte aligned");
     if (M >= (1ll << 31) || N >= (1ll << 31) || K >= (1ll << 31))
         return fail(OLLIE_E_UNSUPPORTED, "GEMM extent exceeds int32 TMA coordinates");
-    const int BN = choose_bn(N);
+    const int BN = gemm_bn(M, N);
     const uint32_t BK = (uint32_t)(GEMM_BK_BYTES / es);
     CUtensorMap ta, tb;
     ollie_status st = make_tmap_2d(&ta, A, tf32, (uint64_t)K, (uint64_t)M, (uint64_t)(K * es), BK, GEMM_BM);
@@ -1681,11 +1690,11 @@ extern "C" ollie_status ollie_plan_describe(const ollie_conv_shape *s, ollie_dty
                  a.tmem_cols == 256 ? 2 : 1, a.pair, a.grb, a.nsb, a.ksplit);
     } else if (rp == OLLIE_PLAN_GEMM_RED) {
         snprintf(buf, len, "gemm_red BN=%d (%s as fp32 L2 reductions in the GEMM epilogue) + finish",
-                 choose_bn(s->r * s->s * s->f), transposed ? "selective add" : "OffsetAdd");
+                 gemm_bn(s->n * s->h * s->w, s->r * s->s * s->f), transposed ? "selective add" : "OffsetAdd");
     } else if (is_identity_offset_add(s, transposed)) {
-        snprintf(buf, len, "unfused-identity gemm BN=%d (OffsetAdd eliminated)", choose_bn(s->r * s->s * s->f));
+        snprintf(buf, len, "unfused-identity gemm BN=%d (OffsetAdd eliminated)", gemm_bn(s->n * s->h * s->w, s->r * s->s * s->f));
     } else {
-        snprintf(buf, len, "unfused gemm BN=%d ldT=%lld + %s", choose_bn(s->r * s->s * s->f), (long long)ldT_of(s),
+        snprintf(buf, len, "unfused gemm BN=%d ldT=%lld + %s", gemm_bn(s->n * s->h * s->w, s->r * s->s * s->f), (long long)ldT_of(s),
                  transposed ? "selective_add" : "offset_add");
     }
     return ok();
