@@ -17,7 +17,7 @@ for i, l in enumerate(layers):
     xs.append(x.cuda()); ws.append(w.cuda())
 st.prepare(ws)
 O._lib.ollie_debug_set_trace.argtypes = [ctypes.c_void_p]
-bufs = [torch.zeros(148 * 32, dtype=torch.int64, device="cuda") for _ in layers]
+bufs = [torch.zeros(4096 * 32, dtype=torch.int64, device="cuda") for _ in layers]
 s = torch.cuda.Stream()
 inputs = xs[0] if chained else xs
 with torch.cuda.stream(s):
@@ -40,19 +40,19 @@ for it in range(5):
     e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
 step_us = e0.elapsed_time(e1) * 1e3
 print(f"graph step {step_us:.1f} us")
-clk = 1.965e3  # cycles per us (max clock; clock64 deltas -> us)
+# trace slots (fused_conv.cuh FC_TRACE): %globaltimer ns; 30 = CTA entry, 29 = epilogue warp past the
+# final barrier (CTA exit), 0 = setup done, 1 = first A landed (MMA warp)
 prev_end = None
 for k, (sl, b) in enumerate(zip(st.layers, bufs)):
     t = b.view(-1, 32).cpu()
-    t = t[t[:, 30] != 0]
+    t = t[t[:, 30] != 0].double()
     if t.shape[0] == 0:
         print(f"{sl.layer.name:24s} (unfused / not traced) plan: {O.plan_describe(sl.conv.shape, sl.conv.code, sl.conv.plan, sl.conv.transposed)[:40]}")
         prev_end = None
         continue
-    start = t[:, 30].min().item()
-    end = (t[:, 30] + (t[:, 7].double() / clk * 1e3).long()).max().item()
-    setup = t[:, 0].double().median().item() / clk
-    a0 = t[:, 1].double().median().item() / clk
+    start, end = t[:, 30].min().item(), t[:, 29].max().item()
+    setup = ((t[:, 0] - t[:, 30]) / 1e3).median().item()
+    a0 = ((t[:, 1] - t[:, 30]) / 1e3).median().item()
     gap = (start - prev_end) / 1e3 if prev_end else float("nan")
     print(f"{sl.layer.name:24s} start->end {(end - start) / 1e3:7.2f} us  gap-before {gap:6.2f} us  "
           f"setup {setup:5.2f} us  first-data {a0:5.2f} us  CTAs {t.shape[0]}")

@@ -11,7 +11,7 @@
 using namespace ollie;
 
 __device__ __forceinline__ bool lane_is0() { return (threadIdx.x & 31) == 0; }
-__global__ void __launch_bounds__(128, 1) bench(int N, int nmma, int arow, int rnd, int m256, long long *out,
+__global__ void __launch_bounds__(256, 1) bench(int N, int nmma, int arow, int rnd, int m256, long long *out,
                                                int taps, int stw, int xb = 16) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -87,7 +87,14 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int nmma, int arow, int r
         mbar_wait(&bar, 0);
         if (lane_is0()) out[blockIdx.x] = clock64() - s0;
         if (lane_is0()) stop = 1;
-    } else if (threadIdx.x >= 64 && threadIdx.x < 96 && stw >= 4) {
+    } else if (threadIdx.x >= 64 && stw == 7) {
+        // other warps block in mbarrier.try_wait (like the fused kernel's producer / epilogue warps)
+        uint32_t ok = 0;
+        while (!stop) {
+            asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                         "selp.u32 %0, 1, 0, P1;\n}" : "=r"(ok) : "r"(smem_u32(&sink2)), "r"(0u) : "memory");
+        }
+    } else if (threadIdx.x >= 64 && threadIdx.x < 96 && stw >= 4 && stw < 7) {
         uint4 *dst = reinterpret_cast<uint4 *>(smem + 180 * 1024);
         int i = threadIdx.x - 64;
         while (!stop) {
@@ -112,6 +119,21 @@ int main(int argc, char **argv) {
     cudaMalloc(&d, 148 * sizeof(long long));
     cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     const int nmma = 36 * 128;
+    if (argc > 2) {   // blocked-waiter test: 128 vs 256 threads, other warps in try_wait
+        for (int thr : {128, 256})
+            for (int stw : {3, 7})
+                for (int N : {16, 32, 64, 128}) {
+                    bench<<<148, thr, 200 * 1024>>>(N, nmma, 0, 1, 1, d, 1, stw, 9);
+                    cudaError_t e = cudaDeviceSynchronize();
+                    if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+                    long long h[148];
+                    cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+                    long long mx = 0;
+                    for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+                    printf("threads=%d stw=%d N=%3d : %6.1f cyc/mma\n", thr, stw, N, (double)mx / nmma);
+                }
+        return 0;
+    }
     if (argc > 1) {   // row-pitch sweep: conv tap offsets (t/3)*xb + t%3 (the fused kernel's patch width)
         for (int xb : {16, 8, 9, 10, 13, 18, 30})
             for (int N : {32, 64, 128}) {
