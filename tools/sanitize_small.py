@@ -20,6 +20,13 @@ for lay in layers:
         except O.OllieError as e:
             if e.status != O.E_UNSUPPORTED:
                 raise
+# merged GEMM: TMA-store epilogue (BN % 32 == 0, M tail), narrow-N small-M tiles, row-store fallback
+for M, N, K in ((777, 1024, 64), (49, 4608, 128), (300, 200, 136)):
+    a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    b = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    ldT = (N + 3) // 4 * 4
+    T = torch.empty(M, ldT, device="cuda")
+    O.merged_gemm(M, N, K, O.BF16, a, b, T, ldT)
 for spec, shapes in ((ec.transpose_nchw_to_nhwc(2, 33, 5, 7), [(2, 33, 5, 7)]),
                      (ec.channel_pad(2, 5, 6, 3, 8), [(2, 5, 6, 3)]),
                      (ec.fused_pad_then_offset_add(1, 4, 5, 2, 3, 3, 1, 3), [(1, 4, 5, 18)])):
