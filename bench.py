@@ -347,31 +347,91 @@ def gpu_main(args):
         # and output through pinned host memory inside the timed region
         h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
         nl = len(stack.layers)
-        ev_in = [torch.cuda.Event() for _ in range(nl)]
-        ev_done = [torch.cuda.Event() for _ in range(nl)]
-        ev_out = [torch.cuda.Event() for _ in range(nl)]
-        e2e_s.record(stream)
-        h2d_s.wait_stream(stream)
-        d2h_s.wait_stream(stream)
-        for k in range(args.steps):
-            for i, sl in enumerate(stack.layers):
-                if k > 0:
-                    h2d_s.wait_event(ev_done[i])          # the previous step consumed in_dev[i]
+
+        # Inputs and outputs live in ONE pinned host buffer and ONE device buffer per direction
+        # (per-layer views at 256-byte offsets): a step is one H2D copy, the layers, one D2H copy.
+        # Eight per-layer copies per direction ran at ~31 GB/s (tools/pcie_check.py: chunked copy
+        # pattern) against ~48 GB/s per direction for one copy each way at once.  Two device buffer
+        # sets alternate between steps, so step k+1's H2D overlaps step k's layers and D2H.
+        def _flat(ts, pinned, device=None):
+            offs, tot = [], 0
+            for t in ts:
+                offs.append(tot)
+                tot += -(-t.numel() * t.element_size() // 256) * 256
+            buf = torch.empty(tot, dtype=torch.uint8, pin_memory=pinned, device=device)
+            views = [buf[o:o + t.numel() * t.element_size()].view(t.dtype).view(t.shape) for o, t in zip(offs, ts)]
+            return buf, views
+
+        flat_ok = all(sl.pad_eop is None for sl in stack.layers)
+        if flat_ok:
+            hin_buf, hin_views = _flat(in_host, True)
+            for v, t in zip(hin_views, in_host):
+                v.copy_(t)
+            hout_buf, hout_views = _flat(out_host, True)
+            din = [_flat(in_dev, False, dev) for _ in range(2)]
+            dout = [_flat(out_dev, False, dev) for _ in range(2)]
+            out_host[:] = hout_views          # results land in the flat host buffer's views
+            h2d, d2h = hin_buf.numel(), hout_buf.numel()   # bytes actually copied per step
+
+        def e2e_loop(nsteps):
+            if not flat_ok:
+                for k in range(nsteps):
+                    for i, sl in enumerate(stack.layers):
+                        in_dev[i].copy_(in_host[i], non_blocking=True)
+                        sl(in_dev[i], stream.cuda_stream)
+                        out_host[i].copy_(out_dev[i], non_blocking=True)
+                return
+            ev_in = [torch.cuda.Event() for _ in range(2)]
+            ev_done = [torch.cuda.Event() for _ in range(2)]
+            ev_out = [torch.cuda.Event() for _ in range(2)]
+            h2d_s.wait_stream(stream)
+            d2h_s.wait_stream(stream)
+            for k in range(nsteps):
+                b = k % 2
+                if k >= 2:
+                    h2d_s.wait_event(ev_done[b])              # step k-2's layers read this buffer
                 with torch.cuda.stream(h2d_s):
-                    in_dev[i].copy_(in_host[i], non_blocking=True)
-                    ev_in[i].record(h2d_s)
-                stream.wait_event(ev_in[i])
-                if k > 0:
-                    stream.wait_event(ev_out[i])          # the previous step's D2H read out_dev[i]
-                sl(in_dev[i], stream.cuda_stream)
-                ev_done[i].record(stream)
-                d2h_s.wait_event(ev_done[i])
+                    din[b][0].copy_(hin_buf, non_blocking=True)
+                    ev_in[b].record(h2d_s)
+                stream.wait_event(ev_in[b])
+                if k >= 2:
+                    stream.wait_event(ev_out[b])              # step k-2's D2H read this buffer
+                for i, sl in enumerate(stack.layers):
+                    sl.conv(din[b][1][i], dout[b][1][i], stream.cuda_stream)
+                ev_done[b].record(stream)
+                d2h_s.wait_event(ev_done[b])
                 with torch.cuda.stream(d2h_s):
-                    out_host[i].copy_(out_dev[i], non_blocking=True)
-                    ev_out[i].record(d2h_s)
-        stream.wait_stream(d2h_s)
-        e2e_e.record(stream)
+                    hout_buf.copy_(dout[b][0], non_blocking=True)
+                    ev_out[b].record(d2h_s)
+            stream.wait_stream(h2d_s)
+            stream.wait_stream(d2h_s)
+
+        # The K-step pipeline (every step's H2D, layers and D2H, cross-step overlap included) is
+        # captured from these same API calls into one CUDA graph, so the host's per-call launch
+        # cost (~80 runtime calls per step) does not pace the copy engines; eager if capture fails.
+        e2e_graph = None
+        if graph is not None:
+            try:
+                with torch.cuda.stream(stream):
+                    e2e_loop(1)                                   # warm-up (plans already tuned)
+                torch.cuda.synchronize()
+                e2e_graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(e2e_graph, stream=stream):
+                    e2e_loop(args.steps)
+                torch.cuda.synchronize()
+            except Exception:                                     # noqa: BLE001
+                e2e_graph = None
+                torch.cuda.synchronize()
+        e2e_mode = "cuda graph of the K-step pipeline" if e2e_graph is not None else "eager"
+        with torch.cuda.stream(stream):
+            e2e_s.record(stream)
+            if e2e_graph is not None:
+                e2e_graph.replay()
+            else:
+                e2e_loop(args.steps)
+            e2e_e.record(stream)
     else:
+        e2e_mode = "eager"
         with torch.cuda.stream(stream):
             e2e_s.record(stream)
             for k in range(args.steps):
@@ -515,6 +575,7 @@ def gpu_main(args):
                        "allgather": bool(gather_bufs is not None),
                        "parallelism": f"batch-sharded x{world}" if world > 1 else "1 GPU"},
             "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "mode": e2e_mode,
                     "ms_per_step": e2e_ms},
             "gpu_launches": stack.launches() * args.steps,
             "roofline": roof,
