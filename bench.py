@@ -431,13 +431,13 @@ def gpu_main(args):
                 e2e_loop(args.steps)
             e2e_e.record(stream)
     else:
-        e2e_mode = "eager"
+        e2e_mode = "copies + the step's CUDA graph" if graph is not None else "eager"
         with torch.cuda.stream(stream):
             e2e_s.record(stream)
             for k in range(args.steps):
                 for hd, dd in zip(in_host, in_dev):
                     dd.copy_(hd, non_blocking=True)
-                step()
+                replay()                  # the same API calls, captured once (eager with --no-graph)
                 gather()
                 for dd, hh in zip(out_dev, out_host):
                     hh.copy_(dd, non_blocking=True)
