@@ -72,6 +72,8 @@ struct FusedArgs {
     int32_t nph;                      // input phases per class (strided Conv2d: nonempty residues of i*dil-pad mod st)
     int32_t ist;                      // input stride of the patch (TMA element stride): st for Conv2d, 1 for ConvT
     int32_t XB, Yb, Xb, Yp;           // output cols / rows per tile, patch width / rows
+    int32_t ipt, Xr, ngrp;            // images per tile (interleaved patch rows [y][image][x]),
+                                      // patch row pitch Xr = ipt * Xb, image groups ceil(n / ipt)
     int32_t tiles_x, tiles_y, f_slices, FS, num_tiles;
     int32_t kchunks, BK;              // channel chunks of BK elements
     int32_t a_box_bytes;              // bytes TMA writes per patch load
@@ -125,8 +127,8 @@ __device__ __forceinline__ TileCoord fc_tile(const FusedArgs &a, int tile) {
     q /= a.tiles_x;
     const int ty = q % a.tiles_y;
     q /= a.tiles_y;
-    t.img = q % a.n;
-    t.cls = q / a.n;
+    t.img = (q % a.ngrp) * a.ipt;     // first image of the tile's group
+    t.cls = q / a.ngrp;
     t.y0 = ty * a.Yb * a.MT;
     t.x0 = tx * a.XB;
     t.f0 = fs * a.FS;
@@ -313,13 +315,13 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                     if (leader) mbar_arrive_expect_tx(&a_full[as], xmul * (uint32_t)a.a_box_bytes);
                     uint8_t *dstA = sA + as * a.a_stage_bytes;
                     if (a.sw128) {
-                        if constexpr (kPair) tma_load_4d_pair(dstA, &tmX, &a_full[as], kc * a.BK, xin, yin, tc.img);
-                        else tma_load_4d(dstA, &tmX, &a_full[as], kc * a.BK, xin, yin, tc.img);
+                        if constexpr (kPair) tma_load_4d_pair(dstA, &tmX, &a_full[as], kc * a.BK, xin, tc.img, yin);
+                        else tma_load_4d(dstA, &tmX, &a_full[as], kc * a.BK, xin, tc.img, yin);
                     } else {
                         if constexpr (kPair)
-                            tma_load_5d_pair(dstA, &tmX, &a_full[as], 0, xin, yin, tc.img, kc * (a.BK / CI));
+                            tma_load_5d_pair(dstA, &tmX, &a_full[as], 0, xin, tc.img, yin, kc * (a.BK / CI));
                         else
-                            tma_load_5d(dstA, &tmX, &a_full[as], 0, xin, yin, tc.img, kc * (a.BK / CI));
+                            tma_load_5d(dstA, &tmX, &a_full[as], 0, xin, tc.img, yin, kc * (a.BK / CI));
                     }
                     if (++as == a.na) { as = 0; ap ^= 1; }
                     if (!a.resident) {
@@ -368,7 +370,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         const uint64_t bdesc_t = ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
                                  ((uint64_t)2 << 61);
         const uint32_t lbo16 = (uint32_t)a.lbo >> 4;
-        const uint32_t mstride16 = (uint32_t)(a.Yb * a.Xb) * rowb16;    // stacked M-tiles, 16-byte units
+        const uint32_t mstride16 = (uint32_t)(a.Yb * a.Xr) * rowb16;    // stacked M-tiles, 16-byte units
         const uint32_t kstep16 = sw ? 2u : 2u * lbo16;                  // one K=16|8 step, 16-byte units
         const uint32_t sA16 = smem_u32(sA) >> 4, sB16 = smem_u32(sB) >> 4;
         const uint32_t astage16 = (uint32_t)a.a_stage_bytes >> 4, bstage16 = (uint32_t)a.b_stage_bytes >> 4;
@@ -528,7 +530,8 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         // ===== epilogue: TMEM -> registers -> Y (bf16 RNE or fp32), one output pixel per thread =====
         const int q = warp - 4;
         const int L = q * 32 + lane;
-        const int ly = L / a.Xb, lx = L - (L / a.Xb) * a.Xb;
+        // lane L = ly * Xr + k * Xb + lx: output row ly, image k of the tile's group, column lx
+        const int ly = L / a.Xr, lrem = L - ly * a.Xr, limg = lrem / a.Xb, lx = lrem - limg * a.Xb;
         int acc = 0;
         uint32_t accp = 0;
         const bool vec = (a.F % (kTF32 ? 4 : 8)) == 0;
@@ -573,10 +576,10 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                 } else {
                     mbar_wait_cluster(recv_full, rc & 1);
                     const int lr = L - krank * rpc;
-                    const int ly = L / a.Xb, lx = L - (L / a.Xb) * a.Xb;
                     const int oy = (tc.y0 + ly) * a.ost + cl.oy0, ox = (tc.x0 + lx) * a.ost + cl.ox0;
-                    const bool valid = tc.valid && ly < a.Yb && lx < a.XB && oy < a.OH && ox < a.OW;
-                    const int64_t pix = ((int64_t)tc.img * a.OH + oy) * a.OW + ox;
+                    const int img = tc.img + limg;
+                    const bool valid = tc.valid && ly < a.Yb && lx < a.XB && img < a.n && oy < a.OH && ox < a.OW;
+                    const int64_t pix = ((int64_t)img * a.OH + oy) * a.OW + ox;
                     for (int c0 = 0; c0 < a.FS; c0 += 32) {
                         uint32_t v[32];
                         tmem_ld_32x32b_x32(tbase + (uint32_t)c0, v);
@@ -652,8 +655,9 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             tc_fence_after();
             for (int m = 0; m < a.MT; ++m) {
                 const int oy = (tc.y0 + m * a.Yb + ly) * a.ost + cl.oy0, ox = (tc.x0 + lx) * a.ost + cl.ox0;
-                const bool valid = tc.valid && ly < a.Yb && lx < a.XB && oy < a.OH && ox < a.OW;
-                const int64_t pix = ((int64_t)tc.img * a.OH + oy) * a.OW + ox;
+                const int img = tc.img + limg;
+                const bool valid = tc.valid && ly < a.Yb && lx < a.XB && img < a.n && oy < a.OH && ox < a.OW;
+                const int64_t pix = ((int64_t)img * a.OH + oy) * a.OW + ox;
                 const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((acc * a.MT + m) * a.acc_cols);
                 // up to 64 columns per round: both TMEM loads in flight before one wait
                 for (int c0 = 0; c0 < a.FS; c0 += 64) {

@@ -286,6 +286,7 @@ extern "C" ollie_status ollie_merged_gemm(int64_t M, int64_t N, int64_t K, ollie
 static int g_force_mt = 0, g_force_fs = 0, g_force_res = -1;   // debug plan overrides (0 / -1 = auto)
 static int g_force_pair = -1;                                   // debug: -1 auto, 0 single CTAs, 1 CTA pairs
 static int g_force_ks = -1;                                     // debug: -1 auto, else the split-K factor
+static int g_force_ipt = 0;                                     // debug: 0 auto, else images per tile
 static thread_local double g_last_fused_cost = 0, g_last_unfused_cost = 0;
 static thread_local std::vector<FusedArgs> g_last_cands;
 
@@ -470,11 +471,19 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
     bool found = false;
     std::vector<std::pair<double, FusedArgs>> all;   // every evaluated plan (autotune candidates)
     for (int XB = (int)std::min<int64_t>(GW, 128); XB >= 1; --XB) {
-        const int Xb = XB + span_x;
-        if (Xb * ist > 256) continue;                // TMA box: <= 256 traversed elements
-        const int Yb = (int)std::min<int64_t>(GH, (128 - XB) / Xb + 1);
+      const int Xb = XB + span_x;
+      if (Xb * ist > 256) continue;                // TMA box: <= 256 traversed elements
+      // ipt > 1: several images share a tile, patch rows interleaved [y][image][x] (row pitch
+      // Xr = ipt * Xb), so every tap is still one row offset -- small images fill the 128 lanes
+      for (int ipt = 1; ipt <= 4; ++ipt) {
+        if (ipt > 1 && (GW > XB || base.n < ipt)) break;
+        if (g_force_ipt > 0 && ipt != g_force_ipt) continue;
+        const int Xr = ipt * Xb;
+        const int lanes_fixed = (ipt - 1) * Xb + XB;     // lanes of the last output row
+        if (lanes_fixed > 128) break;
+        const int Yb = (int)std::min<int64_t>(GH, (128 - lanes_fixed) / Xr + 1);
         if (Yb < 1) continue;
-        if (XB < std::min<int64_t>(GW, 128) && ceil_div(GW, XB) == ceil_div(GW, XB + 1) &&
+        if (ipt == 1 && XB < std::min<int64_t>(GW, 128) && ceil_div(GW, XB) == ceil_div(GW, XB + 1) &&
             (128 - (XB + 1)) / (Xb + 1) + 1 >= Yb)
             continue;
         for (int MT = 1; MT <= 4; ++MT) {
@@ -482,13 +491,13 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
             if (MT > 1 && (int64_t)(MT - 1) * Yb >= GH) break;
             const int Yp = MT * Yb + span_y;
             if (Yp * ist > 256) break;
-            const int max_off = span_y * Xb + span_x + (MT - 1) * Yb * Xb;
+            const int max_off = span_y * Xr + span_x + (MT - 1) * Yb * Xr;
             if (max_off >= 65536) break;
-            const int box = 16 * Xb * Yp * nchunk;   // same bytes in both layouts
-            const int need = sw128 ? (max_off + 128) * 128 : (nchunk - 1) * 16 * Xb * Yp + (max_off + 128) * 16;
+            const int box = 16 * Xb * Yp * ipt * nchunk;   // same bytes in both layouts
+            const int need = sw128 ? (max_off + 128) * 128 : (nchunk - 1) * 16 * Xb * Yp * ipt + (max_off + 128) * 16;
             const int astage = (int)ceil_div(std::max(box, need), 1024) * 1024;
             if (2 * astage > budget) break;
-            const int64_t items_sp = (int64_t)nclass * base.n * ceil_div(GW, XB) * ceil_div(GH, (int64_t)Yb * MT);
+            const int64_t items_sp = (int64_t)nclass * ceil_div(base.n, ipt) * ceil_div(GW, XB) * ceil_div(GH, (int64_t)Yb * MT);
             for (int FS : {(int)std::min<int64_t>(Fp, 256), 256, 192, 128, 96, 64, 48, 32, 16}) {
                 if (FS > Fp) continue;
                 if (g_force_fs > 0 && FS != g_force_fs) continue;
@@ -563,6 +572,7 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                     {
                         FusedArgs a = base;
                         a.XB = XB; a.Xb = Xb; a.Yb = Yb; a.Yp = Yp; a.MT = MT;
+                        a.ipt = ipt; a.Xr = Xr; a.ngrp = (int)ceil_div(base.n, ipt);
                         a.a_box_bytes = box; a.a_stage_bytes = astage;
                         a.FS = FS; a.acc_cols = acc_cols; a.nbuf = nbuf_o; a.b_stage_bytes = bstage_c;
                         a.b_tile_bytes = btile; a.nsb = nsb; a.grb = grb; a.westr = westr;
@@ -581,17 +591,18 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                 }
             }
         }
+      }
     }
     if (!found) return false;
     auto finalize = [&](FusedArgs a) -> FusedArgs {
-    a.lbo = 16 * a.Xb * a.Yp;
+    a.lbo = 16 * a.Xb * a.Yp * a.ipt;
     a.sw128 = sw128 ? 1 : 0;
     (void)rowbytes;
     a.tiles_x = (int)ceil_div(GW, a.XB);
     a.tiles_y = (int)ceil_div(GH, (int64_t)a.Yb * a.MT);
     a.f_slices = (int)ceil_div(s->f, a.FS);
-    a.num_tiles = (int)((int64_t)nclass * a.n * a.tiles_x * a.tiles_y * a.f_slices);
-    a.spatial = (int)((int64_t)nclass * a.n * a.tiles_x * a.tiles_y);
+    a.num_tiles = (int)((int64_t)nclass * a.ngrp * a.tiles_x * a.tiles_y * a.f_slices);
+    a.spatial = (int)((int64_t)nclass * a.ngrp * a.tiles_x * a.tiles_y);
     a.num_items = a.pair ? (int)(nclass * ceil_div(a.spatial / nclass, 2) * a.f_slices) : a.num_tiles;
     // class tables
     if (!transposed) {
@@ -610,8 +621,8 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
             // kernel row wi0 + westr*k reads subsampled-patch row q(k) - qmin with q(k) = q(0) + k*dil/g
             const int step = dil / gcd_i(st, dil);
             const int q0y = floordiv_i((int)(c.wi0 * dil - s->pad), st), q0x = floordiv_i((int)(c.wj0 * dil - s->pad), st);
-            c.a_base = (q0y - pg.qmin_y) * a.Xb + (q0x - pg.qmin_x);
-            c.a_dk = step * a.Xb;
+            c.a_base = (q0y - pg.qmin_y) * a.Xr + (q0x - pg.qmin_x);
+            c.a_dk = step * a.Xr;
             c.a_dl = step;
         }
     } else {
@@ -631,8 +642,8 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                 c.nr = g.ntaps_r;
                 c.ns = g.ntaps_s;
                 // kernel row i0 + st*k reads input row (tile row) + c_a - k: patch row nr-1-k
-                c.a_base = (g.ntaps_r - 1) * a.Xb + (g.ntaps_s - 1);
-                c.a_dk = -a.Xb;
+                c.a_base = (g.ntaps_r - 1) * a.Xr + (g.ntaps_s - 1);
+                c.a_dk = -a.Xr;
                 c.a_dl = -1;
             }
     }
@@ -659,7 +670,7 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
         if ((int)g_last_cands.size() >= 40) break;
         bool dup = false;
         for (auto &d : g_last_cands)
-            dup |= d.MT == c.second.MT && d.FS == c.second.FS && d.resident == c.second.resident &&
+            dup |= d.MT == c.second.MT && d.FS == c.second.FS && d.resident == c.second.resident && d.ipt == c.second.ipt &&
                    d.tmem_cols == c.second.tmem_cols && d.pair == c.second.pair && d.ksplit == c.second.ksplit;
         if (!dup && c.first < 4.0 * best) g_last_cands.push_back(finalize(c.second));
     }
@@ -692,7 +703,7 @@ static std::map<PlanKey, PlanEntry> g_plan_cache;
 static PlanEntry *plan_entry_mut(const ollie_conv_shape *s, bool tf32, int transposed, int64_t OH, int64_t OW) {
     PlanKey k{{s->n, s->c, s->h, s->w, s->f, s->r * 65536 + s->s, s->pad, s->stride * 65536 + s->dilation,
                (int64_t)tf32 * 2 + transposed + 4 * (int64_t)s->output_padding, num_sms(),
-               g_force_mt * 1000 + g_force_fs, (g_force_res * 16 + g_force_pair) * 16 + g_force_ks}};
+               g_force_mt * 1000 + g_force_fs + 1000000 * g_force_ipt, (g_force_res * 16 + g_force_pair) * 16 + g_force_ks}};
     {
         std::lock_guard<std::mutex> g(g_plan_mu);
         auto it = g_plan_cache.find(k);
@@ -845,22 +856,25 @@ static ollie_status run_fused(const ollie_conv_shape *s, bool tf32, int transpos
     // strided Conv2d: the patch is the subsampled image of one input phase, traversed with element
     // stride ist along w and h (ist * Xb traversed elements load Xb pixels)
     const uint32_t ist = (uint32_t)a.ist;
-    if (a.sw128) {   // X as 4-D NHWC {c, w, h, n}, box = 128-byte pixel rows, SWIZZLE_128B
-        cuuint64_t dims[4] = {(cuuint64_t)s->c, (cuuint64_t)s->w, (cuuint64_t)s->h, (cuuint64_t)s->n};
-        cuuint64_t strides[3] = {(cuuint64_t)(s->c * es), (cuuint64_t)(s->w * s->c * es),
-                                 (cuuint64_t)(s->h * s->w * s->c * es)};
-        cuuint32_t box[4] = {(cuuint32_t)a.BK, (cuuint32_t)(a.Xb * ist), (cuuint32_t)(a.Yp * ist), 1};
-        cuuint32_t estr[4] = {1, ist, ist, 1};
+    // X is viewed with dims ordered {c, w, n, h} (strides need not be monotonic), so a box of ipt
+    // images lands in smem as [y][image][x] rows: the interleaved patch of multi-image tiles
+    if (a.sw128) {   // X as 4-D {c, w, n, h}, box = 128-byte pixel rows, SWIZZLE_128B
+        cuuint64_t dims[4] = {(cuuint64_t)s->c, (cuuint64_t)s->w, (cuuint64_t)s->n, (cuuint64_t)s->h};
+        cuuint64_t strides[3] = {(cuuint64_t)(s->c * es), (cuuint64_t)(s->h * s->w * s->c * es),
+                                 (cuuint64_t)(s->w * s->c * es)};
+        cuuint32_t box[4] = {(cuuint32_t)a.BK, (cuuint32_t)(a.Xb * ist), (cuuint32_t)a.ipt, (cuuint32_t)(a.Yp * ist)};
+        cuuint32_t estr[4] = {1, ist, 1, ist};
         CUresult r = enc(&tx, dt, 4, const_cast<void *>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (patch 4d) failed (%d)", (int)r);
-    } else {   // X as 5-D planar view {c_in (16 B), w, h, n, c_out}
-        cuuint64_t dims[5] = {(cuuint64_t)CI, (cuuint64_t)s->w, (cuuint64_t)s->h, (cuuint64_t)s->n,
+    } else {   // X as 5-D planar view {c_in (16 B), w, n, h, c_out}
+        cuuint64_t dims[5] = {(cuuint64_t)CI, (cuuint64_t)s->w, (cuuint64_t)s->n, (cuuint64_t)s->h,
                               (cuuint64_t)(s->c / CI)};
-        cuuint64_t strides[4] = {(cuuint64_t)(s->c * es), (cuuint64_t)(s->w * s->c * es),
-                                 (cuuint64_t)(s->h * s->w * s->c * es), 16};
-        cuuint32_t box[5] = {(cuuint32_t)CI, (cuuint32_t)(a.Xb * ist), (cuuint32_t)(a.Yp * ist), 1, (cuuint32_t)(a.BK / CI)};
-        cuuint32_t estr[5] = {1, ist, ist, 1, 1};
+        cuuint64_t strides[4] = {(cuuint64_t)(s->c * es), (cuuint64_t)(s->h * s->w * s->c * es),
+                                 (cuuint64_t)(s->w * s->c * es), 16};
+        cuuint32_t box[5] = {(cuuint32_t)CI, (cuuint32_t)(a.Xb * ist), (cuuint32_t)a.ipt, (cuuint32_t)(a.Yp * ist),
+                             (cuuint32_t)(a.BK / CI)};
+        cuuint32_t estr[5] = {1, ist, 1, ist, 1};
         CUresult r = enc(&tx, dt, 5, const_cast<void *>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (patch) failed (%d)", (int)r);
@@ -1684,10 +1698,10 @@ extern "C" ollie_status ollie_plan_describe(const ollie_conv_shape *s, ollie_dty
         snprintf(buf, len,
                  "fused XB=%d Yb=%d Xb=%d Yp=%d MT=%d FS=%d f_slices=%d resident=%d nbuf=%d na=%d nb=%d BK=%d "
                  "kchunks=%d tiles=%d grid=%d smem=%zu classes=%d phases=%d ist=%d taps=%d sw128=%d ctas_per_sm=%d "
-                 "pair=%d wbox=%dx%d ksplit=%d",
+                 "pair=%d wbox=%dx%d ksplit=%d ipt=%d",
                  a.XB, a.Yb, a.Xb, a.Yp, a.MT, a.FS, a.f_slices, a.resident, a.nbuf, a.na, a.nb, a.BK, a.kchunks,
                  a.num_tiles, fused_grid(a), fused_smem_bytes(a), a.nclass, a.nph, a.ist, a.max_taps, a.sw128,
-                 a.tmem_cols == 256 ? 2 : 1, a.pair, a.grb, a.nsb, a.ksplit);
+                 a.tmem_cols == 256 ? 2 : 1, a.pair, a.grb, a.nsb, a.ksplit, a.ipt);
     } else if (rp == OLLIE_PLAN_GEMM_RED) {
         snprintf(buf, len, "gemm_red BN=%d (%s as fp32 L2 reductions in the GEMM epilogue) + finish",
                  gemm_bn(s->n * s->h * s->w, s->r * s->s * s->f), transposed ? "selective add" : "OffsetAdd");
@@ -1714,6 +1728,8 @@ extern "C" void ollie_debug_force_plan(int mt, int fs, int resident) {
 extern "C" void ollie_debug_force_pair(int pair) { g_force_pair = pair; }
 // Debug hook (not part of include/ollie.h): -1 auto, else only plans with this split-K factor.
 extern "C" void ollie_debug_force_ksplit(int ks) { g_force_ks = ks; }
+// Debug hook (not part of include/ollie.h): 0 auto, else only plans with this many images per tile.
+extern "C" void ollie_debug_force_ipt(int ipt) { g_force_ipt = ipt; }
 
 // ------------------------------------------------------------------------ autotune
 extern "C" ollie_status ollie_autotune_derived(const ollie_conv_shape *s, ollie_dtype dtype, int transposed,
