@@ -54,6 +54,24 @@ O._lib.ollie_debug_force_ksplit(-1)
 lay = syn.Layer("s", 1, 64, 13, 11, 64, 3, 3, pad=1, stride=2)
 x, w = syn.layer_inputs(lay, 5)
 DerivedConv.from_layer(lay, plan=O.PLAN_FUSED, autotune=False).prepare(w.cuda())(x.cuda())
+# multi-image tiles (ipt 2 / 3; ragged batch, split-K, strided phases, ConvT classes)
+for lay, ipt, ks in ((syn.Layer("i7", 3, 64, 7, 7, 64, 3, 3, pad=1), 2, -1),
+                     (syn.Layer("i7k", 3, 128, 7, 7, 64, 3, 3, pad=1), 2, 2),
+                     (syn.Layer("is2", 3, 64, 10, 10, 64, 3, 3, pad=1, stride=2), 3, -1),
+                     (syn.Layer("it", 3, 64, 4, 4, 32, 4, 4, pad=1, stride=2, transposed=True), 2, -1)):
+    O._lib.ollie_debug_force_ipt(ipt)
+    O._lib.ollie_debug_force_ksplit(ks)
+    x, w = syn.layer_inputs(lay, 8)
+    try:
+        conv = DerivedConv.from_layer(lay, plan=O.PLAN_FUSED, autotune=False).prepare(w.cuda())
+        conv(x.cuda())
+        torch.cuda.synchronize()
+        print("ran", lay.name, O.plan_describe(conv.shape, conv.code, O.PLAN_FUSED, lay.transposed)[-30:], flush=True)
+    except O.OllieError as e:
+        if e.status != O.E_UNSUPPORTED:
+            raise
+O._lib.ollie_debug_force_ipt(0)
+O._lib.ollie_debug_force_ksplit(-1)
 # NEXT-1 and NEXT-4
 from paper_2208_02025_b200 import DilatedAsDense
 lay = syn.Layer("dd", 1, 16, 10, 12, 16, 3, 3, pad=2, dilation=2)
