@@ -47,6 +47,7 @@ constexpr uint32_t FC_TMEM_COLS = 512;
 constexpr int FC_SMEM_BUDGET = 225 * 1024;
 constexpr int FC_MAX_CLASSES = 9;            // table entries: ConvT output classes x strided-conv input phases
 constexpr int FC_MAX_TAPS = 32;
+constexpr int FC_YSTAGE_BYTES = 128 * 128;   // Y staging: <= 128 output pixels x one 128-byte channel chunk
 // split-K receive buffer: (ks - 1) senders x (128 / ks) owned rows x FS fp32 (host sizes it)
 __host__ __device__ constexpr int fc_red_bytes(int ks, int FS) { return ks > 1 ? (ks - 1) * (128 / ks) * FS * 4 : 0; }
 
@@ -72,6 +73,7 @@ struct FusedArgs {
     int32_t nph;                      // input phases per class (strided Conv2d: nonempty residues of i*dil-pad mod st)
     int32_t ist;                      // input stride of the patch (TMA element stride): st for Conv2d, 1 for ConvT
     int32_t XB, Yb, Xb, Yp;           // output cols / rows per tile, patch width / rows
+    int32_t tma_y;                    // 1: Y tiles leave through a SWIZZLE_128B smem stage + TMA stores
     int32_t ipt, Xr, ngrp;            // images per tile (interleaved patch rows [y][image][x]),
                                       // patch row pitch Xr = ipt * Xb, image groups ceil(n / ipt)
     int32_t tiles_x, tiles_y, f_slices, FS, num_tiles;
@@ -159,7 +161,7 @@ __device__ __forceinline__ TileCoord fc_work(const FusedArgs &a, int item, int r
 template <bool kTF32, bool kPair, bool kOneEntry, bool kSplit>
 __global__ void __launch_bounds__(FC_THREADS, 2)
 fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
-                  const __grid_constant__ FusedArgs a) {
+                  const __grid_constant__ CUtensorMap tmY, const __grid_constant__ FusedArgs a) {
     constexpr int ES = kTF32 ? 4 : 2;
     constexpr int CI = 16 / ES;                  // elements per 16-byte planar chunk
     constexpr int KI = 32 / ES;                  // K per tcgen05.mma (16 bf16 / 8 tf32)
@@ -172,7 +174,9 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     uint8_t *sB = sA + a.na * a.a_stage_bytes;
     // split-K receive buffer: [sender slot][FS/4 float4 column groups][owned rows]
     float4 *sRed = reinterpret_cast<float4 *>(sB + b_region);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sB + b_region + (kSplit ? fc_red_bytes(a.ksplit, a.FS) : 0));
+    // Y staging (tma_y plans, never split-K): 1024-aligned since stages and tiles are
+    uint8_t *sY = sB + b_region + (kSplit ? fc_red_bytes(a.ksplit, a.FS) : 0);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sY + (a.tma_y ? FC_YSTAGE_BYTES : 0));
     uint64_t *a_full = bars;
     uint64_t *a_empty = a_full + a.na;
     uint64_t *b_full = a_empty + a.na;      // [nb]   (resident: b_full[0] = "all weights loaded")
@@ -659,6 +663,50 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                 const bool valid = tc.valid && ly < a.Yb && lx < a.XB && img < a.n && oy < a.OH && ox < a.OW;
                 const int64_t pix = ((int64_t)img * a.OH + oy) * a.OW + ox;
                 const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((acc * a.MT + m) * a.acc_cols);
+                if (a.tma_y) {
+                    // One 128-byte channel chunk at a time: every lane of the tile writes its pixel's chunk
+                    // into the SWIZZLE_128B stage (row = (y * ipt + image) * XB + x, the TMA box order
+                    // {c, x, image, y}), then one thread stores the whole Yb x ipt x XB box; rows / images /
+                    // channels past the tensor are clipped by TMA.  Full-line writes instead of
+                    // thread-per-pixel 16-byte stores (which cost 1-2 us per layer, OLLIE_FC_DBG=4).
+                    constexpr int CB = kTF32 ? 32 : 64;          // channels per 128-byte row
+                    const bool in_tile = ly < a.Yb && lx < a.XB;
+                    const int srow = (ly * a.ipt + limg) * a.XB + lx;
+                    for (int c0 = 0; c0 < a.FS; c0 += CB) {
+                        uint32_t v[64];
+                        tmem_ld_32x32b_x32(tbase + (uint32_t)c0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+                        if (!kTF32) tmem_ld_32x32b_x32(tbase + (uint32_t)(c0 + 32), *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+                        tmem_ld_wait();
+                        const int f = tc.f0 + c0;
+                        if (a.epi.on && valid && f < a.F)
+                            epi_apply_bits<!kTF32, 64>(a.epi, v, pix * a.F + f, f, min(min(CB, a.FS - c0), a.F - f));
+                        if (threadIdx.x == 128) bulk_wait_read<0>();   // the stage's previous store has read it
+                        named_bar_sync(1, 128);
+                        if (in_tile) {
+                            uint8_t *row = sY + srow * 128;
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                uint4 pk;
+                                if constexpr (kTF32) {
+                                    pk = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                                } else {
+                                    pk.x = pack_bf16x2_rn(__uint_as_float(v[8 * j]), __uint_as_float(v[8 * j + 1]));
+                                    pk.y = pack_bf16x2_rn(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+                                    pk.z = pack_bf16x2_rn(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+                                    pk.w = pack_bf16x2_rn(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+                                }
+                                *reinterpret_cast<uint4 *>(row + ((j ^ (srow & 7)) << 4)) = pk;
+                            }
+                        }
+                        fence_proxy_async_smem();
+                        named_bar_sync(1, 128);
+                        if (threadIdx.x == 128 && tc.valid) {   // (the odd CTA of a last pair stores nothing)
+                            tma_store_4d(&tmY, sY, f, tc.x0, tc.img, tc.y0 + m * a.Yb);
+                            bulk_commit();
+                        }
+                    }
+                    continue;
+                }
                 // up to 64 columns per round: both TMEM loads in flight before one wait
                 for (int c0 = 0; c0 < a.FS; c0 += 64) {
                     uint32_t v[64];
@@ -712,6 +760,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             if (threadIdx.x == 128 && item == cid) FC_TRACE(5);
             if (++acc == a.nbuf) { acc = 0; accp ^= 1; }
         }
+        if (a.tma_y && threadIdx.x == 128) bulk_wait<0>();   // Y stores complete before the stage retires
         if (ks > 1 && rc > 0 && (L / (128 / ks)) != krank) {
             // pusher warps: the owners' last "consumed" arrives must land before this CTA may leave
             mbar_wait_cluster(peer_done, (rc - 1) & 1);

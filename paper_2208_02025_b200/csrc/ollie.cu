@@ -287,6 +287,10 @@ static int g_force_mt = 0, g_force_fs = 0, g_force_res = -1;   // debug plan ove
 static int g_force_pair = -1;                                   // debug: -1 auto, 0 single CTAs, 1 CTA pairs
 static int g_force_ks = -1;                                     // debug: -1 auto, else the split-K factor
 static int g_force_ipt = 0;                                     // debug: 0 auto, else images per tile
+static const bool g_no_tma_y = [] {   // OLLIE_NO_TMA_Y=1: fused-kernel Y by thread stores (A/B switch)
+    const char *e = getenv("OLLIE_NO_TMA_Y");
+    return e && e[0] == '1';
+}();
 static thread_local double g_last_fused_cost = 0, g_last_unfused_cost = 0;
 static thread_local std::vector<FusedArgs> g_last_cands;
 
@@ -525,7 +529,12 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                     const int btile = pair ? bstage / 2 : bstage;      // one tap's tile in this CTA
                     const int64_t items_c = pair ? nclass * ceil_div(items_sp / nclass, 2) * slices : items;
                     // occ = 2: two CTAs per SM, each with half the smem and 256 TMEM columns
-                    const int bud = (occ == 1 ? budget : (113 * 1024 - 2048)) - fc_red_bytes(ksp, FS);
+                    // Y through a smem stage + TMA stores: Conv2d (one output class), no split-K, whole
+                    // 128-byte channel chunks per slice, 16-byte output rows
+                    const int tma_y = (!transposed && ksp == 1 && FS % (128 / es) == 0 && (s->f * es) % 16 == 0 &&
+                                       !g_no_tma_y) ? 1 : 0;
+                    const int bud = (occ == 1 ? budget : (113 * 1024 - 2048)) - fc_red_bytes(ksp, FS) -
+                                    (tma_y ? FC_YSTAGE_BYTES : 0);
                     const int nbuf_o = occ == 1 ? nbuf : (2 * MT * acc_cols <= 256 ? 2 : 1);
                     if (occ == 2 && MT * acc_cols > 256) continue;
                     // largest weight box (fewest TMA ops) that fits: grb kernel rows per box
@@ -573,6 +582,7 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                         FusedArgs a = base;
                         a.XB = XB; a.Xb = Xb; a.Yb = Yb; a.Yp = Yp; a.MT = MT;
                         a.ipt = ipt; a.Xr = Xr; a.ngrp = (int)ceil_div(base.n, ipt);
+                        a.tma_y = tma_y;
                         a.a_box_bytes = box; a.a_stage_bytes = astage;
                         a.FS = FS; a.acc_cols = acc_cols; a.nbuf = nbuf_o; a.b_stage_bytes = bstage_c;
                         a.b_tile_bytes = btile; a.nsb = nsb; a.grb = grb; a.westr = westr;
@@ -742,7 +752,8 @@ static int fused_grid(const FusedArgs &a, int max_units = 0) {
 
 static size_t fused_smem_bytes(const FusedArgs &a) {
     const size_t b_region = a.resident ? (size_t)a.kchunks * a.kc_tiles * a.b_tile_bytes : (size_t)a.nb * a.b_stage_bytes;
-    return 1024 + (size_t)a.na * a.a_stage_bytes + b_region + (size_t)fc_red_bytes(a.ksplit, a.FS) + 1024;
+    return 1024 + (size_t)a.na * a.a_stage_bytes + b_region + (size_t)fc_red_bytes(a.ksplit, a.FS) +
+           (a.tma_y ? FC_YSTAGE_BYTES : 0) + 1024;
 }
 
 static bool out_hw(const ollie_conv_shape *s, int transposed, int64_t *OH, int64_t *OW) {
@@ -784,7 +795,8 @@ static bool fused_preferred(const ollie_conv_shape *s, bool tf32, int transposed
 }
 
 template <bool TF32, bool PAIR, bool ONE, bool SPLIT>
-static ollie_status launch_fused_t(const CUtensorMap &tx, const CUtensorMap &tw, const FusedArgs &a, cudaStream_t stream) {
+static ollie_status launch_fused_t(const CUtensorMap &tx, const CUtensorMap &tw, const CUtensorMap &ty, const FusedArgs &a,
+                                   cudaStream_t stream) {
     auto kern = fused_conv_kernel<TF32, PAIR, ONE, SPLIT>;
     static bool attr_done[64] = {false};
     int dev = 0;
@@ -825,9 +837,9 @@ static ollie_status launch_fused_t(const CUtensorMap &tx, const CUtensorMap &tw,
                 cache[key] = maxc;
             }
         }
-        CUDA_TRY(launch_cluster(kern, dim3(fused_grid(a, maxc)), dim3(FC_THREADS), smem, stream, csz, tx, tw, a));
+        CUDA_TRY(launch_cluster(kern, dim3(fused_grid(a, maxc)), dim3(FC_THREADS), smem, stream, csz, tx, tw, ty, a));
     } else
-        CUDA_TRY(launch(kern, dim3(fused_grid(a)), dim3(FC_THREADS), fused_smem_bytes(a), stream, tx, tw, a));
+        CUDA_TRY(launch(kern, dim3(fused_grid(a)), dim3(FC_THREADS), fused_smem_bytes(a), stream, tx, tw, ty, a));
     return OLLIE_OK;
 }
 
@@ -892,17 +904,34 @@ static ollie_status run_fused(const ollie_conv_shape *s, bool tf32, int transpos
                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (weights) failed (%d)", (int)r);
     }
+    // Y as 4-D {f, ow, n, oh} (the tile's box {128-byte channel chunk, XB, ipt, Yb} in the stage's row
+    // order); without a usable map (misaligned Y) the kernel falls back to thread stores
+    CUtensorMap ty = tx;
+    if (a.tma_y) {
+        if (!aligned16(y)) {
+            a.tma_y = 0;   // (the stage stays reserved in smem; only the store path changes)
+        } else {
+            cuuint64_t dims[4] = {(cuuint64_t)s->f, (cuuint64_t)OW, (cuuint64_t)s->n, (cuuint64_t)OH};
+            cuuint64_t strides[3] = {(cuuint64_t)(s->f * es), (cuuint64_t)(OH * OW * s->f * es),
+                                     (cuuint64_t)(OW * s->f * es)};
+            cuuint32_t box[4] = {(cuuint32_t)(128 / es), (cuuint32_t)a.XB, (cuuint32_t)a.ipt, (cuuint32_t)a.Yb};
+            cuuint32_t estr[4] = {1, 1, 1, 1};
+            CUresult r = enc(&ty, dt, 4, y, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (Y store) failed (%d)", (int)r);
+        }
+    }
     const bool one = a.nclass * a.nph == 1;
     if (a.pair) {
-        if (one) return tf32 ? launch_fused_t<true, true, true, false>(tx, tw, a, stream) : launch_fused_t<false, true, true, false>(tx, tw, a, stream);
-        return tf32 ? launch_fused_t<true, true, false, false>(tx, tw, a, stream) : launch_fused_t<false, true, false, false>(tx, tw, a, stream);
+        if (one) return tf32 ? launch_fused_t<true, true, true, false>(tx, tw, ty, a, stream) : launch_fused_t<false, true, true, false>(tx, tw, ty, a, stream);
+        return tf32 ? launch_fused_t<true, true, false, false>(tx, tw, ty, a, stream) : launch_fused_t<false, true, false, false>(tx, tw, ty, a, stream);
     }
     if (a.ksplit > 1) {
-        if (one) return tf32 ? launch_fused_t<true, false, true, true>(tx, tw, a, stream) : launch_fused_t<false, false, true, true>(tx, tw, a, stream);
-        return tf32 ? launch_fused_t<true, false, false, true>(tx, tw, a, stream) : launch_fused_t<false, false, false, true>(tx, tw, a, stream);
+        if (one) return tf32 ? launch_fused_t<true, false, true, true>(tx, tw, ty, a, stream) : launch_fused_t<false, false, true, true>(tx, tw, ty, a, stream);
+        return tf32 ? launch_fused_t<true, false, false, true>(tx, tw, ty, a, stream) : launch_fused_t<false, false, false, true>(tx, tw, ty, a, stream);
     }
-    if (one) return tf32 ? launch_fused_t<true, false, true, false>(tx, tw, a, stream) : launch_fused_t<false, false, true, false>(tx, tw, a, stream);
-    return tf32 ? launch_fused_t<true, false, false, false>(tx, tw, a, stream) : launch_fused_t<false, false, false, false>(tx, tw, a, stream);
+    if (one) return tf32 ? launch_fused_t<true, false, true, false>(tx, tw, ty, a, stream) : launch_fused_t<false, false, true, false>(tx, tw, ty, a, stream);
+    return tf32 ? launch_fused_t<true, false, false, false>(tx, tw, ty, a, stream) : launch_fused_t<false, false, false, false>(tx, tw, ty, a, stream);
 }
 
 // ------------------------------------------------------------------------ shapes
@@ -1698,10 +1727,10 @@ extern "C" ollie_status ollie_plan_describe(const ollie_conv_shape *s, ollie_dty
         snprintf(buf, len,
                  "fused XB=%d Yb=%d Xb=%d Yp=%d MT=%d FS=%d f_slices=%d resident=%d nbuf=%d na=%d nb=%d BK=%d "
                  "kchunks=%d tiles=%d grid=%d smem=%zu classes=%d phases=%d ist=%d taps=%d sw128=%d ctas_per_sm=%d "
-                 "pair=%d wbox=%dx%d ksplit=%d ipt=%d",
+                 "pair=%d wbox=%dx%d ksplit=%d ipt=%d tma_y=%d",
                  a.XB, a.Yb, a.Xb, a.Yp, a.MT, a.FS, a.f_slices, a.resident, a.nbuf, a.na, a.nb, a.BK, a.kchunks,
                  a.num_tiles, fused_grid(a), fused_smem_bytes(a), a.nclass, a.nph, a.ist, a.max_taps, a.sw128,
-                 a.tmem_cols == 256 ? 2 : 1, a.pair, a.grb, a.nsb, a.ksplit, a.ipt);
+                 a.tmem_cols == 256 ? 2 : 1, a.pair, a.grb, a.nsb, a.ksplit, a.ipt, a.tma_y);
     } else if (rp == OLLIE_PLAN_GEMM_RED) {
         snprintf(buf, len, "gemm_red BN=%d (%s as fp32 L2 reductions in the GEMM epilogue) + finish",
                  gemm_bn(s->n * s->h * s->w, s->r * s->s * s->f), transposed ? "selective add" : "OffsetAdd");
