@@ -673,35 +673,43 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                     const bool in_tile = ly < a.Yb && lx < a.XB;
                     const int srow = (ly * a.ipt + limg) * a.XB + lx;
                     for (int c0 = 0; c0 < a.FS; c0 += CB) {
-                        uint32_t v[64];
-                        tmem_ld_32x32b_x32(tbase + (uint32_t)c0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
-                        if (!kTF32) tmem_ld_32x32b_x32(tbase + (uint32_t)(c0 + 32), *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
-                        tmem_ld_wait();
-                        const int f = tc.f0 + c0;
-                        if (a.epi.on && valid && f < a.F)
-                            epi_apply_bits<!kTF32, 64>(a.epi, v, pix * a.F + f, f, min(min(CB, a.FS - c0), a.F - f));
                         if (threadIdx.x == 128) bulk_wait_read<0>();   // the stage's previous store has read it
                         named_bar_sync(1, 128);
-                        if (in_tile) {
-                            uint8_t *row = sY + srow * 128;
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) {
-                                uint4 pk;
+                        // 32 columns at a time (bf16: two halves of the 128-byte row) keeps the epilogue
+                        // within the register budget of the 2-CTA/SM variants
+#pragma unroll 1
+                        for (int h = 0; h < CB; h += 32) {
+                            uint32_t v[32];
+                            tmem_ld_32x32b_x32(tbase + (uint32_t)(c0 + h), v);
+                            tmem_ld_wait();
+                            const int f = tc.f0 + c0 + h;
+                            if (a.epi.on && valid && f < a.F)
+                                epi_apply_bits<!kTF32, 32>(a.epi, v, pix * a.F + f, f, min(min(32, a.FS - c0 - h), a.F - f));
+                            if (in_tile) {
+                                uint8_t *row = sY + srow * 128;
                                 if constexpr (kTF32) {
-                                    pk = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+#pragma unroll
+                                    for (int j = 0; j < 8; ++j)
+                                        *reinterpret_cast<uint4 *>(row + ((j ^ (srow & 7)) << 4)) =
+                                            make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
                                 } else {
-                                    pk.x = pack_bf16x2_rn(__uint_as_float(v[8 * j]), __uint_as_float(v[8 * j + 1]));
-                                    pk.y = pack_bf16x2_rn(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
-                                    pk.z = pack_bf16x2_rn(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
-                                    pk.w = pack_bf16x2_rn(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+#pragma unroll
+                                    for (int j = 0; j < 4; ++j) {
+                                        uint4 pk;
+                                        pk.x = pack_bf16x2_rn(__uint_as_float(v[8 * j]), __uint_as_float(v[8 * j + 1]));
+                                        pk.y = pack_bf16x2_rn(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+                                        pk.z = pack_bf16x2_rn(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+                                        pk.w = pack_bf16x2_rn(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+                                        const int jj = (h >> 3) + j;          // 16-byte chunk of the row
+                                        *reinterpret_cast<uint4 *>(row + ((jj ^ (srow & 7)) << 4)) = pk;
+                                    }
                                 }
-                                *reinterpret_cast<uint4 *>(row + ((j ^ (srow & 7)) << 4)) = pk;
                             }
                         }
                         fence_proxy_async_smem();
                         named_bar_sync(1, 128);
                         if (threadIdx.x == 128 && tc.valid) {   // (the odd CTA of a last pair stores nothing)
-                            tma_store_4d(&tmY, sY, f, tc.x0, tc.img, tc.y0 + m * a.Yb);
+                            tma_store_4d(&tmY, sY, tc.f0 + c0, tc.x0, tc.img, tc.y0 + m * a.Yb);
                             bulk_commit();
                         }
                     }

@@ -684,6 +684,17 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                    d.tmem_cols == c.second.tmem_cols && d.pair == c.second.pair && d.ksplit == c.second.ksplit;
         if (!dup && c.first < 4.0 * best) g_last_cands.push_back(finalize(c.second));
     }
+    // the staged TMA-store epilogue is not always the faster one (very large HBM-bound outputs can
+    // prefer thread stores that overlap the next item's MMAs): measure both for the leading plans
+    {
+        const size_t n0 = g_last_cands.size();
+        for (size_t i = 0; i < n0 && i < 8; ++i)
+            if (g_last_cands[i].tma_y) {
+                FusedArgs c = g_last_cands[i];
+                c.tma_y = 0;
+                g_last_cands.push_back(c);
+            }
+    }
     // the cost of the same layer unfused (GEMM writes T, OffsetAdd reads it back): AUTO only fuses
     // when the fused estimate is lower
     const double tbytes_unf = (double)(s->n * s->h * s->w) * (double)(s->r * s->s * s->f) * 4.0;
