@@ -709,7 +709,8 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                         fence_proxy_async_smem();
                         named_bar_sync(1, 128);
                         if (threadIdx.x == 128 && tc.valid) {   // (the odd CTA of a last pair stores nothing)
-                            tma_store_4d(&tmY, sY, tc.f0 + c0, tc.x0, tc.img, tc.y0 + m * a.Yb);
+                            tma_store_4d(&tmY, sY, tc.f0 + c0, tc.x0 * a.ost + cl.ox0, tc.img,
+                                         (tc.y0 + m * a.Yb) * a.ost + cl.oy0);
                             bulk_commit();
                         }
                     }

@@ -531,8 +531,10 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                     // occ = 2: two CTAs per SM, each with half the smem and 256 TMEM columns
                     // Y through a smem stage + TMA stores: Conv2d (one output class), no split-K, whole
                     // 128-byte channel chunks per slice, 16-byte output rows
-                    const int tma_y = (!transposed && ksp == 1 && FS % (128 / es) == 0 && (s->f * es) % 16 == 0 &&
-                                       !g_no_tma_y) ? 1 : 0;
+                    // (ConvTranspose classes store their interleaved outputs with TMA element strides)
+                    const int ostr = transposed ? (int)s->stride : 1;
+                    const int tma_y = (ksp == 1 && FS % (128 / es) == 0 && (s->f * es) % 16 == 0 &&
+                                       XB * ostr <= 256 && Yb * ostr <= 256 && !g_no_tma_y) ? 1 : 0;
                     const int bud = (occ == 1 ? budget : (113 * 1024 - 2048)) - fc_red_bytes(ksp, FS) -
                                     (tma_y ? FC_YSTAGE_BYTES : 0);
                     const int nbuf_o = occ == 1 ? nbuf : (2 * MT * acc_cols <= 256 ? 2 : 1);
@@ -925,8 +927,9 @@ static ollie_status run_fused(const ollie_conv_shape *s, bool tf32, int transpos
             cuuint64_t dims[4] = {(cuuint64_t)s->f, (cuuint64_t)OW, (cuuint64_t)s->n, (cuuint64_t)OH};
             cuuint64_t strides[3] = {(cuuint64_t)(s->f * es), (cuuint64_t)(OH * OW * s->f * es),
                                      (cuuint64_t)(OW * s->f * es)};
-            cuuint32_t box[4] = {(cuuint32_t)(128 / es), (cuuint32_t)a.XB, (cuuint32_t)a.ipt, (cuuint32_t)a.Yb};
-            cuuint32_t estr[4] = {1, 1, 1, 1};
+            const cuuint32_t o = (cuuint32_t)a.ost;   // ConvT class: every ost-th output pixel
+            cuuint32_t box[4] = {(cuuint32_t)(128 / es), (cuuint32_t)a.XB * o, (cuuint32_t)a.ipt, (cuuint32_t)a.Yb * o};
+            cuuint32_t estr[4] = {1, o, 1, o};
             CUresult r = enc(&ty, dt, 4, y, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (Y store) failed (%d)", (int)r);
