@@ -169,34 +169,57 @@ merged_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         uint32_t acc_phase = 0;
         const bool vec = kOutBF16 ? (args.ldo % 8 == 0) : (args.ldo % 4 == 0);
         pdl_wait();
-        if (lane == 0 && !kOutBF16 && !kRed && args.tma_out) tma_prefetch_desc(&tmO);
+        if (lane == 0 && !kRed && args.tma_out) tma_prefetch_desc(&tmO);
         uint32_t nst = 0;                        // TMA-store path: staging buffers used (buffer = nst & 1)
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             const int m_blk = tile / num_n, n_blk = tile % num_n;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            if constexpr (!kOutBF16 && !kRed) {
-                if (args.tma_out && !args.epi.on) {
-                    // fp32 tile -> 32 x 32 SWIZZLE_128B smem blocks -> TMA stores: full 128-byte lines
-                    // (thread-per-row 16-byte stores wrote half sectors and throttled the LSU)
+            if constexpr (!kRed) {
+                if (args.tma_out) {
+                    // tile -> 32-row x 128-byte SWIZZLE_128B smem blocks (32 fp32 / 64 bf16 columns, the
+                    // NEXT-3 epilogue applied first) -> TMA stores: full 128-byte lines (thread-per-row
+                    // 16-byte stores wrote half sectors and throttled the LSU)
+                    constexpr int CW = kOutBF16 ? 64 : 32;   // output columns per staged 128-byte row
                     const uint32_t tb0 = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * GEMM_MAX_BN);
                     const int ncols = (int)min((int64_t)BN, N - (int64_t)n_blk * BN);
-                    for (int c0 = 0; c0 < ncols; c0 += 32) {
-                        uint32_t v[32];
-                        tmem_ld_32x32b_x32(tb0 + (uint32_t)c0, v);
-                        tmem_ld_wait();
-                        if (c0 + 32 >= ncols) {          // accumulator drained: the MMA warp may reuse it
-                            tc_fence_before();
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive(&tempty[acc]);
-                        }
+                    const int64_t row = (int64_t)m_blk * GEMM_BM + ew * 32 + lane;
+                    for (int c0 = 0; c0 < ncols; c0 += CW) {
                         uint8_t *buf = stg + ew * GEMM_STG_BYTES + (nst & 1) * (32 * 128);
                         if (lane == 0) bulk_wait_read<1>();      // this buffer's previous store has read it
                         __syncwarp();
 #pragma unroll
-                        for (int c = 0; c < 8; ++c)
-                            *reinterpret_cast<uint4 *>(buf + lane * 128 + ((c ^ (lane & 7)) << 4)) =
-                                make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                        for (int h = 0; h < CW; h += 32) {
+                            uint32_t v[32];
+                            tmem_ld_32x32b_x32(tb0 + (uint32_t)(c0 + h), v);
+                            tmem_ld_wait();
+                            if (c0 + h + 32 >= ncols) {          // accumulator drained: the MMA warp may reuse it
+                                tc_fence_before();
+                                __syncwarp();
+                                if (lane == 0) mbar_arrive(&tempty[acc]);
+                            }
+                            const int64_t col = (int64_t)n_blk * BN + c0 + h;
+                            if (args.epi.on && row < M && col < N)
+                                epi_apply_bits<kOutBF16, 32>(args.epi, v, row * args.ldo + col, (int)col,
+                                                             (int)min((int64_t)32, N - col));
+                            if constexpr (kOutBF16) {
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    uint4 pk;
+                                    pk.x = pack_bf16x2_rn(__uint_as_float(v[8 * j]), __uint_as_float(v[8 * j + 1]));
+                                    pk.y = pack_bf16x2_rn(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+                                    pk.z = pack_bf16x2_rn(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+                                    pk.w = pack_bf16x2_rn(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+                                    const int jj = (h >> 3) + j;
+                                    *reinterpret_cast<uint4 *>(buf + lane * 128 + ((jj ^ (lane & 7)) << 4)) = pk;
+                                }
+                            } else {
+#pragma unroll
+                                for (int c = 0; c < 8; ++c)
+                                    *reinterpret_cast<uint4 *>(buf + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                                        make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                            }
+                        }
                         fence_proxy_async_smem();
                         __syncwarp();
                         if (lane == 0) {

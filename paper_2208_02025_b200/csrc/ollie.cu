@@ -258,11 +258,14 @@ static ollie_status run_gemm(int64_t M, int64_t N, int64_t K, bool tf32, const v
     st = make_tmap_2d(&tb, B, tf32, (uint64_t)K, (uint64_t)N, (uint64_t)(K * es), BK, (uint32_t)BN);
     if (st != OLLIE_OK) return st;
     GemmArgs ga{M, N, K, BN, out, ldo, 0, epi ? *epi : EpiArgs{}, red ? *red : RedArgs{}};
-    // fp32 output without an element-wise epilogue (the unfused plan's T): staged TMA stores
+    // staged TMA stores of the output tile (the unfused plan's fp32 T, the identity plan's bf16 / fp32 Y
+    // with its NEXT-3 epilogue): 128-byte boxes of 32 fp32 / 64 bf16 columns x 32 rows
     CUtensorMap to = tb;   // placeholder when unused
-    if (!red && !out_bf16 && !(epi && epi->on) && BN % 32 == 0 && aligned16(out) && (ldo * 4) % 16 == 0 &&
-        !g_gemm_no_tma_out) {   // (32-column store boxes must not cross into the next tile)
-        st = make_tmap_2d(&to, out, true, (uint64_t)N, (uint64_t)M, (uint64_t)(ldo * 4), 32, 32);
+    const int cw = out_bf16 ? 64 : 32;
+    const int oes = out_bf16 ? 2 : 4;
+    if (!red && BN % cw == 0 && aligned16(out) && (ldo * oes) % 16 == 0 &&
+        !g_gemm_no_tma_out) {   // (store boxes must not cross into the next tile)
+        st = make_tmap_2d(&to, out, !out_bf16, (uint64_t)N, (uint64_t)M, (uint64_t)(ldo * oes), (uint32_t)cw, 32);
         if (st != OLLIE_OK) return st;
         ga.tma_out = 1;
     }
