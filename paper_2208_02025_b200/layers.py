@@ -28,12 +28,13 @@ class DerivedConv:
         nbytes = _o.workspace_bytes(self.shape, self.code, plan, self.transposed)
         self.autotune = autotune and plan == _o.PLAN_AUTO
         if self.autotune:
-            # the unfused and GEMM_RED plans are autotune candidates when their workspaces are modest
+            # the unfused and GEMM_RED plans are autotune candidates when their workspaces fit a few
+            # GB (B200: 180 GB HBM; FSRCNN's 9x9 ConvT needs a 1.4 GB T)
             unf = _o.workspace_bytes(self.shape, self.code, _o.PLAN_UNFUSED, self.transposed)
-            if unf <= (1 << 30):
+            if unf <= (4 << 30):
                 nbytes = max(nbytes, unf)
             red = _o.workspace_bytes(self.shape, self.code, _o.PLAN_GEMM_RED, self.transposed)
-            if red <= (1 << 30):
+            if red <= (4 << 30):
                 nbytes = max(nbytes, red)
         self.ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device) if nbytes else None
         self.ws_bytes = nbytes
