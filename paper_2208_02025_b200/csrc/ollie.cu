@@ -1035,14 +1035,18 @@ static ollie_status run_offset_add(const ollie_conv_shape *s, int transposed, co
     const bool vec4 = (s->f % 4 == 0) && (ldT % 4 == 0) && aligned16(T) && (out_bf16 ? (reinterpret_cast<uintptr_t>(y) & 7) == 0 : aligned16(y));
     const int VEC = vec4 ? 4 : 1;
     a.items = s->n * OH * OW * (s->f / VEC);
-    const int64_t blocks = std::min<int64_t>(ceil_div(a.items, 256), (int64_t)num_sms() * 16);
+    // small outputs (ResNet b1 layers: a few thousand items) use 64-thread blocks so the loads spread
+    // over more SMs; large ones 256-thread blocks, grid capped at 16 per SM (grid-stride loop)
+    static const int tpb_env = [] { const char *e = getenv("OLLIE_OA_TPB"); return e ? atoi(e) : 0; }();
+    const int tpb = tpb_env > 0 ? tpb_env : (a.items < (int64_t)num_sms() * 512 ? 64 : 256);
+    const int64_t blocks = std::min<int64_t>(ceil_div(a.items, tpb), (int64_t)num_sms() * 16);
     const unsigned g = (unsigned)std::max<int64_t>(blocks, 1);
     // 32-bit index decoding when the item count and the grid stride fit comfortably
-    const bool i32 = a.items + (int64_t)g * 256 < (1ll << 31);
+    const bool i32 = a.items + (int64_t)g * tpb < (1ll << 31);
 #define OA_LAUNCH(K, V, B)                                                                 \
     do {                                                                                   \
-        if (i32) CUDA_TRY(launch(K<V, B, int32_t>, dim3(g), dim3(256), 0, stream, a));        \
-        else CUDA_TRY(launch(K<V, B, int64_t>, dim3(g), dim3(256), 0, stream, a));            \
+        if (i32) CUDA_TRY(launch(K<V, B, int32_t>, dim3(g), dim3(tpb), 0, stream, a));        \
+        else CUDA_TRY(launch(K<V, B, int64_t>, dim3(g), dim3(tpb), 0, stream, a));            \
     } while (0)
     if (!transposed) {
         if (vec4) { if (out_bf16) OA_LAUNCH(offset_add_kernel, 4, true); else OA_LAUNCH(offset_add_kernel, 4, false); }
