@@ -80,7 +80,9 @@ typedef struct {
 } ollie_conv_shape;
 
 /* Plans of the derived layer:
- *   AUTO     -- measured choice (first call per shape: ollie_autotune_derived) or the cost model
+ *   AUTO     -- measured choice (first call per shape: ollie_autotune_derived) or the cost model;
+ *               the choice is process-wide, so re-query ollie_workspace_bytes(AUTO) after tuning --
+ *               a call whose ws cannot hold the tuned plan's T / accumulator runs FUSED instead
  *   FUSED    -- a8: OffsetAdd / selective add fused into the GEMM, T only in TMEM / smem
  *   UNFUSED  -- the literal two-kernel program: merged GEMM writes T (workspace), then a3 / a4
  *   GEMM_RED -- merged GEMM over full n*h*w rows whose epilogue adds every T element into its
@@ -189,8 +191,8 @@ ollie_status ollie_autotune_derived(const ollie_conv_shape *shape, ollie_dtype d
 
 /* a2 standalone (the merged Matmul of P:1342-1352 on tcgen05 tensor cores):
  *   T[m][n] = sum_k A[m][k] * B[n][k]      A [M][K], B [N][K] in `dtype` (BF16 / TF32),
- *   T fp32 with row stride ldT elements (ldT >= N, ldT % 4 == 0).  K % 8 (bf16) or
- *   K % 4 (tf32) must be 0 (16-byte rows). */
+ *   T fp32 with row stride ldT elements (ldT >= N, ldT % 4 == 0), 16-byte aligned, else
+ *   OLLIE_E_ALIGN.  K % 8 (bf16) or K % 4 (tf32) must be 0 (16-byte rows). */
 ollie_status ollie_merged_gemm(int64_t M, int64_t N, int64_t K, ollie_dtype dtype,
                                const void *A, const void *B, float *T, int64_t ldT,
                                ollie_stream_t stream);
@@ -273,7 +275,8 @@ ollie_status ollie_eop_eval(const ollie_eop *eop, const void *const *inputs, voi
  * and 0 where the B row m + d*(w - W) lies outside [0, L).
  *   A, B : [batch][L][K] dtype elements, 16-byte aligned (device); K*sizeof(elem) == 128
  *          (K = 64 bf16 / 32 tf32), else E_UNSUPPORTED
- *   out  : [batch][L][ldo], ldo >= 2W+1; bf16 (BF16) or fp32 (TF32); columns >= 2W+1 untouched
+ *   out  : [batch][L][ldo], ldo >= 2W+1, 16-byte aligned (else E_ALIGN); bf16 (BF16) or fp32
+ *          (TF32); columns >= 2W+1 untouched.  batch, L, 2W+1 and the work items must fit int32.
  *   form : OLLIE_G2BMM_DERIVED -- the paper's dilated -> non-dilated rewrite: tiles of one
  *          residue class m = r + d*u, a dense band product per class (TMA element stride d);
  *          OLLIE_G2BMM_DIRECT -- dilated tiles over contiguous rows (band columns d apart), d <= 4.

@@ -88,6 +88,9 @@ CONFIGS = {
     "csrnet": [Layer("csrnet_d2_512x64_b16", 16, 512, 64, 64, 512, 3, 3, pad=2, dilation=2)],
     # configs[3]: InfoGAN ConvT (paper Table shape; f=448 reading Q18) and DCGAN generator
     "infogan": [Layer("infogan_t256to448_b16", 16, 256, 2, 2, 448, 4, 4, pad=1, stride=2, transposed=True)],
+    # the same layer with fp32 storage / TF32 MMA: the paper's Table row is fp32 (reading Q1)
+    "infogan_tf32": [Layer("infogan_t256to448_b16_tf32", 16, 256, 2, 2, 448, 4, 4, pad=1, stride=2,
+                           transposed=True, dtype="tf32")],
     "dcgan": [Layer(f"dcgan_t{c}to{f}_b16", 16, c, hw, hw, f, 4, 4, pad=1, stride=2, transposed=True)
               for c, f, hw in ((512, 256, 4), (256, 128, 8), (128, 64, 16), (64, 3, 32))],
     # configs[4]: FSRCNN(56,12,4) x2, batch 64, LR 256x256 (reading Q17).  c=1 and c=12

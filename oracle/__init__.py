@@ -68,6 +68,7 @@ def _load():
             lib.oracle_g2bmm.argtypes = [I] * 5 + [_dp] * 3
             lib.oracle_selective_add.argtypes = [I] * 10 + [_dp] * 2
             lib.oracle_num_threads.restype = ctypes.c_int
+            lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
             _lib = lib
     return _lib
 
@@ -85,6 +86,11 @@ def _p(a: np.ndarray):
 
 def num_threads() -> int:
     return int(_load().oracle_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP thread count for later oracle calls (no effect on the arithmetic)."""
+    _load().oracle_set_num_threads(int(n))
 
 
 def conv_out_size(n, k, pad, stride, dil) -> int:

@@ -219,6 +219,9 @@ void oracle_g2bmm(i64 batch, i64 L, i64 K, i64 W, i64 d, const double *A, const 
 #ifdef _OPENMP
 #include <omp.h>
 int oracle_num_threads(void) { return omp_get_max_threads(); }
+/* Thread count for later calls (bench.py's single-thread cpu_baseline figure); arithmetic unchanged. */
+void oracle_set_num_threads(int n) { omp_set_num_threads(n > 0 ? n : 1); }
 #else
 int oracle_num_threads(void) { return 1; }
+void oracle_set_num_threads(int n) { (void)n; }
 #endif

@@ -324,6 +324,19 @@ g2bmm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
                     if (lane == 0) mbar_arrive(&tempty[(cg0 + (uint32_t)c_freed) % G2_NBUF]);
                 }
             }
+            // warps whose first band block is past nwb (small W: nwb < PERQ) read no window, but the
+            // tempty barriers count every epilogue warp: release each remaining chunk once it exists
+            while (c_freed + 1 < a.nchunks) {
+                ++c_freed;
+                while (c_ready < c_freed) {
+                    ++c_ready;
+                    const uint32_t cgc = cg0 + (uint32_t)c_ready;
+                    mbar_wait(&tfull[cgc % G2_NBUF], (cgc / G2_NBUF) & 1);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[(cg0 + (uint32_t)c_freed) % G2_NBUF]);
+            }
             cg0 += (uint32_t)a.nchunks;
         }
     }

@@ -280,6 +280,8 @@ extern "C" ollie_status ollie_merged_gemm(int64_t M, int64_t N, int64_t K, ollie
     if (dtype != OLLIE_BF16 && dtype != OLLIE_TF32) return fail(OLLIE_E_UNSUPPORTED, "GEMM dtype must be BF16 or TF32");
     if (!A || !B || !T) return fail(OLLIE_E_INVALID, "null pointer");
     if (ldT < N) return fail(OLLIE_E_INVALID, "ldT < N");
+    // the epilogue's vector / TMA stores assume a 16-byte aligned T and 16-byte row pitch (header)
+    if (!aligned16(T) || ldT % 4 != 0) return fail(OLLIE_E_ALIGN, "T must be 16-byte aligned with ldT %% 4 == 0");
     ollie_status st = run_gemm(M, N, K, dtype == OLLIE_TF32, A, B, T, ldT, false, (cudaStream_t)stream);
     return st == OLLIE_OK ? ok() : st;
 }
@@ -1156,8 +1158,17 @@ static ollie_status derived_layer(const ollie_conv_shape *s, ollie_dtype dtype, 
     if ((s->c * elem_size(dtype)) % 16 != 0)
         return fail(OLLIE_E_ALIGN, "c*sizeof(elem) = %lld not a multiple of 16: channel-pad x with an eOperator",
                     (long long)(s->c * elem_size(dtype)));
-    const int rp = resolve_plan(s, dtype, plan, transposed);
+    int rp = resolve_plan(s, dtype, plan, transposed);
     const int64_t M = s->n * s->h * s->w, N = s->r * s->s * s->f, K = s->c;
+    if (plan == OLLIE_PLAN_AUTO && !is_identity_offset_add(s, transposed) &&
+        (rp == OLLIE_PLAN_UNFUSED || rp == OLLIE_PLAN_GEMM_RED)) {
+        // AUTO follows the (process-wide) autotuned choice; a caller that sized its workspace
+        // before another instance tuned this shape may not hold that plan's T / accumulator:
+        // then AUTO runs the fused plan instead of failing (ollie.h, OLLIE_PLAN_AUTO)
+        const size_t need = rp == OLLIE_PLAN_GEMM_RED ? red_acc_bytes(s, OH, OW)
+                                                      : (size_t)M * (size_t)ldT_of(s) * sizeof(float);
+        if ((!ws || ws_bytes < need) && fused_supported(s, tf32, transposed)) rp = OLLIE_PLAN_FUSED;
+    }
     if (rp == OLLIE_PLAN_FUSED) {
         if (!fused_supported(s, tf32, transposed))
             return fail(OLLIE_E_UNSUPPORTED, "fused plan not available for this shape/dtype");
@@ -1879,14 +1890,19 @@ extern "C" ollie_status ollie_autotune_derived(const ollie_conv_shape *s, ollie_
         t_red = time_it([&] { return run_gemm_red(s, transposed, tf32, x, wp, (float *)ws, y, OH, OW, stream, nullptr); });
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    const bool any_timed = best < 1e29f || t_unf < 1e29f || t_red < 1e29f;
     {
         std::lock_guard<std::mutex> g(g_plan_mu);
-        if (best_k >= 0) e->args = cands[best_k];
-        if (t_red < best && t_red <= t_unf) e->tuned = 3;
-        else e->tuned = (t_unf < best || best_k < 0) ? 2 : 1;
+        if (!cands.empty()) e->args = cands[best_k >= 0 ? best_k : 0];
+        // record a decision only when some plan actually ran and was timed: a failed tuning leaves
+        // AUTO to the cost model instead of pinning it to an unmeasured plan
+        if (any_timed) {
+            if (t_red < best && t_red <= t_unf) e->tuned = 3;
+            else e->tuned = (t_unf < best || best_k < 0) ? 2 : 1;
+        }
     }
     if (best_us) *best_us = 1e3f * std::min(std::min(best, t_unf), t_red);
-    if (best_k < 0 && !unfused_ok && !red_ok) return fail(OLLIE_E_UNSUPPORTED, "no runnable plan to tune");
+    if (!any_timed) return fail(OLLIE_E_UNSUPPORTED, "no runnable plan to tune");
     if (tune_file) {
         if (FILE *fp = fopen(tune_file, "a")) {
             const int t = e->tuned;
@@ -1927,10 +1943,14 @@ extern "C" ollie_status ollie_g2bmm(int64_t batch, int64_t L, int64_t K, int64_t
     if (form != OLLIE_G2BMM_DERIVED && form != OLLIE_G2BMM_DIRECT) return fail(OLLIE_E_INVALID, "unknown G2BMM form %d", form);
     if (!A || !B || !out) return fail(OLLIE_E_INVALID, "null pointer");
     if (ldo < 2 * W + 1) return fail(OLLIE_E_INVALID, "ldo < 2W + 1");
+    if (batch > INT32_MAX || L > INT32_MAX || W > (INT32_MAX - 1) / 2)
+        return fail(OLLIE_E_UNSUPPORTED, "G2BMM extents exceed int32");
     const bool tf32 = dtype == OLLIE_TF32;
     const int es = tf32 ? 4 : 2;
     if (K * es != 128) return fail(OLLIE_E_UNSUPPORTED, "G2BMM implemented for K*sizeof(elem) == 128 (K = 64 bf16 / 32 tf32)");
     if (!aligned16(A) || !aligned16(B)) return fail(OLLIE_E_ALIGN, "A / B must be 16-byte aligned");
+    // the epilogue picks 16-byte (ldo % 8 == 0) or 4-byte stores from the pitch: the base must match
+    if (!aligned16(out)) return fail(OLLIE_E_ALIGN, "out must be 16-byte aligned");
     if (batch * L * (2 * W + 1) >= (1ll << 40) || L >= (1ll << 30)) return fail(OLLIE_E_UNSUPPORTED, "G2BMM extents too large");
     // derived: tiles over one residue class (rows r + d*u, stride d), band columns dense (cs = 1);
     // direct: contiguous rows, band columns d apart (cs = d)
@@ -1951,6 +1971,7 @@ extern "C" ollie_status ollie_g2bmm(int64_t batch, int64_t L, int64_t K, int64_t
     g.nres = derived ? (int)d : 1;
     const int64_t rows_per_res = derived ? ceil_div(L, d) : L;
     g.tiles_r = (int)ceil_div(rows_per_res, 128);
+    if (batch * g.nres * (int64_t)g.tiles_r > INT32_MAX) return fail(OLLIE_E_UNSUPPORTED, "G2BMM work items exceed int32");
     g.num_items = (int)(batch * g.nres * g.tiles_r);
     g.ldo = ldo;
     g.out = out;

@@ -78,8 +78,13 @@ class DerivedConv:
             # first call: pick the plan by measurement; not during graph capture
             if not torch.cuda.is_current_stream_capturing():
                 # candidates write a scratch output: y may alias the residual (in-place epilogue)
-                _o.autotune_derived(self.shape, self.code, self.transposed, x, self.w_prep, self.new_output(),
+                scratch = self.new_output()
+                _o.autotune_derived(self.shape, self.code, self.transposed, x, self.w_prep, scratch,
                                     self.ws, self.ws_bytes, stream)
+                # the last candidate launch still writes `scratch` on `stream`: finish it before the
+                # caching allocator may hand the block to other work (one-time cost per layer)
+                torch.cuda.synchronize(self.device)
+                del scratch
                 self._tuned = True
         if epi is None:
             fn = _o.convtranspose2d_derived if self.transposed else _o.conv2d_derived

@@ -79,11 +79,12 @@ class StackLayer:
         self.conv.prepare(w)
         return self
 
-    def __call__(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+    def __call__(self, x: torch.Tensor, stream=None, y: torch.Tensor | None = None) -> torch.Tensor:
+        """y: optional caller-owned output (same shape as self.y) instead of the layer's own buffer."""
         if self.pad_eop is not None:
             _o.eop_eval(self.pad_eop, [x], self.x_pad, stream)
             x = self.x_pad
-        return self.conv(x, self.y, stream)
+        return self.conv(x, self.y if y is None else y, stream)
 
     def launches(self) -> int:
         """Kernels one call launches (pad eOp + 1 fused / identity-eliminated, 2 unfused, or 3 for
@@ -116,16 +117,22 @@ class DerivedStack:
             sl.prepare(w)
         return self
 
-    def __call__(self, inputs, stream=None):
+    def __call__(self, inputs, stream=None, out=None):
         """inputs: one tensor (chained) or one per layer (independent).  Returns the layers'
-        logical outputs (views without padding channels)."""
+        logical outputs (views without padding channels).  out (optional): caller-owned output of
+        the last layer (chained) or one per layer (independent), written instead of the layers'
+        own buffers -- e.g. a micro-batch's slice of a rank's output shard (parallel.BlockCyclic)."""
         outs = []
         x = inputs if self.chained else None
+        last = len(self.layers) - 1
         for k, sl in enumerate(self.layers):
             src = x if self.chained else inputs[k]
-            sl(src, stream)
-            outs.append(sl.y_logical)
-            x = sl.y
+            dst = None
+            if out is not None and (not self.chained or k == last):
+                dst = out if self.chained else out[k]
+            y = sl(src, stream, dst)
+            outs.append(y[..., : sl.layer.f] if dst is None else y)
+            x = y
         return outs
 
     def launches(self) -> int:

@@ -87,3 +87,34 @@ def test_g2bmm_errors(O):
     with pytest.raises(O.OllieError) as e:
         O.g2bmm(1, 10, 48, 1, 0, O.BF16, x, x, y)
     assert e.value.status == O.E_INVALID
+
+
+# with a narrow band (nwb < epilogue warps per TMEM quadrant) some epilogue warps
+# read no window; they must still release every TMEM chunk, or a CTA that wraps the 4-buffer ring
+# (more than ~2 items per CTA) waits forever.  Many items per CTA, small W, both forms.
+@pytest.mark.parametrize("form,W,d", [(0, 8, 4), (0, 15, 2), (1, 7, 2), (1, 3, 4)])
+def test_g2bmm_small_band_many_items_per_cta(O, form, W, d):
+    g = syn.G2("many_items", 8, 10000, 64, W, d)
+    a, b = syn.g2bmm_inputs(g, 703, exact_int=True)
+    got, nw = _run(O, g, a, b, form)
+    rows = np.r_[0:300, 4900:5300, 9700:10000]                 # sampled rows, every tile position kind
+    full = oracle.g2bmm(a, b, g.W, g.d)
+    assert np.array_equal(got[:, rows, :nw], _round_like(full[:, rows], g.dtype))
+
+
+def test_g2bmm_misaligned_out_is_status(O):
+    g = CASES[0]
+    a, b = syn.g2bmm_inputs(g, 704, exact_int=True)
+    buf = torch.zeros(g.batch * g.L * 7 + 1, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(O.OllieError) as ei:
+        O.g2bmm(g.batch, g.L, g.K, g.W, g.d, O.BF16, a.cuda(), b.cuda(), buf[1:], 7)
+    assert ei.value.status == O.E_ALIGN
+
+
+def test_merged_gemm_misaligned_T_is_status(O):
+    a = torch.zeros(64, 64, dtype=torch.bfloat16, device="cuda")
+    b = torch.zeros(32, 64, dtype=torch.bfloat16, device="cuda")
+    T = torch.zeros(64 * 32 + 1, dtype=torch.float32, device="cuda")
+    with pytest.raises(O.OllieError) as ei:
+        O.merged_gemm(64, 32, 64, O.BF16, a, b, T[1:], 32)
+    assert ei.value.status == O.E_ALIGN

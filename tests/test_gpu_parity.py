@@ -194,7 +194,8 @@ def test_strided_fused_random_tolerance(O, lay):
 
 def _configured():
     out = []
-    for name in ("motivating", "resnet18", "resnet18_s2", "csrnet", "infogan", "dcgan", "paper_conv3x3"):
+    for name in ("motivating", "resnet18", "resnet18_s2", "csrnet", "infogan", "infogan_tf32", "dcgan",
+                 "paper_conv3x3"):
         for i, lay in enumerate(syn.CONFIGS[name]):
             out.append((name, i, lay))
     return out
