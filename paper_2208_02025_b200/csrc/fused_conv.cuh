@@ -76,6 +76,12 @@ struct FusedArgs {
     int32_t tma_y;                    // 1: Y tiles leave through a SWIZZLE_128B smem stage + TMA stores
     int32_t ipt, Xr, ngrp;            // images per tile (interleaved patch rows [y][image][x]),
                                       // patch row pitch Xr = ipt * Xb, image groups ceil(n / ipt)
+    int32_t grp8;                     // lane layout: 0 = 128 consecutive patch rows (lane = y*Xr + k*Xb + x);
+                                      // 1 = 16 groups of 8 lanes, group g = y*ipt + k starting at patch row
+                                      // g*Xb (XB <= 8): the A descriptor's 8-row stride SBO = Xb rows, so
+                                      // no lane maps to a halo column
+    int32_t lane_lp, lane_ip;         // lane decode: ly = L / lane_lp, image (L % lane_lp) / lane_ip, lx = L % lane_ip
+    int32_t a_sbo;                    // A descriptor stride between 8-row groups, bytes
     int32_t tiles_x, tiles_y, f_slices, FS, num_tiles;
     int32_t kchunks, BK;              // channel chunks of BK elements
     int32_t a_box_bytes;              // bytes TMA writes per patch load
@@ -366,10 +372,11 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         const uint32_t idesc = make_idesc(kTF32, kPair ? 256 : 128, (uint32_t)a.FS);
         const bool sw = a.sw128 != 0;
         // A: interleaved (LBO = planar chunk stride, SBO = 128 B) or SWIZZLE_128B (SBO = 1024 B)
-        const uint64_t adesc_t = sw ? (((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
-                                       ((uint64_t)2 << 61))
-                                    : (((uint64_t)((a.lbo >> 4) & 0x3FFF) << 16) | ((uint64_t)(128 >> 4) << 32) |
-                                       ((uint64_t)1 << 46));
+        // (grp8 lanes: SBO = Xb patch rows, so group g starts at patch row g*Xb; SWIZZLE_128B still
+        // works since the tensor core swizzles absolute smem address bits, as TMA wrote them)
+        const uint64_t sbo_f = (uint64_t)(((uint32_t)a.a_sbo >> 4) & 0x3FFF) << 32;
+        const uint64_t adesc_t = sw ? (((uint64_t)1 << 16) | sbo_f | ((uint64_t)1 << 46) | ((uint64_t)2 << 61))
+                                    : (((uint64_t)((a.lbo >> 4) & 0x3FFF) << 16) | sbo_f | ((uint64_t)1 << 46));
         const uint32_t rowb16 = sw ? 8u : 1u;                           // one patch row, 16-byte units
         const uint64_t bdesc_t = ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
                                  ((uint64_t)2 << 61);
@@ -534,8 +541,9 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
         // ===== epilogue: TMEM -> registers -> Y (bf16 RNE or fp32), one output pixel per thread =====
         const int q = warp - 4;
         const int L = q * 32 + lane;
-        // lane L = ly * Xr + k * Xb + lx: output row ly, image k of the tile's group, column lx
-        const int ly = L / a.Xr, lrem = L - ly * a.Xr, limg = lrem / a.Xb, lx = lrem - limg * a.Xb;
+        // lane L = ly * Xr + k * Xb + lx (grp8: ly * 8 * ipt + k * 8 + lx): output row ly, image k of the
+        // tile's group, column lx
+        const int ly = L / a.lane_lp, lrem = L - ly * a.lane_lp, limg = lrem / a.lane_ip, lx = lrem - limg * a.lane_ip;
         int acc = 0;
         uint32_t accp = 0;
         const bool vec = (a.F % (kTF32 ? 4 : 8)) == 0;

@@ -292,6 +292,7 @@ static int g_force_mt = 0, g_force_fs = 0, g_force_res = -1;   // debug plan ove
 static int g_force_pair = -1;                                   // debug: -1 auto, 0 single CTAs, 1 CTA pairs
 static int g_force_ks = -1;                                     // debug: -1 auto, else the split-K factor
 static int g_force_ipt = 0;                                     // debug: 0 auto, else images per tile
+static int g_force_g8 = -1;                                     // debug: -1 auto, else the lane layout (grp8)
 static const bool g_no_tma_y = [] {   // OLLIE_NO_TMA_Y=1: fused-kernel Y by thread stores (A/B switch)
     const char *e = getenv("OLLIE_NO_TMA_Y");
     return e && e[0] == '1';
@@ -479,7 +480,16 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
     FusedArgs a_best{};
     bool found = false;
     std::vector<std::pair<double, FusedArgs>> all;   // every evaluated plan (autotune candidates)
-    for (int XB = (int)std::min<int64_t>(GW, 128); XB >= 1; --XB) {
+    // Two lane layouts of the 128-row A operand (fused_conv.cuh, FusedArgs::grp8):
+    //  g8 = 0: 128 consecutive patch rows, lane = y*Xr + image*Xb + x -- the lanes of the Xb - XB halo
+    //          columns of each row compute nothing;
+    //  g8 = 1: 16 groups of 8 consecutive rows, group g = y*ipt + image at patch row g*Xb (the
+    //          descriptor's 8-row stride SBO = Xb rows): XB <= 8 output columns per tile, every lane an
+    //          output pixel (CSRNet 64x64: 128 of 128 lanes instead of 110, 64 of 64 columns instead of 66)
+    for (int g8 = 0; g8 <= 1; ++g8) {
+    if (g_force_g8 >= 0 && g8 != g_force_g8) continue;
+    const int xb_hi = (int)std::min<int64_t>(GW, g8 ? 8 : 128);
+    for (int XB = xb_hi; XB >= (g8 ? xb_hi : 1); --XB) {
       const int Xb = XB + span_x;
       if (Xb * ist > 256) continue;                // TMA box: <= 256 traversed elements
       // ipt > 1: several images share a tile, patch rows interleaved [y][image][x] (row pitch
@@ -487,14 +497,16 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
       for (int ipt = 1; ipt <= 4; ++ipt) {
         if (ipt > 1 && (GW > XB || base.n < ipt)) break;
         if (g_force_ipt > 0 && ipt != g_force_ipt) continue;
+        if (g8 && 16 % ipt) continue;
         const int Xr = ipt * Xb;
         const int lanes_fixed = (ipt - 1) * Xb + XB;     // lanes of the last output row
-        if (lanes_fixed > 128) break;
-        const int Yb = (int)std::min<int64_t>(GH, (128 - lanes_fixed) / Xr + 1);
+        if (!g8 && lanes_fixed > 128) break;
+        const int Yb = g8 ? (int)std::min<int64_t>(GH, 16 / ipt) : (int)std::min<int64_t>(GH, (128 - lanes_fixed) / Xr + 1);
         if (Yb < 1) continue;
-        if (ipt == 1 && XB < std::min<int64_t>(GW, 128) && ceil_div(GW, XB) == ceil_div(GW, XB + 1) &&
+        if (!g8 && ipt == 1 && XB < std::min<int64_t>(GW, 128) && ceil_div(GW, XB) == ceil_div(GW, XB + 1) &&
             (128 - (XB + 1)) / (Xb + 1) + 1 >= Yb)
             continue;
+        const int lane_span = g8 ? 15 * Xb + 8 : 128;   // patch rows the 128 lanes of one tap read
         for (int MT = 1; MT <= 4; ++MT) {
             if (g_force_mt > 0 && MT != g_force_mt) continue;
             if (MT > 1 && (int64_t)(MT - 1) * Yb >= GH) break;
@@ -503,7 +515,8 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
             const int max_off = span_y * Xr + span_x + (MT - 1) * Yb * Xr;
             if (max_off >= 65536) break;
             const int box = 16 * Xb * Yp * ipt * nchunk;   // same bytes in both layouts
-            const int need = sw128 ? (max_off + 128) * 128 : (nchunk - 1) * 16 * Xb * Yp * ipt + (max_off + 128) * 16;
+            const int need = sw128 ? (max_off + lane_span) * 128
+                                   : (nchunk - 1) * 16 * Xb * Yp * ipt + (max_off + lane_span) * 16;
             const int astage = (int)ceil_div(std::max(box, need), 1024) * 1024;
             if (2 * astage > budget) break;
             const int64_t items_sp = (int64_t)nclass * ceil_div(base.n, ipt) * ceil_div(GW, XB) * ceil_div(GH, (int64_t)Yb * MT);
@@ -589,6 +602,10 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                         FusedArgs a = base;
                         a.XB = XB; a.Xb = Xb; a.Yb = Yb; a.Yp = Yp; a.MT = MT;
                         a.ipt = ipt; a.Xr = Xr; a.ngrp = (int)ceil_div(base.n, ipt);
+                        a.grp8 = g8;
+                        a.lane_lp = g8 ? 8 * ipt : Xr;
+                        a.lane_ip = g8 ? 8 : Xb;
+                        a.a_sbo = g8 ? Xb * rowbytes : 8 * rowbytes;
                         a.tma_y = tma_y;
                         a.a_box_bytes = box; a.a_stage_bytes = astage;
                         a.FS = FS; a.acc_cols = acc_cols; a.nbuf = nbuf_o; a.b_stage_bytes = bstage_c;
@@ -609,6 +626,7 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
             }
         }
       }
+    }
     }
     if (!found) return false;
     auto finalize = [&](FusedArgs a) -> FusedArgs {
@@ -688,7 +706,8 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
         bool dup = false;
         for (auto &d : g_last_cands)
             dup |= d.MT == c.second.MT && d.FS == c.second.FS && d.resident == c.second.resident && d.ipt == c.second.ipt &&
-                   d.tmem_cols == c.second.tmem_cols && d.pair == c.second.pair && d.ksplit == c.second.ksplit;
+                   d.tmem_cols == c.second.tmem_cols && d.pair == c.second.pair && d.ksplit == c.second.ksplit &&
+                   d.grp8 == c.second.grp8;
         if (!dup && c.first < 4.0 * best) g_last_cands.push_back(finalize(c.second));
     }
     // the staged TMA-store epilogue is not always the faster one (very large HBM-bound outputs can
@@ -731,7 +750,8 @@ static std::map<PlanKey, PlanEntry> g_plan_cache;
 static PlanEntry *plan_entry_mut(const ollie_conv_shape *s, bool tf32, int transposed, int64_t OH, int64_t OW) {
     PlanKey k{{s->n, s->c, s->h, s->w, s->f, s->r * 65536 + s->s, s->pad, s->stride * 65536 + s->dilation,
                (int64_t)tf32 * 2 + transposed + 4 * (int64_t)s->output_padding, num_sms(),
-               g_force_mt * 1000 + g_force_fs + 1000000 * g_force_ipt, (g_force_res * 16 + g_force_pair) * 16 + g_force_ks}};
+               g_force_mt * 1000 + g_force_fs + 1000000 * g_force_ipt,
+               ((g_force_res * 16 + g_force_pair) * 16 + g_force_ks) * 16 + g_force_g8}};
     {
         std::lock_guard<std::mutex> g(g_plan_mu);
         auto it = g_plan_cache.find(k);
@@ -1759,10 +1779,10 @@ extern "C" ollie_status ollie_plan_describe(const ollie_conv_shape *s, ollie_dty
         snprintf(buf, len,
                  "fused XB=%d Yb=%d Xb=%d Yp=%d MT=%d FS=%d f_slices=%d resident=%d nbuf=%d na=%d nb=%d BK=%d "
                  "kchunks=%d tiles=%d grid=%d smem=%zu classes=%d phases=%d ist=%d taps=%d sw128=%d ctas_per_sm=%d "
-                 "pair=%d wbox=%dx%d ksplit=%d ipt=%d tma_y=%d",
+                 "pair=%d wbox=%dx%d ksplit=%d ipt=%d tma_y=%d grp8=%d",
                  a.XB, a.Yb, a.Xb, a.Yp, a.MT, a.FS, a.f_slices, a.resident, a.nbuf, a.na, a.nb, a.BK, a.kchunks,
                  a.num_tiles, fused_grid(a), fused_smem_bytes(a), a.nclass, a.nph, a.ist, a.max_taps, a.sw128,
-                 a.tmem_cols == 256 ? 2 : 1, a.pair, a.grb, a.nsb, a.ksplit, a.ipt, a.tma_y);
+                 a.tmem_cols == 256 ? 2 : 1, a.pair, a.grb, a.nsb, a.ksplit, a.ipt, a.tma_y, a.grp8);
     } else if (rp == OLLIE_PLAN_GEMM_RED) {
         snprintf(buf, len, "gemm_red BN=%d (%s as fp32 L2 reductions in the GEMM epilogue) + finish",
                  gemm_bn(s->n * s->h * s->w, s->r * s->s * s->f), transposed ? "selective add" : "OffsetAdd");
@@ -1791,6 +1811,8 @@ extern "C" void ollie_debug_force_pair(int pair) { g_force_pair = pair; }
 extern "C" void ollie_debug_force_ksplit(int ks) { g_force_ks = ks; }
 // Debug hook (not part of include/ollie.h): 0 auto, else only plans with this many images per tile.
 extern "C" void ollie_debug_force_ipt(int ipt) { g_force_ipt = ipt; }
+// Debug hook (not part of include/ollie.h): -1 auto, 0 consecutive-row lanes only, 1 grp8 lanes only.
+extern "C" void ollie_debug_force_grp8(int g8) { g_force_g8 = g8; }
 
 // ------------------------------------------------------------------------ autotune
 extern "C" ollie_status ollie_autotune_derived(const ollie_conv_shape *s, ollie_dtype dtype, int transposed,

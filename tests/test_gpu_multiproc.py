@@ -1,7 +1,9 @@
 """a9 / SURVEY 8(e) with the PRODUCT kernels under a process group: every rank runs the derived
 stack (libollie) on its block-cyclic shard of the batch in micro-batches, each chunk's output is
 all-gathered into its final slice of the full batch, and the result equals the 1-process run of
-the same stack bit for bit (T5).
+the same stack bit for bit (T5).  Integer-mode inputs: the per-rank batch differs from the
+1-process batch, so autotuning may pick another plan (tile shape, split-K) whose fp32 summation
+order differs; with exact integer sums every order gives the same bits.
 
   * NCCL over NVLink with world = min(8, visible GPUs), one GPU per rank (skipped below 2 GPUs);
   * two ranks sharing cuda:0 over gloo (its device collectives go through host staging in
@@ -37,7 +39,7 @@ def _free_port():
 def _single(n):
     from paper_2208_02025_b200.stack import DerivedStack
     lays = _layers(n)
-    x, w = syn.layer_inputs(lays[0], 901)
+    x, w = syn.layer_inputs(lays[0], 901, exact_int=True)
     st = DerivedStack(lays, False)
     st.prepare([w.cuda()])
     y = st([x.cuda()])[0]
@@ -57,7 +59,7 @@ def _worker(rank, world, port, backend, n, chunks, q):
         from paper_2208_02025_b200.stack import DerivedStack
         sh = BlockCyclic(n, world, rank, chunks)
         lays = _layers(n)
-        x, w = syn.layer_inputs(lays[0], 901)                 # the full batch, same seed everywhere
+        x, w = syn.layer_inputs(lays[0], 901, exact_int=True)  # the full batch, same seed everywhere
         xl = sh.local(x).cuda()
         st = DerivedStack([l.with_batch(sh.cb) for l in lays], False)
         st.prepare([w.cuda()])
