@@ -89,8 +89,21 @@ typedef struct {
  *               output pixel as fp32 L2 reductions (red.global.add.v4.f32; "the L2 reduction",
  *               P:1580), then Y = epilogue(acc): the workspace holds the fp32 accumulator
  *               [n][OH][OW][f] (zeroed by the call); f % 4 == 0; summation order is not fixed
- *               (fp32 atomics: results are deterministic only up to rounding, reading Q12). */
-enum { OLLIE_PLAN_AUTO = 0, OLLIE_PLAN_FUSED = 1, OLLIE_PLAN_UNFUSED = 2, OLLIE_PLAN_GEMM_RED = 3 };
+ *               (fp32 atomics: results are deterministic only up to rounding, reading Q12).
+ *   ROWSTREAM -- a8 for narrow outputs: summation splitting of the r*s taps into kernel
+ *               columns (accumulated by the tensor core from column-shifted A operands) and kernel
+ *               rows (on the MMA's N, N = r*f; their OffsetAdd done in the epilogue by adding the
+ *               TMEM accumulators of consecutive input rows); a ConvTranspose2d first becomes the
+ *               stride-1 program over the union of its output residue classes' input offsets,
+ *               classes on N too (expression splitting; the epilogue writes the classes
+ *               interleaved -- the fused pair of P:1437-1438).  Each input row is streamed through
+ *               shared memory once.  Plannable for dilation 1, Conv2d stride 1 or any
+ *               ConvTranspose2d stride, c*sizeof(elem) <= 128, w <= 512, f <= 64 and
+ *               r' * stride^2 * f <= 64 with stride^2 * f in {4, 8, 12, 16} (r', s' <= 16 the
+ *               stride-1 program's kernel, its column padding <= 8); else OLLIE_E_UNSUPPORTED.
+ *               No workspace. */
+enum { OLLIE_PLAN_AUTO = 0, OLLIE_PLAN_FUSED = 1, OLLIE_PLAN_UNFUSED = 2, OLLIE_PLAN_GEMM_RED = 3,
+       OLLIE_PLAN_ROWSTREAM = 4 };
 
 /* ---------------------------------------------------------------------------------
  * Versioning and errors
@@ -131,7 +144,7 @@ size_t ollie_workspace_bytes(const ollie_conv_shape *shape, ollie_dtype dtype, i
  *                                    launch), which the weight DLT allows by never triggering early
  *   y_nhwc : [n][OH][OW][f]          dtype elements, fully overwritten (device)
  *   ws     : ollie_workspace_bytes() bytes (device), may be NULL if that is 0
- *   plan   : OLLIE_PLAN_AUTO / FUSED / UNFUSED
+ *   plan   : OLLIE_PLAN_AUTO / FUSED / UNFUSED / GEMM_RED / ROWSTREAM
  * ConvTranspose2d requires dilation == 1 (the configured workloads); else UNSUPPORTED.
  * --------------------------------------------------------------------------------- */
 ollie_status ollie_conv2d_derived(const ollie_conv_shape *shape, ollie_dtype dtype,
@@ -179,8 +192,8 @@ ollie_status ollie_plan_describe(const ollie_conv_shape *shape, ollie_dtype dtyp
                                  char *buf, size_t len);
 
 /* Plan selection by measurement (the paper keeps the candidate with the best measured
- * performance): times the planner's fused candidates (best few by its cost model) and,
- * when ws can hold T, the unfused plan, on `stream` (synchronizing it), and makes
+ * performance): times the planner's fused candidates (best few by its cost model), the
+ * row-streaming plan when the layer admits it and, when ws can hold T, the unfused plan, on `stream` (synchronizing it), and makes
  * OLLIE_PLAN_AUTO use the fastest for this (shape, dtype, direction) from then on, process-wide.
  * x / w_prep / y / ws as for ollie_conv2d_derived; y ends up holding the layer's result.
  * best_us (may be NULL) receives the winner's time in microseconds.  Not for capture into a

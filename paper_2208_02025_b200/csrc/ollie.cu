@@ -27,6 +27,7 @@
 #include "fused_conv.cuh"
 #include "g2bmm.cuh"
 #include "merged_gemm.cuh"
+#include "rowstream_conv.cuh"
 
 using namespace ollie;
 
@@ -742,7 +743,8 @@ struct PlanEntry {
     FusedArgs args;                 // the plan in use (model's best, or the autotuned winner)
     std::vector<FusedArgs> cands;   // autotune candidates (cands[0] = model's best)
     double fused_cost, unfused_cost;
-    int tuned;                      // 0: model decides; 1: autotuned fused; 2: autotuned unfused; 3: GEMM_RED
+    int tuned;                      // 0: model decides; 1: autotuned fused; 2: autotuned unfused; 3: GEMM_RED;
+                                    // 4: row-streaming
 };
 static std::mutex g_plan_mu;
 static std::map<PlanKey, PlanEntry> g_plan_cache;
@@ -890,6 +892,14 @@ static ollie_status run_fused(const ollie_conv_shape *s, bool tf32, int transpos
     a.y = y;
     a.epi = epi ? *epi : EpiArgs{};
     a.trace = g_fc_trace;
+    {   // debug-only ablations (OLLIE_RS_DBG, see RsArgs::dbg); 0 in production
+        static int dbg = -1;
+        if (dbg < 0) {
+            const char *e = getenv("OLLIE_RS_DBG");
+            dbg = e ? atoi(e) : 0;
+        }
+        a.dbg = dbg;
+    }
     {   // debug-only kernel switches (OLLIE_FC_DBG, see FusedArgs::dbg); 0 in production
         static int dbg = -1;
         if (dbg < 0) {
@@ -971,6 +981,142 @@ static ollie_status run_fused(const ollie_conv_shape *s, bool tf32, int transpos
     }
     if (one) return tf32 ? launch_fused_t<true, false, true, false>(tx, tw, ty, a, stream) : launch_fused_t<false, false, true, false>(tx, tw, ty, a, stream);
     return tf32 ? launch_fused_t<true, false, false, false>(tx, tw, ty, a, stream) : launch_fused_t<false, false, false, false>(tx, tw, ty, a, stream);
+}
+
+// ------------------------------------------------------------------------ row-streaming plan (a8, narrow f)
+// rowstream_conv.cuh: kernel columns (and, for a ConvTranspose2d, the output residue classes) on
+// the MMA's N, kernel rows as A-row shifts, the column OffsetAdd in the epilogue.  Plannable when
+// the layer is (or rewrites to) a stride-1 program with s' * sigma^2 * f <= 64 columns per kernel
+// row, one <= 128-byte channel chunk, and image rows of <= 512 pixels.
+static bool plan_rowstream(const ollie_conv_shape *s, bool tf32, int transposed, int64_t OH, int64_t OW, RsArgs *out) {
+    const int es = tf32 ? 4 : 2;
+    if (s->dilation != 1) return false;
+    if (!transposed && s->stride != 1) return false;
+    if ((s->c * es) % 16 != 0 || s->c * es > 128) return false;
+    if (s->n > INT32_MAX || s->h > 32768 || s->w > 512 || s->f > 64) return false;
+    RsArgs a{};
+    a.n = (int)s->n; a.H = (int)s->h; a.W = (int)s->w; a.C = (int)s->c; a.F = (int)s->f;
+    a.R0 = (int)s->r; a.S0 = (int)s->s; a.pad0 = s->pad;
+    a.OH = (int)OH; a.OW = (int)OW;
+    if (!transposed) {
+        a.sub = 1;
+        a.R = a.R0; a.S = a.S0; a.pad_y = a.pad_x = s->pad;
+        a.OHc = (int)OH; a.OWc = (int)OW;
+    } else {
+        // class cy of output row sigma*q + cy reads input row q + d with kernel row k = cy + p - sigma*d:
+        // the stride-1 program runs over the union of the classes' offsets d
+        const int st = s->stride, p = s->pad;
+        auto span = [&](int K, int *dmin, int *dmax) {
+            *dmin = INT32_MAX; *dmax = INT32_MIN;
+            for (int cy = 0; cy < st; ++cy)
+                for (int k = 0; k < K; ++k)
+                    if ((cy + p - k) % st == 0) {
+                        const int d = (cy + p - k) / st;
+                        *dmin = std::min(*dmin, d); *dmax = std::max(*dmax, d);
+                    }
+        };
+        int dy0, dy1, dx0, dx1;
+        span(a.R0, &dy0, &dy1);
+        span(a.S0, &dx0, &dx1);
+        if (dy0 > dy1 || dx0 > dx1) return false;
+        a.sub = st;
+        a.tr = 1;
+        a.R = dy1 - dy0 + 1; a.S = dx1 - dx0 + 1;
+        a.pad_y = -dy0; a.pad_x = -dx0;
+        a.OHc = (int)ceil_div(OH, st); a.OWc = (int)ceil_div(OW, st);
+    }
+    a.Fp = a.sub * a.sub * a.F;
+    if (a.Fp != 4 && a.Fp != 8 && a.Fp != 12 && a.Fp != 16) return false;   // kernel variants
+    a.N = a.R * a.Fp;                                                         // kernel rows x f' on N
+    if (a.N > RS_MAX_NP || a.S > 16 || a.pad_y < 0) return false;
+    // column shifts read the zero pixel rows kept on both sides of a slot
+    if (a.pad_x < 0 || a.pad_x > RS_ZR || a.S - 1 - a.pad_x > RS_ZR) return false;
+    a.NP = (int)ceil_div(a.N, 16) * 16;
+    a.acc_cols = (int)ceil_div(a.NP, 32) * 32;
+    const int cb = (int)(s->c * es);
+    a.rowbytes = cb <= 32 ? 32 : (cb <= 64 ? 64 : 128);
+    a.swz = a.rowbytes == 32 ? 6 : (a.rowbytes == 64 ? 4 : 2);
+    a.ksteps = (int)ceil_div(cb, 32);
+    a.mtr = (int)ceil_div(std::max<int64_t>(s->w, a.OWc), 128);
+    if (a.mtr > 4) return false;
+    a.slot_bytes = (2 * RS_ZR + a.mtr * 128) * a.rowbytes;
+    // one TMA box per <= 256 pixels; boxes land on whole swizzle atoms (8 rows) and fit the slot
+    a.nbox = (int)ceil_div(s->w, 256);
+    a.wbox = a.nbox == 1 ? (int)s->w : (int)ceil_div(ceil_div(s->w, a.nbox), 8) * 8;
+    if (a.wbox > 256 || a.nbox * a.wbox > a.mtr * 128 + RS_ZR) return false;
+    a.rows_total = s->n * a.OHc;
+    a.tmem_cols = 512;
+    a.row_cols = a.mtr * a.acc_cols;
+    a.nt = std::min(16, 512 / a.row_cols);
+    if (a.nt < a.R + 1) return false;                 // the r-row window plus one row of look-ahead
+    a.ring = 0;
+    const int fixed = (int)rs_smem_bytes(a) + 8 * 2 * 16;
+    a.ring = std::min(16, (227 * 1024 - fixed) / a.slot_bytes);
+    if (a.ring < 2) return false;
+    if (rs_smem_bytes(a) > (size_t)227 * 1024) return false;
+    *out = a;
+    return true;
+}
+static int rowstream_grid(const RsArgs &a) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(a.rows_total, (int64_t)num_sms()));
+}
+static bool rowstream_supported(const ollie_conv_shape *s, bool tf32, int transposed, int64_t OH, int64_t OW) {
+    RsArgs a;
+    return plan_rowstream(s, tf32, transposed, OH, OW, &a);
+}
+
+template <bool TF32, int FP>
+static ollie_status launch_rowstream_t(const CUtensorMap &tx, const RsArgs &a, cudaStream_t stream) {
+    auto kern = rowstream_conv_kernel<TF32, FP>;
+    static bool attr_done[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_done[dev & 63]) {
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_done[dev & 63] = true;
+    }
+    CUDA_TRY(launch(kern, dim3(rowstream_grid(a)), dim3(RS_THREADS), rs_smem_bytes(a), stream, tx, a));
+    return OLLIE_OK;
+}
+
+static ollie_status run_rowstream(const ollie_conv_shape *s, bool tf32, int transposed, const void *x, const void *wp,
+                                  void *y, int64_t OH, int64_t OW, cudaStream_t stream, const EpiArgs *epi = nullptr) {
+    RsArgs a;
+    if (!plan_rowstream(s, tf32, transposed, OH, OW, &a)) return fail(OLLIE_E_UNSUPPORTED, "no row-streaming plan for this shape");
+    a.wprep = wp;
+    a.y = y;
+    a.epi = epi ? *epi : EpiArgs{};
+    a.trace = g_fc_trace;
+    {   // debug-only ablations (OLLIE_RS_DBG, see RsArgs::dbg); 0 in production
+        static int dbg = -1;
+        if (dbg < 0) {
+            const char *e = getenv("OLLIE_RS_DBG");
+            dbg = e ? atoi(e) : 0;
+        }
+        a.dbg = dbg;
+    }
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
+    const int es = tf32 ? 4 : 2;
+    CUtensorMap tx;
+    {   // X as 4-D {c, w, h, n}; one box = wbox pixel rows of one image row, swizzled like the UMMA operand
+        cuuint64_t dims[4] = {(cuuint64_t)s->c, (cuuint64_t)s->w, (cuuint64_t)s->h, (cuuint64_t)s->n};
+        cuuint64_t strides[3] = {(cuuint64_t)(s->c * es), (cuuint64_t)(s->w * s->c * es), (cuuint64_t)(s->h * s->w * s->c * es)};
+        cuuint32_t box[4] = {(cuuint32_t)(a.rowbytes / es), (cuuint32_t)a.wbox, 1, 1};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        const CUtensorMapSwizzle sw = a.rowbytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                      : (a.rowbytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
+        CUresult r = enc(&tx, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                         const_cast<void *>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (row stream) failed (%d)", (int)r);
+    }
+    switch (a.Fp) {
+        case 4: return tf32 ? launch_rowstream_t<true, 4>(tx, a, stream) : launch_rowstream_t<false, 4>(tx, a, stream);
+        case 8: return tf32 ? launch_rowstream_t<true, 8>(tx, a, stream) : launch_rowstream_t<false, 8>(tx, a, stream);
+        case 12: return tf32 ? launch_rowstream_t<true, 12>(tx, a, stream) : launch_rowstream_t<false, 12>(tx, a, stream);
+        default: return tf32 ? launch_rowstream_t<true, 16>(tx, a, stream) : launch_rowstream_t<false, 16>(tx, a, stream);
+    }
 }
 
 // ------------------------------------------------------------------------ shapes
@@ -1105,10 +1251,19 @@ static bool is_identity_offset_add(const ollie_conv_shape *s, int transposed) {
 static int tuned_choice(const ollie_conv_shape *s, bool tf32, int transposed);   // autotune result (0 none)
 
 static int resolve_plan(const ollie_conv_shape *s, ollie_dtype dtype, int plan, int transposed) {
-    if (plan == OLLIE_PLAN_FUSED || plan == OLLIE_PLAN_UNFUSED || plan == OLLIE_PLAN_GEMM_RED) return plan;
-    if (is_identity_offset_add(s, transposed)) return OLLIE_PLAN_UNFUSED;
-    if (tuned_choice(s, dtype == OLLIE_TF32, transposed) == 3) return OLLIE_PLAN_GEMM_RED;
-    return fused_preferred(s, dtype == OLLIE_TF32, transposed) ? OLLIE_PLAN_FUSED : OLLIE_PLAN_UNFUSED;
+    if (plan == OLLIE_PLAN_FUSED || plan == OLLIE_PLAN_UNFUSED || plan == OLLIE_PLAN_GEMM_RED ||
+        plan == OLLIE_PLAN_ROWSTREAM)
+        return plan;
+    const bool tf32 = dtype == OLLIE_TF32;
+    const int tc = tuned_choice(s, tf32, transposed);
+    if (tc == 3) return OLLIE_PLAN_GEMM_RED;
+    if (tc == 4) return OLLIE_PLAN_ROWSTREAM;
+    if (is_identity_offset_add(s, transposed)) return tc == 1 ? OLLIE_PLAN_FUSED : OLLIE_PLAN_UNFUSED;
+    if (tc == 0 && s->w >= 96) {   // untuned: narrow layers over wide rows stream rows (>= 75% of the lanes busy)
+        int64_t OH, OW;
+        if (out_hw(s, transposed, &OH, &OW) && rowstream_supported(s, tf32, transposed, OH, OW)) return OLLIE_PLAN_ROWSTREAM;
+    }
+    return fused_preferred(s, tf32, transposed) ? OLLIE_PLAN_FUSED : OLLIE_PLAN_UNFUSED;
 }
 
 // GEMM_RED plan: fp32 output accumulator [n][OH][OW][F] in the workspace.
@@ -1188,6 +1343,10 @@ static ollie_status derived_layer(const ollie_conv_shape *s, ollie_dtype dtype, 
         const size_t need = rp == OLLIE_PLAN_GEMM_RED ? red_acc_bytes(s, OH, OW)
                                                       : (size_t)M * (size_t)ldT_of(s) * sizeof(float);
         if ((!ws || ws_bytes < need) && fused_supported(s, tf32, transposed)) rp = OLLIE_PLAN_FUSED;
+    }
+    if (rp == OLLIE_PLAN_ROWSTREAM) {
+        st = run_rowstream(s, tf32, transposed, x, wp, y, OH, OW, stream, &epi);
+        return st == OLLIE_OK ? ok() : st;
     }
     if (rp == OLLIE_PLAN_FUSED) {
         if (!fused_supported(s, tf32, transposed))
@@ -1783,6 +1942,12 @@ extern "C" ollie_status ollie_plan_describe(const ollie_conv_shape *s, ollie_dty
                  a.XB, a.Yb, a.Xb, a.Yp, a.MT, a.FS, a.f_slices, a.resident, a.nbuf, a.na, a.nb, a.BK, a.kchunks,
                  a.num_tiles, fused_grid(a), fused_smem_bytes(a), a.nclass, a.nph, a.ist, a.max_taps, a.sw128,
                  a.tmem_cols == 256 ? 2 : 1, a.pair, a.grb, a.nsb, a.ksplit, a.ipt, a.tma_y, a.grp8);
+    } else if (rp == OLLIE_PLAN_ROWSTREAM) {
+        RsArgs a;
+        if (!plan_rowstream(s, tf32, transposed, OH, OW, &a)) return fail(OLLIE_E_UNSUPPORTED, "no row-streaming plan");
+        snprintf(buf, len,
+                 "rowstream R=%d S=%d sub=%d N=%d NP=%d ring=%d mtr=%d rowbytes=%d ksteps=%d tmem_rows=%d grid=%d smem=%zu",
+                 a.R, a.S, a.sub, a.N, a.NP, a.ring, a.mtr, a.rowbytes, a.ksteps, a.nt, rowstream_grid(a), rs_smem_bytes(a));
     } else if (rp == OLLIE_PLAN_GEMM_RED) {
         snprintf(buf, len, "gemm_red BN=%d (%s as fp32 L2 reductions in the GEMM epilogue) + finish",
                  gemm_bn(s->n * s->h * s->w, s->r * s->s * s->f), transposed ? "selective add" : "OffsetAdd");
@@ -1814,6 +1979,7 @@ extern "C" void ollie_debug_force_ipt(int ipt) { g_force_ipt = ipt; }
 // Debug hook (not part of include/ollie.h): -1 auto, 0 consecutive-row lanes only, 1 grp8 lanes only.
 extern "C" void ollie_debug_force_grp8(int g8) { g_force_g8 = g8; }
 
+
 // ------------------------------------------------------------------------ autotune
 extern "C" ollie_status ollie_autotune_derived(const ollie_conv_shape *s, ollie_dtype dtype, int transposed,
                                                const void *x, const void *wp, void *y, void *ws, size_t ws_bytes,
@@ -1825,14 +1991,13 @@ extern "C" ollie_status ollie_autotune_derived(const ollie_conv_shape *s, ollie_
     if (!x || !wp || !y) return fail(OLLIE_E_INVALID, "null pointer");
     cudaStream_t stream = (cudaStream_t)stream_;
     const bool tf32 = dtype == OLLIE_TF32;
-    if (is_identity_offset_add(s, transposed)) {   // nothing to choose: the GEMM writes Y
-        if (best_us) *best_us = 0.f;
-        return ok();
-    }
+    // identity OffsetAdd (1x1, a6): the "unfused" candidate is the GEMM writing Y directly; the fused
+    // and row-streaming kernels (one tap) compete with it
+    const bool ident = is_identity_offset_add(s, transposed);
     PlanEntry *e = plan_entry_mut(s, tf32, transposed, OH, OW);
     const int64_t M = s->n * s->h * s->w;
-    const size_t need = (size_t)M * (size_t)ldT_of(s) * sizeof(float);
-    const bool unfused_ok = ws && ws_bytes >= need && !(transposed && s->dilation != 1);
+    const size_t need = ident ? 0 : (size_t)M * (size_t)ldT_of(s) * sizeof(float);
+    const bool unfused_ok = (ident || (ws && ws_bytes >= need)) && !(transposed && s->dilation != 1);
     std::vector<FusedArgs> cands;
     {
         std::lock_guard<std::mutex> g(g_plan_mu);
@@ -1858,6 +2023,7 @@ extern "C" ollie_status ollie_autotune_derived(const ollie_conv_shape *s, ollie_
                 if (d[0] == 'f' && idx >= 0 && idx < (int)cands.size()) { e->args = cands[idx]; e->tuned = 1; hit = true; }
                 else if (d[0] == 'u' && unfused_ok) { e->tuned = 2; hit = true; }
                 else if (d[0] == 'r') { e->tuned = 3; hit = true; }
+                else if (d[0] == 's' && rowstream_supported(s, tf32, transposed, OH, OW)) { e->tuned = 4; hit = true; }
             }
             fclose(fp);
             if (hit) {
@@ -1899,7 +2065,9 @@ extern "C" ollie_status ollie_autotune_derived(const ollie_conv_shape *s, ollie_
         if (t < best) { best = t; best_k = k; }
     }
     float t_unf = 1e30f;
-    if (unfused_ok && aligned16(ws)) {
+    if (ident) {
+        t_unf = time_it([&] { return run_gemm(M, s->f, s->c, tf32, x, wp, y, s->f, !tf32, stream); });
+    } else if (unfused_ok && aligned16(ws)) {
         t_unf = time_it([&] {
             ollie_status r = run_gemm(M, s->r * s->s * s->f, s->c, tf32, x, wp, ws, ldT_of(s), false, stream);
             if (r != OLLIE_OK) return r;
@@ -1910,25 +2078,30 @@ extern "C" ollie_status ollie_autotune_derived(const ollie_conv_shape *s, ollie_
     const bool red_ok = red_supported(s, transposed) && ws && ws_bytes >= red_acc_bytes(s, OH, OW) && aligned16(ws);
     if (red_ok)
         t_red = time_it([&] { return run_gemm_red(s, transposed, tf32, x, wp, (float *)ws, y, OH, OW, stream, nullptr); });
+    float t_rs = 1e30f;
+    if (rowstream_supported(s, tf32, transposed, OH, OW))
+        t_rs = time_it([&] { return run_rowstream(s, tf32, transposed, x, wp, y, OH, OW, stream); });
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    const bool any_timed = best < 1e29f || t_unf < 1e29f || t_red < 1e29f;
+    const bool any_timed = best < 1e29f || t_unf < 1e29f || t_red < 1e29f || t_rs < 1e29f;
     {
         std::lock_guard<std::mutex> g(g_plan_mu);
         if (!cands.empty()) e->args = cands[best_k >= 0 ? best_k : 0];
         // record a decision only when some plan actually ran and was timed: a failed tuning leaves
         // AUTO to the cost model instead of pinning it to an unmeasured plan
         if (any_timed) {
-            if (t_red < best && t_red <= t_unf) e->tuned = 3;
-            else e->tuned = (t_unf < best || best_k < 0) ? 2 : 1;
+            const float t_min = std::min(std::min(best, t_unf), std::min(t_red, t_rs));
+            if (t_rs == t_min) e->tuned = 4;
+            else if (t_red == t_min) e->tuned = 3;
+            else e->tuned = (t_unf == t_min || best_k < 0) ? 2 : 1;
         }
     }
-    if (best_us) *best_us = 1e3f * std::min(std::min(best, t_unf), t_red);
+    if (best_us) *best_us = 1e3f * std::min(std::min(best, t_unf), std::min(t_red, t_rs));
     if (!any_timed) return fail(OLLIE_E_UNSUPPORTED, "no runnable plan to tune");
     if (tune_file) {
         if (FILE *fp = fopen(tune_file, "a")) {
             const int t = e->tuned;
-            fprintf(fp, "%s %s %d\n", key, t == 1 ? "f" : t == 2 ? "u" : "r", t == 1 ? best_k : 0);
+            fprintf(fp, "%s %s %d\n", key, t == 1 ? "f" : t == 2 ? "u" : t == 3 ? "r" : "s", t == 1 ? best_k : 0);
             fclose(fp);
         }
     }
