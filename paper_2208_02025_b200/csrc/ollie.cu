@@ -1028,7 +1028,7 @@ static bool plan_rowstream(const ollie_conv_shape *s, bool tf32, int transposed,
     a.Fp = a.sub * a.sub * a.F;
     if (a.Fp != 4 && a.Fp != 8 && a.Fp != 12 && a.Fp != 16) return false;   // kernel variants
     a.N = a.R * a.Fp;                                                         // kernel rows x f' on N
-    if (a.N > RS_MAX_NP || a.S > 16 || a.pad_y < 0) return false;
+    if (a.N > RS_MAX_NP || a.S > RS_MAX_S || a.pad_y < 0) return false;
     // column shifts read the zero pixel rows kept on both sides of a slot
     if (a.pad_x < 0 || a.pad_x > RS_ZR || a.S - 1 - a.pad_x > RS_ZR) return false;
     a.NP = (int)ceil_div(a.N, 16) * 16;

@@ -40,8 +40,9 @@
 
 namespace ollie {
 
-constexpr int RS_THREADS = 256;       // warps 0-3: TMA, MMA, TMEM, idle; 4-7: epilogue
+constexpr int RS_THREADS = 384;       // warps 0-3: TMA, MMA, TMEM, idle; 4-11: two epilogue groups
 constexpr int RS_MAX_NP = 64;          // columns per input row the epilogue reads (r * f')
+constexpr int RS_MAX_S = 9;            // kernel columns of the stride-1 program (A-row shifts)
 constexpr int RS_ZR = 8;               // zero pixel rows before / after the image row in a slot (one swizzle atom)
 
 struct RsArgs {
@@ -141,7 +142,7 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
     if (warp == 0 && lane == 0) tma_prefetch_desc(&tmX);
     if (warp == 1 && lane == 0) {
         for (int i = 0; i < a.ring; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-        for (int i = 0; i < a.nt; ++i) { mbar_init(&afull[i], 1); mbar_init(&aempty[i], 4); }
+        for (int i = 0; i < a.nt; ++i) { mbar_init(&afull[i], 1); mbar_init(&aempty[i], 8); }
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -240,14 +241,24 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
                 tc_fence_after();
                 const uint32_t d0 = tmem_base + (uint32_t)t * row_cols;
                 const uint32_t a0 = ring_a16 + (uint32_t)slot * slot16;
+                // One elected thread issues the row.  The (shift, k-step) walk is unrolled with compile-time
+                // bounds so every MMA gets its own descriptor registers: rewriting the registers an in-flight
+                // tcgen05.mma still reads stalls the issue (a rolled loop ran at ~230 cycles per MMA).
                 if (elect_one()) {
-                    for (int h = 0; h < mtr; ++h)
-                        for (int j = 0; j < S; ++j)
-                            for (int k = 0; k < ksteps; ++k)
-                                umma<kTF32>(d0 + (uint32_t)h * acc_cols,
-                                            dtpl | (uint64_t)((a0 + (uint32_t)h * mt16 + (uint32_t)j * row16 + 2u * k) & 0x3FFF),
-                                            dtpl | (uint64_t)((b16 + (uint32_t)j * bj16 + 2u * k) & 0x3FFF), idesc,
-                                            (j == 0 && k == 0) ? 0u : 1u);
+                    for (int h = 0; h < mtr; ++h) {
+                        const uint32_t dh = d0 + (uint32_t)h * acc_cols, ah = a0 + (uint32_t)h * mt16;
+#pragma unroll
+                        for (int j = 0; j < RS_MAX_S; ++j) {
+                            if (j < S) {
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+                                    if (k < ksteps)
+                                        umma<kTF32>(dh, dtpl | (uint64_t)((ah + (uint32_t)j * row16 + 2u * k) & 0x3FFF),
+                                                    dtpl | (uint64_t)((b16 + (uint32_t)j * bj16 + 2u * k) & 0x3FFF), idesc,
+                                                    (j == 0 && k == 0) ? 0u : 1u);
+                            }
+                        }
+                    }
                 }
                 __syncwarp();
                 umma_commit_elect(&afull[t]);
@@ -261,7 +272,12 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
         }
     } else if (warp >= 4) {
         // ===== epilogue: Y[y] = Sum_i column group i of D_{y - pad_y + i}; element-wise ops; stores =====
+        // Two groups of 4 warps: group gi takes the CTA's output rows k with k % 2 == gi (one warp per SM
+        // sub-partition runs this loop at dependent-instruction latency: two rows in flight per
+        // sub-partition double the rate).  Each group hands every input row's TMEM slot back once
+        // (aempty counts 8 arrivals): after its last output row reading it, or at the run's end.
         const int q = warp & 3;                          // TMEM lane quadrant of this warp
+        const int gi = (warp - 4) >> 2;
         pdl_wait();                                      // Y may still be read by the previous kernel
         const int nt = a.nt, R = a.R, mtr = a.mtr, pad_y = a.pad_y, OWc = a.OWc, sub = a.sub, F = a.F;
         const uint32_t row_cols = (uint32_t)a.row_cols, acc_cols = (uint32_t)a.acc_cols;
@@ -273,6 +289,7 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
         uint32_t seq0 = 0;                               // sequence number of the run's first loaded row
         uint32_t n_c = 0, ph_c = 0;                      // cursor: newest row waited for (seq, slot, phase)
         int t_c = 0;
+        uint32_t krow = 0;                               // output row index in the CTA's sequence
         for (int64_t g = g0; g < g1;) {
             const RsSeg s = rs_seg(a, g, g1);
             int rel = s.rlo;                             // next input row whose TMEM slot is handed back
@@ -287,7 +304,8 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
                 }
             };
             const int64_t img_el = (int64_t)s.img * a.OH;
-            for (int y = s.ylo; y < s.yhi; ++y) {
+            for (int y = s.ylo; y < s.yhi; ++y, ++krow) {
+                if ((int)(krow & 1u) != gi) continue;
                 const int rb = y - pad_y;                // input row of kernel row 0
                 const int rtop = min(rb + R - 1, s.rhi - 1);
                 if (rtop >= s.rlo) {                     // D of every row up to rtop is complete (in-order commits)
@@ -390,7 +408,7 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
                     const int64_t kr = (int64_t)(y - s.ylo) + (g - g0);
                     if (kr < 64) a.trace[192 + kr] = rs_gtimer();
                 }
-                release_upto(rb);                        // input row rb is read by no later output row
+                release_upto(rb + 1);                    // this group's next row (y + 2) reads rows >= rb + 2
             }
             release_upto(s.rhi - 1);
             seq0 += (uint32_t)(s.rhi - s.rlo);
