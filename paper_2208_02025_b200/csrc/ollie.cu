@@ -1032,7 +1032,7 @@ static bool plan_rowstream(const ollie_conv_shape *s, bool tf32, int transposed,
     // column shifts read the zero pixel rows kept on both sides of a slot
     if (a.pad_x < 0 || a.pad_x > RS_ZR || a.S - 1 - a.pad_x > RS_ZR) return false;
     a.NP = (int)ceil_div(a.N, 16) * 16;
-    a.acc_cols = (int)ceil_div(a.NP, 32) * 32;
+    a.acc_cols = a.NP;                                  // accumulators packed at 16-column granularity
     const int cb = (int)(s->c * es);
     a.rowbytes = cb <= 32 ? 32 : (cb <= 64 ? 64 : 128);
     a.swz = a.rowbytes == 32 ? 6 : (a.rowbytes == 64 ? 4 : 2);
