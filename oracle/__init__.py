@@ -14,6 +14,8 @@ explicit im2col, torch CPU fp64 ``F.conv2d`` / ``F.conv_transpose2d`` as an
 independent library, the all-ones worked example, closed forms,
 adjointness, the derivation identity, the row-wrap sentinel (Q5),
 the ConvT tap table, identity / permutation / round-trip checks for eOps.
+The im2col ("tap folding") eOperator and its weight side are pinned by the exact
+derivation identity conv == fold(X) . fold(W)^T and by textbook sliding windows.
 No function here is "parity unpinned".
 """
 from __future__ import annotations
@@ -280,4 +282,41 @@ def g2bmm_residue_split(a_blk, b_blk, W: int, d: int) -> np.ndarray:
     for r in range(d):
         if r < L:
             out[:, r::d] = g2bmm(a[:, r::d], b[:, r::d], W, 1)
+    return out
+
+
+# ----------------------------------------------------------------------------- im2col ("tap folding") eOperator
+def tap_fold(x_nhwc, r: int, s: int, pad: int = 0, stride: int = 1, dilation: int = 1, kp: int | None = None) -> np.ndarray:
+    """The im2col layout eOperator of a Conv2d -- variable substitution of the conv expression
+    (E1) that moves the taps into the reduction index so operator matching
+    sees a plain Matmul with k = (i, j, c):
+        A'[b, oy, ox, (i*S + j)*C + c] = X[b, oy*st - p + i*d, ox*st - p + j*d, c]
+    zero outside the image and for k >= r*s*C up to the padded width kp.  Written out
+    per (i, j) tap by strided slicing of the zero-padded input."""
+    x = _f64(x_nhwc)
+    n, h, w, c = x.shape
+    oh = conv_out_size(h, r, pad, stride, dilation)
+    ow = conv_out_size(w, s, pad, stride, dilation)
+    kp = r * s * c if kp is None else int(kp)
+    if kp < r * s * c:
+        raise ValueError("kp must cover r*s*c")
+    xp = np.zeros((n, h + 2 * pad, w + 2 * pad, c))
+    xp[:, pad:pad + h, pad:pad + w, :] = x
+    out = np.zeros((n, oh, ow, kp))
+    for i in range(r):
+        for j in range(s):
+            k0 = (i * s + j) * c
+            y0, x0 = i * dilation, j * dilation
+            out[:, :, :, k0:k0 + c] = xp[:, y0:y0 + stride * (oh - 1) + 1:stride, x0:x0 + stride * (ow - 1) + 1:stride, :]
+    return out
+
+
+def weight_fold(w_fcrs, kp: int | None = None) -> np.ndarray:
+    """The weight side of the im2col derivation: W''[f, (i*S + j)*C + c] = W[f, c, i, j], zero for
+    k >= r*s*C (the 1x1 conv / Matmul weight that pairs with tap_fold)."""
+    w = _f64(w_fcrs)
+    f, c, r, s = w.shape
+    kp = r * s * c if kp is None else int(kp)
+    out = np.zeros((f, kp))
+    out[:, :r * s * c] = w.transpose(0, 2, 3, 1).reshape(f, r * s * c)
     return out

@@ -256,3 +256,42 @@ def test_configured_layers_sampled_small():
                 b = oracle.conv2d_derived(x, w, lay.pad, lay.stride, lay.dilation)
             assert a.shape == (1, lay.oh, lay.ow, lay.f)
             assert np.array_equal(a, b)
+
+
+# ----------------------------------------------------------------------------- im2col ("tap folding") eOperator
+FOLD = [  # (h, w, c, f, r, s, pad, stride, dil, kp)
+    (6, 7, 1, 4, 5, 5, 2, 1, 1, 32), (5, 6, 3, 2, 3, 3, 1, 1, 1, 32), (7, 7, 2, 2, 3, 3, 1, 2, 1, 24),
+    (8, 6, 1, 3, 3, 3, 2, 1, 2, 16), (9, 9, 1, 2, 9, 9, 4, 1, 1, 88),
+]
+
+
+@pytest.mark.parametrize("h,w,c,f,r,s,pad,st,dil,kp", FOLD)
+def test_tap_fold_derivation_exact(h, w, c, f, r, s, pad, st, dil, kp):
+    """conv(X, W) == tap_fold(X) . weight_fold(W)^T exactly in integer mode (the im2col derivation),
+    tap_fold's columns are the textbook sliding windows in (i, j, c) order, and the padding columns
+    k >= r*s*c are zero."""
+    x = _ints((2, h, w, c), 31 + h)
+    wt = _ints((f, c, r, s), 32 + w)
+    a = oracle.tap_fold(x, r, s, pad, st, dil, kp)
+    wf = oracle.weight_fold(wt, kp)
+    assert np.array_equal(a @ wf.T, oracle.conv2d(x, wt, pad, st, dil))
+    assert not a[..., r * s * c:].any()
+    xp = np.pad(x, ((0, 0), (pad, pad), (pad, pad), (0, 0)))
+    win = np.lib.stride_tricks.sliding_window_view(xp, (dil * (r - 1) + 1, dil * (s - 1) + 1), axis=(1, 2))
+    win = win[:, ::st, ::st, :, ::dil, ::dil]                        # n, OH, OW, c, r, s
+    cols = win.transpose(0, 1, 2, 4, 5, 3).reshape(win.shape[0], win.shape[1], win.shape[2], -1)   # (r, s, c)
+    assert np.array_equal(a[..., :r * s * c], cols)
+
+
+def test_tap_fold_one_hot_positions():
+    """A single one at input pixel (2, 3): column (i, j) of output (oy, ox) is 1 exactly where
+    oy - 2 + i = 2 and ox - 2 + j = 3 (5x5, pad 2, stride 1)."""
+    x = np.zeros((1, 6, 7, 1))
+    x[0, 2, 3, 0] = 1
+    a = oracle.tap_fold(x, 5, 5, 2, 1, 1, 25)
+    for oy in range(6):
+        for ox in range(7):
+            for i in range(5):
+                for j in range(5):
+                    want = 1.0 if (oy - 2 + i == 2 and ox - 2 + j == 3) else 0.0
+                    assert a[0, oy, ox, i * 5 + j] == want
