@@ -218,6 +218,18 @@ ollie_status ollie_merged_gemm(int64_t M, int64_t N, int64_t K, ollie_dtype dtyp
 ollie_status ollie_offset_add(const ollie_conv_shape *shape, int transposed, const float *T,
                               int64_t ldT, ollie_dtype y_dtype, void *y_nhwc, ollie_stream_t stream);
 
+/* im2col ("tap folding") layout eOperator of the Conv2d `shape` describes (stride, dilation, pad;
+ * the output grid OH x OW is the conv's): variable substitution of E1 that moves the taps
+ * into the Matmul's reduction index, so operator matching sees a plain Matmul:
+ *     out[b][oy][ox][k] = x[b][oy*stride - pad + i*dil][ox*stride - pad + j*dil][ch],
+ *     k = (i*s + j)*c + ch < r*s*c;  0 outside the image and for r*s*c <= k < kp.
+ * Used for layers with few input channels (FSRCNN's c = 1 feature extraction), which then run as a
+ * 1x1 conv over kp-wide pixels.  x_nhwc [n][h][w][c], out [n][OH][OW][kp], device, `dtype` elements
+ * (BF16, or TF32 / FP32 for 4-byte storage); kp >= r*s*c with kp*sizeof(elem) % 16 == 0 and out
+ * 16-byte aligned, else OLLIE_E_INVALID / OLLIE_E_ALIGN.  Pure indexing: bit-exact. */
+ollie_status ollie_tap_fold(const ollie_conv_shape *shape, ollie_dtype dtype, const void *x_nhwc, int64_t kp,
+                            void *out, ollie_stream_t stream);
+
 /* ---------------------------------------------------------------------------------
  * a5-a7 -- scoped index-expression eOperator (SPEC IndexExpr / TensorDecl / Scope /
  * Compute; general format L_x Sum_y f(T[tau(x,y)])).

@@ -14,6 +14,7 @@
 // thread owns VEC consecutive f of one output pixel and issues all its r*s tap loads
 // before summing.  Tap order (i, j) is fixed, so results are deterministic.
 #pragma once
+#include <type_traits>
 #include "sm100_ptx.cuh"
 #include "epilogue.cuh"
 
@@ -211,6 +212,129 @@ __global__ void __launch_bounds__(256) weight_dlt_kernel(const E *__restrict__ s
     for (int k = ty; k < 32; k += 8) {
         const int64_t ij = ij0 + k, c = c0 + tx;
         if (c < C && ij < RS) dst[(ij * F + f) * C + c] = tile[tx][k];
+    }
+}
+
+// a7 instance: the im2col ("tap folding") layout eOperator of a Conv2d -- variable substitution of
+// E1 that moves the taps into the Matmul's reduction index (operator matching):
+//     A'[b, oy, ox, k] = X[b, oy*st - p + i*d, ox*st - p + j*d, c],   k = (i*S + j)*C + c < R*S*C
+// zero outside the image and for R*S*C <= k < KP.  A layer with few channels (FSRCNN's
+// c = 1 feature extraction) then runs as a 1x1 conv over KP-wide pixels instead of r*s taps that
+// each use one channel of a 16-wide MMA K.  One thread writes one 16-byte chunk of one output pixel
+// (coalesced stores, the HBM-bound side); the r*s gathered reads hit L1 / L2 (every input pixel is
+// read by r*s neighbours).
+struct TapFoldArgs {
+    const void *x;
+    void *out;
+    int32_t H, W, C, R, S, pad, st, dil, OH, OW, KP, RSC;
+    int64_t items;             // n * OH * OW * (KP / VE)
+};
+
+template <bool kF32, typename I>
+__global__ void __launch_bounds__(256) tap_fold_kernel(TapFoldArgs a) {
+    constexpr int VE = kF32 ? 4 : 8;                 // elements per 16-byte chunk
+    using E = typename std::conditional<kF32, uint32_t, uint16_t>::type;
+    pdl_wait();                                      // X may be written by the previous kernel
+    const E *x = reinterpret_cast<const E *>(a.x);
+    const I chunks = (I)(a.KP / VE);
+    const I stride = (I)gridDim.x * blockDim.x;
+    for (I it = (I)blockIdx.x * blockDim.x + threadIdx.x; it < (I)a.items; it += stride) {
+        const I kc = it % chunks;
+        I pix = it / chunks;
+        const int ox = (int)(pix % a.OW);
+        pix /= a.OW;
+        const int oy = (int)(pix % a.OH);
+        const I b = pix / a.OH;
+        // (i, j, c) of the chunk's first k, then walked incrementally
+        const int k0 = (int)kc * VE;
+        int c = k0 % a.C, tap = k0 / a.C;
+        int j = tap % a.S, i = tap / a.S;
+        E v[VE];
+#pragma unroll
+        for (int e = 0; e < VE; ++e) {
+            E val = 0;
+            if (k0 + e < a.RSC) {
+                const int iy = oy * a.st - a.pad + i * a.dil, ix = ox * a.st - a.pad + j * a.dil;
+                if (iy >= 0 && iy < a.H && ix >= 0 && ix < a.W)
+                    val = __ldg(x + (((int64_t)b * a.H + iy) * a.W + ix) * a.C + c);
+                if (++c == a.C) {
+                    c = 0;
+                    if (++j == a.S) { j = 0; ++i; }
+                }
+            }
+            v[e] = val;
+        }
+        uint4 pk;
+        if constexpr (kF32) {
+            pk = make_uint4(v[0], v[1], v[2], v[3]);
+        } else {
+            pk = make_uint4((uint32_t)v[0] | ((uint32_t)v[1] << 16), (uint32_t)v[2] | ((uint32_t)v[3] << 16),
+                            (uint32_t)v[4] | ((uint32_t)v[5] << 16), (uint32_t)v[6] | ((uint32_t)v[7] << 16));
+        }
+        *reinterpret_cast<uint4 *>(reinterpret_cast<E *>(a.out) + (int64_t)it * VE) = pk;
+    }
+}
+
+// Row-tiled form: one CTA per output row (b, oy) stages the r input rows the row reads
+// (oy*st - p + i*d, zero outside the image) in shared memory with coalesced loads, then writes the
+// row's OW * KP outputs as consecutive 16-byte chunks (lane t -> chunk t: fully coalesced stores).
+template <bool kF32>
+__global__ void __launch_bounds__(256) tap_fold_rows_kernel(TapFoldArgs a) {
+    constexpr int VE = kF32 ? 4 : 8;
+    using E = typename std::conditional<kF32, uint32_t, uint16_t>::type;
+    extern __shared__ uint8_t tf_smem[];
+    E *rows = reinterpret_cast<E *>(tf_smem);        // [R][W * C]
+    pdl_wait();
+    const E *x = reinterpret_cast<const E *>(a.x);
+    const int WC = a.W * a.C;
+    const int cpp = a.KP / VE;                       // 16-byte chunks per output pixel
+    const int chunks = a.OW * cpp;
+    int off[VE], jd[VE];                             // smem offset (without the pixel) and column shift per element
+    bool kv[VE];
+    {
+        const int k0 = (threadIdx.x % cpp) * VE;
+        int c = k0 % a.C, tap = k0 / a.C;
+        int j = tap % a.S, i = tap / a.S;
+#pragma unroll
+        for (int e = 0; e < VE; ++e) {
+            kv[e] = k0 + e < a.RSC;
+            off[e] = i * WC + c;
+            jd[e] = j * a.dil;
+            if (++c == a.C) {
+                c = 0;
+                if (++j == a.S) { j = 0; ++i; }
+            }
+        }
+    }
+    for (int64_t row = blockIdx.x; row < a.items; row += gridDim.x) {   // items = n * OH output rows
+        const int oy = (int)(row % a.OH);
+        const int64_t b = row / a.OH;
+        __syncthreads();                             // the previous row's readers are done
+        for (int t = threadIdx.x; t < a.R * WC; t += blockDim.x) {
+            const int i = t / WC, e = t - i * WC;
+            const int iy = oy * a.st - a.pad + i * a.dil;
+            rows[t] = (iy >= 0 && iy < a.H) ? __ldg(x + (b * a.H + iy) * (int64_t)WC + e) : (E)0;
+        }
+        __syncthreads();
+        E *orow = reinterpret_cast<E *>(a.out) + row * (int64_t)a.OW * a.KP;
+        for (int ch = threadIdx.x; ch < chunks; ch += blockDim.x) {
+            // the thread's k-chunk is fixed (blockDim % (KP / VE) == 0, host-checked): its (i, j, c)
+            // offsets were decoded once, only the pixel moves
+            const int ox = ch / cpp;
+            const int xo = ox * a.st - a.pad;
+            E v[VE];
+#pragma unroll
+            for (int e = 0; e < VE; ++e) {
+                const int ix = xo + jd[e];
+                v[e] = (kv[e] && ix >= 0 && ix < a.W) ? rows[off[e] + ix * a.C] : (E)0;
+            }
+            uint4 pk;
+            if constexpr (kF32) pk = make_uint4(v[0], v[1], v[2], v[3]);
+            else
+                pk = make_uint4((uint32_t)v[0] | ((uint32_t)v[1] << 16), (uint32_t)v[2] | ((uint32_t)v[3] << 16),
+                                (uint32_t)v[4] | ((uint32_t)v[5] << 16), (uint32_t)v[6] | ((uint32_t)v[7] << 16));
+            *reinterpret_cast<uint4 *>(orow + (int64_t)ch * VE) = pk;
+        }
     }
 }
 

@@ -1228,6 +1228,56 @@ static ollie_status run_offset_add(const ollie_conv_shape *s, int transposed, co
     return OLLIE_OK;
 }
 
+// ------------------------------------------------------------------------ im2col ("tap folding") eOperator
+extern "C" ollie_status ollie_tap_fold(const ollie_conv_shape *shape, ollie_dtype dtype, const void *x_nhwc, int64_t kp,
+                                       void *out, ollie_stream_t stream) {
+    if (!shape) return fail(OLLIE_E_INVALID, "null shape");
+    int64_t OH, OW;
+    ollie_status st = check_shape(shape, 0, &OH, &OW);
+    if (st != OLLIE_OK) return st;
+    if (dtype != OLLIE_BF16 && dtype != OLLIE_TF32 && dtype != OLLIE_FP32)
+        return fail(OLLIE_E_UNSUPPORTED, "tap fold dtype must be BF16 or TF32 / FP32");
+    const int es = dtype == OLLIE_BF16 ? 2 : 4;
+    const int64_t rsc = shape->r * shape->s * shape->c;
+    if (kp < rsc) return fail(OLLIE_E_INVALID, "kp = %lld < r*s*c = %lld", (long long)kp, (long long)rsc);
+    if ((kp * es) % 16 != 0) return fail(OLLIE_E_ALIGN, "kp * sizeof(elem) must be a multiple of 16");
+    if (!x_nhwc || !out) return fail(OLLIE_E_INVALID, "null pointer");
+    if (!aligned16(out)) return fail(OLLIE_E_ALIGN, "out must be 16-byte aligned");
+    if (shape->h > INT32_MAX || shape->w > INT32_MAX || shape->c > INT32_MAX || kp > INT32_MAX)
+        return fail(OLLIE_E_UNSUPPORTED, "tap fold extents exceed int32");
+    TapFoldArgs a{};
+    a.x = x_nhwc;
+    a.out = out;
+    a.H = (int)shape->h; a.W = (int)shape->w; a.C = (int)shape->c; a.R = (int)shape->r; a.S = (int)shape->s;
+    a.pad = shape->pad; a.st = shape->stride; a.dil = shape->dilation;
+    a.OH = (int)OH; a.OW = (int)OW; a.KP = (int)kp; a.RSC = (int)rsc;
+    const int ve = 16 / es;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t rows_smem = (size_t)shape->r * shape->w * shape->c * es;
+    if (rows_smem <= 48 * 1024 && 256 % (kp / ve) == 0) {   // row-tiled: r input rows in smem, coalesced stores
+        a.items = shape->n * OH;
+        const unsigned g1 = (unsigned)std::max<int64_t>(std::min<int64_t>(a.items, (int64_t)num_sms() * 64), 1);
+        if (es == 2) CUDA_TRY(launch(tap_fold_rows_kernel<false>, dim3(g1), dim3(256), rows_smem, s, a));
+        else CUDA_TRY(launch(tap_fold_rows_kernel<true>, dim3(g1), dim3(256), rows_smem, s, a));
+        CHECK_LAUNCH();
+        return ok();
+    }
+    a.items = shape->n * OH * OW * (kp / ve);
+    const int tpb = 256;
+    const int64_t blocks = std::min<int64_t>(ceil_div(a.items, tpb), (int64_t)num_sms() * 16);
+    const unsigned g = (unsigned)std::max<int64_t>(blocks, 1);
+    const bool i32 = a.items + (int64_t)g * tpb < (1ll << 31);
+    if (es == 2) {
+        if (i32) CUDA_TRY(launch(tap_fold_kernel<false, int32_t>, dim3(g), dim3(tpb), 0, s, a));
+        else CUDA_TRY(launch(tap_fold_kernel<false, int64_t>, dim3(g), dim3(tpb), 0, s, a));
+    } else {
+        if (i32) CUDA_TRY(launch(tap_fold_kernel<true, int32_t>, dim3(g), dim3(tpb), 0, s, a));
+        else CUDA_TRY(launch(tap_fold_kernel<true, int64_t>, dim3(g), dim3(tpb), 0, s, a));
+    }
+    CHECK_LAUNCH();
+    return ok();
+}
+
 extern "C" ollie_status ollie_offset_add(const ollie_conv_shape *shape, int transposed, const float *T, int64_t ldT,
                                          ollie_dtype y_dtype, void *y_nhwc, ollie_stream_t stream) {
     int64_t OH, OW;

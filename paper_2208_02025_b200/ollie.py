@@ -104,6 +104,7 @@ _sig = {
     "ollie_merged_gemm": (c_int, [c_int64, c_int64, c_int64, c_int, c_void_p, c_void_p, c_void_p, c_int64,
                                   c_void_p]),
     "ollie_offset_add": (c_int, [_P(ConvShape), c_int, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
+    "ollie_tap_fold": (c_int, [_P(ConvShape), c_int, c_void_p, c_int64, c_void_p, c_void_p]),
     "ollie_eop_analyze": (c_int, [_P(Eop), _P(EopInfo)]),
     "ollie_g2bmm": (c_int, [c_int64, c_int64, c_int64, c_int64, c_int64, c_int, c_void_p, c_void_p, c_void_p, c_int64,
                             c_int, c_void_p]),
@@ -248,6 +249,11 @@ def merged_gemm(M: int, N: int, K: int, dtype: int, A, B, T, ldT: int, stream=No
 def offset_add(shape: ConvShape, transposed: bool, T, ldT: int, y_dtype: int, y, stream=None):
     _check(_lib.ollie_offset_add(ctypes.byref(shape), int(transposed), _ptr(T), ldT, y_dtype, _ptr(y),
                                  _stream(stream)), "ollie_offset_add")
+
+
+def tap_fold(shape: ConvShape, dtype: int, x, kp: int, out, stream=None):
+    """im2col ("tap folding") eOperator: out[b, oy, ox, (i*s + j)*c + ch] = x[b, oy*st-p+i*d, ox*st-p+j*d, ch]."""
+    _check(_lib.ollie_tap_fold(ctypes.byref(shape), dtype, _ptr(x), kp, _ptr(out), _stream(stream)), "ollie_tap_fold")
 
 
 # ----------------------------------------------------------------------------- eOperators

@@ -65,6 +65,9 @@ def test_dcgan_stack_random():
 def test_launch_counts():
     from paper_2208_02025_b200.stack import DerivedStack
     st = DerivedStack(_fsrcnn_small(1, 16), True)
-    # f=12 layers write zero-padded 16-channel outputs instead of a separate pad launch
-    assert sum(1 for sl in st.layers if sl.pad_eop is not None) == 1   # only the c=1 network input
+    # f=12 layers write zero-padded 16-channel outputs instead of a separate pad launch; the c=1
+    # network input is tap-folded (im2col eOperator) for its 5x5 layer, nothing else is padded
+    assert sum(1 for sl in st.layers if sl.pad_eop is not None) == 0
+    assert [sl.fold for sl in st.layers] == [True] + [False] * (len(st.layers) - 1)
+    assert DerivedStack(_fsrcnn_small(1, 16), True, fold_taps=False).layers[0].pad_eop is not None
     assert st.launches() >= len(st.layers)
