@@ -636,8 +636,10 @@ def gpu_main(args):
     d, dl = recs[dom], wl.layers[dom]
     if d["bound"] == "tensor":
         pk = d["tc_peak_tflops"]
+        nominal = 2250.0 if dl.dtype == "bf16" else 1125.0          # dense bf16 / TF32 per GPU (B200 spec)
         roof = {"kernel": d["layer"], "bound": "tensor", "achieved": d["tflops"], "peak": pk, "unit": "TFLOP/s",
-                "frac": d["tflops"] / pk, "peak_source": peak_src}
+                "frac": d["tflops"] / pk, "peak_source": peak_src,
+                "frac_of_nominal": d["tflops"] / nominal, "nominal_peak": nominal}
     else:
         roof = {"kernel": d["layer"], "bound": "hbm", "achieved": d["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": d["gbs"] / peaks["hbm_gbs"], "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peaks['source']})"}

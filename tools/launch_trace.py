@@ -33,9 +33,16 @@ with torch.cuda.stream(s):
     for _ in range(3):
         conv(xd, y, s.cuda_stream)
 torch.cuda.synchronize()
+FLUSH = os.environ.get("FLUSH", "0") == "1"       # evict L2 (2x L2 write + read back) before every launch
+if FLUSH:
+    fbuf = torch.empty(2 * torch.cuda.get_device_properties(0).L2_cache_size, dtype=torch.uint8, device="cuda")
+    fsink = torch.empty((), dtype=torch.int64, device="cuda")
 g = torch.cuda.CUDAGraph()
 with torch.cuda.graph(g, stream=s):
     for k in range(REPS):
+        if FLUSH:
+            fbuf.fill_(k)
+            torch.sum(fbuf.view(torch.int64), dim=0, out=fsink)
         O._lib.ollie_debug_set_trace(bufs[k].data_ptr())
         conv(xd, y, s.cuda_stream)
 O._lib.ollie_debug_set_trace(None)

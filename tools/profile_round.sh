@@ -17,7 +17,7 @@ for cfg in ${CFGS:-resnet18 csrnet fsrcnn}; do
       python bench.py --config $cfg --steps 2 --warmup 3 --no-cpu-baseline --no-cudnn --no-graph \
       > gpurun_out/${TAG}_launches_${cfg}.log 2>&1
   timeout 1500 ncu --set full --clock-control none --import-source on --profile-from-start off \
-      -k regex:"fused_conv|merged_gemm|offset_add|selective_add|eop_" -s ${SKIP:-0} -c ${COUNT:-12} \
+      -k regex:"fused_conv|merged_gemm|rowstream_conv|tap_fold|offset_add|selective_add|eop_" -s ${SKIP:-0} -c ${COUNT:-12} \
       -o gpurun_out/${TAG}_full_${cfg} python tools/run_layer.py --config $cfg --iters 1 \
       > gpurun_out/${TAG}_full_${cfg}.log 2>&1
   echo "$cfg done"

@@ -36,8 +36,8 @@ SCALE = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1, "Tbyte": 1e12, "us
 
 
 def family(name):
-    for f in ("fused_conv", "merged_gemm", "offset_add", "selective_add", "eop_affine_gather",
-              "eop_affine_transpose", "eop_eval", "weight_dlt"):
+    for f in ("fused_conv", "merged_gemm", "rowstream_conv", "tap_fold", "offset_add", "selective_add",
+              "eop_affine_gather", "eop_affine_rows", "eop_affine_transpose", "eop_eval", "weight_dlt"):
         if f in name:
             return f
     return name.split("(")[0][-40:]
@@ -100,8 +100,9 @@ for cfg in cfgs:
                 t = float(r[vi].replace(",", "")) / 1e3
             tot[family(r[ki])] += t
             n[family(r[ki])] += 1
-        ours = {k: v for k, v in tot.items() if k in ("fused_conv", "merged_gemm", "offset_add", "selective_add",
-                                                      "eop_affine_gather", "eop_affine_transpose", "eop_eval",
+        ours = {k: v for k, v in tot.items() if k in ("fused_conv", "merged_gemm", "rowstream_conv", "tap_fold",
+                                                      "offset_add", "selective_add", "eop_affine_gather",
+                                                      "eop_affine_rows", "eop_affine_transpose", "eop_eval",
                                                       "weight_dlt")}
         s_all = sum(ours.values()) or 1.0
         lines = [f"# {tag} launch list of `python bench.py --config {cfg} --steps 2 --warmup 3 --no-graph` under "
