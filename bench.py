@@ -276,6 +276,40 @@ def _graph(torch, fn, stream, reps=1):
     return g
 
 
+def time_graph_flushed(torch, fn, stream, flusher, reps=20):
+    """Device time (us) of one call of fn(stream) from an evicted L2, measured differentially: a CUDA
+    graph of `reps` x (flush + fn) and a graph of `reps` x flush are each timed as one event pair,
+    and the difference is divided by reps -- single short replays cannot be timed directly here
+    (CUDA event timestamps on this box are quantised to ~2 us).  Median of 3 such measurements."""
+    def cap(with_fn):
+        gg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gg, stream=stream):
+            for k in range(reps):
+                flusher(k)
+                if with_fn:
+                    fn(stream)
+        torch.cuda.synchronize()
+        return gg
+    with torch.cuda.stream(stream):
+        fn(stream)                                   # (autotune / cuDNN algorithm choice outside capture)
+    torch.cuda.synchronize()
+    gf, gfl = cap(False), cap(True)
+    out = []
+    for _ in range(3):
+        ts = []
+        for gg in (gf, gfl):
+            with torch.cuda.stream(stream):
+                gg.replay()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                gg.replay()
+                e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3)
+        out.append((ts[1] - ts[0]) / reps)
+    return sorted(out)[1]
+
+
 def time_graph(torch, g, stream, flush, reps=21, per=1):
     """Device time (us) of one replay of g: L2 flushed before each replay when `flush` is given
     (cold), else replays back to back after one warm replay; divided by `per`.  CUDA event
@@ -400,8 +434,9 @@ def _cudnn_fns(torch, layers, chained, x_host, w_dev, dev):
 
 
 def per_layer_records(torch, wl, stream, flush, peaks, tc_peak, with_cudnn=True):
-    """Per layer: ours and cuDNN, each layer captured alone in a CUDA graph; flushed (L2 evicted
-    before each replay) and warm (10 calls back to back in one graph) device times."""
+    """Per layer: ours and cuDNN by the same method -- flushed (L2 evicted before each call,
+    time_graph_flushed's differential graph timing) and warm (10 calls back to back in one graph)
+    device times; the step likewise."""
     from paper_2208_02025_b200 import ollie as O
     recs = []
     cud_step = cud_layers = None
@@ -418,28 +453,24 @@ def per_layer_records(torch, wl, stream, flush, peaks, tc_peak, with_cudnn=True)
         x = sl.y
     for li, (sl, lay) in enumerate(zip(wl.stack.layers, wl.layers)):
         fn = (lambda sl, src: (lambda s: sl(src, s.cuda_stream)))(sl, srcs[li])
-        g1 = _graph(torch, fn, stream)
         g10 = _graph(torch, fn, stream, reps=10)
-        ours_f = time_graph(torch, g1, stream, flush)
+        ours_f = time_graph_flushed(torch, fn, stream, flush)
         ours_w = time_graph(torch, g10, stream, None, per=10)
         rec = {"layer": lay.name, "plan": O.plan_describe(sl.conv.shape, sl.conv.code, sl.conv.plan, sl.conv.transposed),
                "launches": sl.launches(), "useful_gflop": lay.useful_flops / 1e9, "alg_mb": layer_bytes(lay) / 1e6,
                "ours_us": ours_f, "ours_warm_us": ours_w, **roofline_entry(lay, ours_f, peaks, tc_peak)}
         if cud_layers is not None:
-            c1 = _graph(torch, cud_layers[li], stream)
             c10 = _graph(torch, cud_layers[li], stream, reps=10)
-            cf = time_graph(torch, c1, stream, flush)
+            cf = time_graph_flushed(torch, cud_layers[li], stream, flush)
             cw = time_graph(torch, c10, stream, None, per=10)
             rec.update({"cudnn_us": cf, "cudnn_warm_us": cw, "cudnn_tflops": lay.useful_flops / (cf * 1e-6) / 1e12,
                         "speedup_vs_cudnn": cf / ours_f, "speedup_vs_cudnn_warm": cw / ours_w})
         recs.append(rec)
     step = {}
-    g = _graph(torch, lambda s: wl.step(s), stream)
-    step["ours_us"] = time_graph(torch, g, stream, flush)
+    step["ours_us"] = time_graph_flushed(torch, lambda s: wl.step(s), stream, flush)
     step["ours_tflops"] = wl.flops / (step["ours_us"] * 1e-6) / 1e12
     if cud_step is not None:
-        gc = _graph(torch, cud_step, stream)
-        step["cudnn_us"] = time_graph(torch, gc, stream, flush)
+        step["cudnn_us"] = time_graph_flushed(torch, cud_step, stream, flush)
         step["cudnn_tflops"] = wl.flops / (step["cudnn_us"] * 1e-6) / 1e12
         step["speedup_vs_cudnn"] = step["cudnn_us"] / step["ours_us"]
     elif with_cudnn:

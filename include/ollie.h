@@ -201,6 +201,15 @@ ollie_status ollie_plan_describe(const ollie_conv_shape *shape, ollie_dtype dtyp
 ollie_status ollie_autotune_derived(const ollie_conv_shape *shape, ollie_dtype dtype, int transposed,
                                     const void *x_nhwc, const void *w_prep, void *y_nhwc, void *ws,
                                     size_t ws_bytes, ollie_stream_t stream, float *best_us);
+/* Same, measuring every candidate from an evicted L2: flush_buf (caller-owned device memory, >= 2x
+ * the L2 size for a full eviction) is rewritten by cudaMemsetAsync before each timed launch, and each
+ * candidate's time is the mean of 5 such single launches.  For workloads whose layers start cold (a
+ * flushed benchmark step; weights evicted by the rest of a network).  flush_buf NULL / flush_bytes 0:
+ * OLLIE_E_INVALID. */
+ollie_status ollie_autotune_derived_cold(const ollie_conv_shape *shape, ollie_dtype dtype, int transposed,
+                                         const void *x_nhwc, const void *w_prep, void *y_nhwc, void *ws,
+                                         size_t ws_bytes, void *flush_buf, size_t flush_bytes,
+                                         ollie_stream_t stream, float *best_us);
 
 /* a2 standalone (the merged Matmul of P:1342-1352 on tcgen05 tensor cores):
  *   T[m][n] = sum_k A[m][k] * B[n][k]      A [M][K], B [N][K] in `dtype` (BF16 / TF32),

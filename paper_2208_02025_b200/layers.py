@@ -3,11 +3,29 @@ and the unfused-plan workspace; calling one runs the derived program on the GPU.
 Device memory comes from torch; every computation is a libollie kernel."""
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import ollie as _o
 
 _DT = {"bf16": _o.BF16, "tf32": _o.TF32}
+
+# Plans are tuned with back-to-back bursts (warm L2, the PDL overlap of a chain of layers included);
+# OLLIE_TUNE_COLD=1 times every candidate from an evicted L2 instead (ollie_autotune_derived_cold).
+# Measured on the bench's flushed steps (r02): cold tuning changed a few small-layer plans and made
+# the ResNet-18 / DCGAN steps 2-4% slower, so warm stays the default.
+_TUNE_COLD = os.environ.get("OLLIE_TUNE_COLD", "0") == "1"
+_FLUSH = {}
+
+
+def _flush_buffer(device):
+    """A device buffer of 2x the L2 size, allocated once per device (autotune's L2 eviction)."""
+    key = torch.device(device).index or 0
+    if key not in _FLUSH:
+        l2 = torch.cuda.get_device_properties(key).L2_cache_size
+        _FLUSH[key] = torch.empty(max(2 * l2, 64 << 20), dtype=torch.uint8, device=device)
+    return _FLUSH[key]
 _TORCH = {"bf16": torch.bfloat16, "tf32": torch.float32}
 
 
@@ -79,8 +97,12 @@ class DerivedConv:
             if not torch.cuda.is_current_stream_capturing():
                 # candidates write a scratch output: y may alias the residual (in-place epilogue)
                 scratch = self.new_output()
-                _o.autotune_derived(self.shape, self.code, self.transposed, x, self.w_prep, scratch,
-                                    self.ws, self.ws_bytes, stream)
+                if _TUNE_COLD:
+                    _o.autotune_derived_cold(self.shape, self.code, self.transposed, x, self.w_prep, scratch,
+                                             _flush_buffer(self.device), self.ws, self.ws_bytes, stream)
+                else:
+                    _o.autotune_derived(self.shape, self.code, self.transposed, x, self.w_prep, scratch,
+                                        self.ws, self.ws_bytes, stream)
                 # the last candidate launch still writes `scratch` on `stream`: finish it before the
                 # caching allocator may hand the block to other work (one-time cost per layer)
                 torch.cuda.synchronize(self.device)

@@ -101,6 +101,8 @@ _sig = {
     "ollie_plan_describe": (c_int, [_P(ConvShape), c_int, c_int, c_int, c_char_p, c_size_t]),
     "ollie_autotune_derived": (c_int, [_P(ConvShape), c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
                                        c_size_t, c_void_p, _P(c_float)]),
+    "ollie_autotune_derived_cold": (c_int, [_P(ConvShape), c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+                                            c_size_t, c_void_p, c_size_t, c_void_p, _P(c_float)]),
     "ollie_merged_gemm": (c_int, [c_int64, c_int64, c_int64, c_int, c_void_p, c_void_p, c_void_p, c_int64,
                                   c_void_p]),
     "ollie_offset_add": (c_int, [_P(ConvShape), c_int, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
@@ -238,6 +240,17 @@ def autotune_derived(shape: ConvShape, dtype: int, transposed: bool, x, w_prep, 
     _check(_lib.ollie_autotune_derived(ctypes.byref(shape), dtype, int(transposed), _ptr(x), _ptr(w_prep), _ptr(y),
                                        _ptr(ws), ws_bytes, _stream(stream), ctypes.byref(best)),
            "ollie_autotune_derived")
+    return best.value
+
+
+def autotune_derived_cold(shape: ConvShape, dtype: int, transposed: bool, x, w_prep, y, flush, ws=None,
+                          ws_bytes: int = 0, stream=None) -> float:
+    """Same, every candidate timed from an evicted L2 (`flush`: a device buffer >= 2x the L2 size)."""
+    best = c_float(0.0)
+    _check(_lib.ollie_autotune_derived_cold(ctypes.byref(shape), dtype, int(transposed), _ptr(x), _ptr(w_prep),
+                                            _ptr(y), _ptr(ws), ws_bytes, _ptr(flush), flush.numel() * flush.element_size(),
+                                            _stream(stream), ctypes.byref(best)),
+           "ollie_autotune_derived_cold")
     return best.value
 
 
