@@ -332,6 +332,9 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
                         if (++ti == nt) ti = 0;
                     }
                     tmem_ld_wait();
+                    // the row's last TMEM reads are done: hand the slots back before the stores (this
+                    // group's next row, y + 2, reads rows >= rb + 2), shortening the MMA <-> epilogue chain
+                    if (h == mtr - 1) release_upto(rb + 1);
                     float out[kFp];
 #pragma unroll
                     for (int f = 0; f < kFp; ++f) out[f] = 0.f;
@@ -408,7 +411,6 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
                     const int64_t kr = (int64_t)(y - s.ylo) + (g - g0);
                     if (kr < 64) a.trace[192 + kr] = rs_gtimer();
                 }
-                release_upto(rb + 1);                    // this group's next row (y + 2) reads rows >= rb + 2
             }
             release_upto(s.rhi - 1);
             seq0 += (uint32_t)(s.rhi - s.rlo);

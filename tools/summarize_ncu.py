@@ -14,7 +14,7 @@ from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
-PROF = os.path.join(ROOT, "profiles")
+PROF = os.environ.get("PROF_DIR", os.path.join(ROOT, "profiles"))
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
 cfgs = sys.argv[2:] or ["resnet18", "csrnet", "fsrcnn"]
 
