@@ -255,19 +255,6 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             // arms with the bytes of both; each CTA waits on its own empty barriers (the leader's
             // MMA commit multicasts to both)
             const uint32_t xmul = kPair ? 2u : 1u;
-            if (cid < a.num_items) {
-                // weights are read-only: warm L2 with this CTA's first tiles while the previous
-                // layer (which produces X) may still be running, then wait for it
-                const TileCoord tc0 = fc_work<kPair>(a, cid, rank);
-                const int nent = a.resident ? a.nclass * a.nph : a.nph;
-                const int ebase = a.resident ? 0 : tc0.cls * a.nph;
-                for (int kc = 0; kc < (a.resident ? a.kchunks : 1); ++kc)
-                    for (int e = 0; e < nent; ++e) {
-                        const FusedClass &en = a.cls[ebase + e];
-                        for (int g = 0; g < en.ngroups; ++g)
-                            tma_prefetch_4d(&tmW, kc * (128 / ES), tc0.f0 + rank * fhalf, en.wj0, en.wi0 + g * a.grb * a.westr);
-                    }
-            }
             // Weights are read-only for the whole stream (the weight DLT never triggers its dependents
             // early, ollie.h), so their smem loads go out BEFORE griddepcontrol.wait and overlap the
             // previous kernel's tail: the resident slice, or the first step's weight boxes.
