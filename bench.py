@@ -568,8 +568,15 @@ def gpu_main(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        # OLLIE_BENCH_BACKEND=gloo (ranks sharing the visible GPUs round-robin) exercises the N > 1 path
+        # on a single-GPU box; the driver's multi-GPU runs use NCCL, one GPU per rank
+        backend = os.environ.get("OLLIE_BENCH_BACKEND", "nccl")
+        local = local % max(1, torch.cuda.device_count()) if backend == "gloo" else local
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -824,8 +831,13 @@ def allgather_records(torch, dist, wl, cfg, dev, plan, stream, flush, graph, arg
 
         res["chunks"] = chunks
         res["overlapped_ms"] = timed(overlapped, max(3, min(args.steps, 10)))
-        # the overlapped result equals the serial one (same images, same kernels, same order)
-        res["overlapped_equals_serial"] = all(bool(torch.equal(a, b)) for a, b in zip(ylf, y_full))
+        # the overlapped (micro-batched) result against the serial one: the same images, but the chunk
+        # batch may autotune to another tile plan (another fp32 summation order), so compare within the
+        # bf16 bar rather than bit for bit (tests/test_gpu_multiproc.py checks bit equality in integer mode)
+        diff = max(float((a.float() - b.float()).abs().max()) / max(float(b.float().abs().max()), 1e-30)
+                   for a, b in zip(ylf, y_full))
+        res["overlapped_vs_serial_max_rel"] = diff
+        res["overlapped_matches_serial"] = diff <= 1e-2
     flops = sum(l.useful_flops for l in wl.layers_full)
     for k in ("serial_ms", "overlapped_ms"):
         if k in res:
