@@ -101,9 +101,17 @@ typedef struct {
  *               ConvTranspose2d stride, c*sizeof(elem) <= 128, w <= 512, f <= 64 and
  *               r' * stride^2 * f <= 64 with stride^2 * f in {4, 8, 12, 16} (r', s' <= 16 the
  *               stride-1 program's kernel, its column padding <= 8); else OLLIE_E_UNSUPPORTED.
- *               No workspace. */
+ *               No workspace.  This is the "ysum" form (OLLIE_PLAN_ROWSTREAM_YSUM).
+ *               The "direct" form (OLLIE_PLAN_ROWSTREAM_DIRECT, Conv2d only) puts only the f
+ *               output channels on N and every one of the r*s taps on an A-row shift over the r
+ *               input rows resident in shared memory: one TMEM accumulator per OUTPUT row, no
+ *               epilogue sum (the OffsetAdd of all r*s offsets done by the tensor core,
+ *               P:992-996 applied to both tap dimensions).  Plannable for Conv2d stride 1,
+ *               dilation 1, f <= 64, s <= 9, the same channel / width limits.
+ *               OLLIE_PLAN_ROWSTREAM runs the planner's form: direct when r*s*ceil(c*es/32)
+ *               <= 12 MMAs per M-tile, else ysum (else direct). */
 enum { OLLIE_PLAN_AUTO = 0, OLLIE_PLAN_FUSED = 1, OLLIE_PLAN_UNFUSED = 2, OLLIE_PLAN_GEMM_RED = 3,
-       OLLIE_PLAN_ROWSTREAM = 4 };
+       OLLIE_PLAN_ROWSTREAM = 4, OLLIE_PLAN_ROWSTREAM_YSUM = 5, OLLIE_PLAN_ROWSTREAM_DIRECT = 6 };
 
 /* ---------------------------------------------------------------------------------
  * Versioning and errors

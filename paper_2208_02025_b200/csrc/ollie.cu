@@ -744,7 +744,7 @@ struct PlanEntry {
     std::vector<FusedArgs> cands;   // autotune candidates (cands[0] = model's best)
     double fused_cost, unfused_cost;
     int tuned;                      // 0: model decides; 1: autotuned fused; 2: autotuned unfused; 3: GEMM_RED;
-                                    // 4: row-streaming
+                                    // 5 / 6: row-streaming ysum / direct (OLLIE_PLAN_ROWSTREAM_*)
 };
 static std::mutex g_plan_mu;
 static std::map<PlanKey, PlanEntry> g_plan_cache;
@@ -988,8 +988,35 @@ static ollie_status run_fused(const ollie_conv_shape *s, bool tf32, int transpos
 // the MMA's N, kernel rows as A-row shifts, the column OffsetAdd in the epilogue.  Plannable when
 // the layer is (or rewrites to) a stride-1 program with s' * sigma^2 * f <= 64 columns per kernel
 // row, one <= 128-byte channel chunk, and image rows of <= 512 pixels.
-static bool plan_rowstream(const ollie_conv_shape *s, bool tf32, int transposed, int64_t OH, int64_t OW, RsArgs *out) {
+// Two forms share the kernel: "ysum" (kernel rows on N, the row OffsetAdd in the epilogue) and
+// "direct" (N = f, all r*s taps as A-row shifts over the r resident input rows, one accumulator per
+// OUTPUT row: no epilogue sum and no MMA <-> epilogue lockstep across rows).  mode: 0 ysum,
+// 1 direct, -1 the planner's choice (direct for Conv2d when it needs <= 12 MMAs per M-tile, i.e.
+// r*s*ksteps <= 12, else ysum; OLLIE_RS_MODE=0/1 forces one for ablations).
+static bool plan_rowstream_mode(const ollie_conv_shape *s, bool tf32, int transposed, int64_t OH, int64_t OW, int mode,
+                                RsArgs *out);
+static bool plan_rowstream(const ollie_conv_shape *s, bool tf32, int transposed, int64_t OH, int64_t OW, RsArgs *out,
+                           int mode = -1) {
+    if (mode == 0 || mode == 1) return plan_rowstream_mode(s, tf32, transposed, OH, OW, mode, out);
+    static int forced = -2;
+    if (forced == -2) {
+        const char *e = getenv("OLLIE_RS_MODE");
+        forced = e ? atoi(e) : -1;
+    }
+    if (forced == 0 || forced == 1) return plan_rowstream_mode(s, tf32, transposed, OH, OW, forced, out);
+    RsArgs d;
+    if (plan_rowstream_mode(s, tf32, transposed, OH, OW, 1, &d) && d.R * d.S * d.ksteps <= 12) {
+        *out = d;
+        return true;
+    }
+    if (plan_rowstream_mode(s, tf32, transposed, OH, OW, 0, out)) return true;
+    if (plan_rowstream_mode(s, tf32, transposed, OH, OW, 1, &d)) { *out = d; return true; }
+    return false;
+}
+static bool plan_rowstream_mode(const ollie_conv_shape *s, bool tf32, int transposed, int64_t OH, int64_t OW, int mode,
+                                RsArgs *out) {
     const int es = tf32 ? 4 : 2;
+    if (mode == 1 && transposed) return false;        // direct form: Conv2d only
     if (s->dilation != 1) return false;
     if (!transposed && s->stride != 1) return false;
     if ((s->c * es) % 16 != 0 || s->c * es > 128) return false;
@@ -1026,8 +1053,13 @@ static bool plan_rowstream(const ollie_conv_shape *s, bool tf32, int transposed,
         a.OHc = (int)ceil_div(OH, st); a.OWc = (int)ceil_div(OW, st);
     }
     a.Fp = a.sub * a.sub * a.F;
-    if (a.Fp != 4 && a.Fp != 8 && a.Fp != 12 && a.Fp != 16) return false;   // kernel variants
-    a.N = a.R * a.Fp;                                                         // kernel rows x f' on N
+    if (mode == 1) {
+        a.direct = 1;
+        a.N = a.F;                                                            // output channels on N
+    } else {
+        if (a.Fp != 4 && a.Fp != 8 && a.Fp != 12 && a.Fp != 16) return false;   // kernel variants
+        a.N = a.R * a.Fp;                                                     // kernel rows x f' on N
+    }
     if (a.N > RS_MAX_NP || a.S > RS_MAX_S || a.pad_y < 0) return false;
     // column shifts read the zero pixel rows kept on both sides of a slot
     if (a.pad_x < 0 || a.pad_x > RS_ZR || a.S - 1 - a.pad_x > RS_ZR) return false;
@@ -1048,11 +1080,12 @@ static bool plan_rowstream(const ollie_conv_shape *s, bool tf32, int transposed,
     a.tmem_cols = 512;
     a.row_cols = a.mtr * a.acc_cols;
     a.nt = std::min(16, 512 / a.row_cols);
-    if (a.nt < a.R + 1) return false;                 // the r-row window plus one row of look-ahead
+    // ysum: the r-row window plus one row of look-ahead in TMEM; direct: two output rows in flight
+    if (a.nt < (a.direct ? 2 : a.R + 1)) return false;
     a.ring = 0;
     const int fixed = (int)rs_smem_bytes(a) + 8 * 2 * 16;
     a.ring = std::min(16, (227 * 1024 - fixed) / a.slot_bytes);
-    if (a.ring < 2) return false;
+    if (a.ring < (a.direct ? a.R + 1 : 2)) return false;   // direct: the r-row window stays resident
     if (rs_smem_bytes(a) > (size_t)227 * 1024) return false;
     *out = a;
     return true;
@@ -1060,14 +1093,21 @@ static bool plan_rowstream(const ollie_conv_shape *s, bool tf32, int transposed,
 static int rowstream_grid(const RsArgs &a) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(a.rows_total, (int64_t)num_sms()));
 }
-static bool rowstream_supported(const ollie_conv_shape *s, bool tf32, int transposed, int64_t OH, int64_t OW) {
+static bool rowstream_supported(const ollie_conv_shape *s, bool tf32, int transposed, int64_t OH, int64_t OW,
+                                int mode = -1) {
     RsArgs a;
-    return plan_rowstream(s, tf32, transposed, OH, OW, &a);
+    return plan_rowstream(s, tf32, transposed, OH, OW, &a, mode);
+}
+static bool is_rowstream_plan(int p) {
+    return p == OLLIE_PLAN_ROWSTREAM || p == OLLIE_PLAN_ROWSTREAM_YSUM || p == OLLIE_PLAN_ROWSTREAM_DIRECT;
+}
+static int rowstream_mode_of(int p) {
+    return p == OLLIE_PLAN_ROWSTREAM_YSUM ? 0 : (p == OLLIE_PLAN_ROWSTREAM_DIRECT ? 1 : -1);
 }
 
-template <bool TF32, int FP>
+template <bool TF32, int FP, bool DIRECT = false>
 static ollie_status launch_rowstream_t(const CUtensorMap &tx, const RsArgs &a, cudaStream_t stream) {
-    auto kern = rowstream_conv_kernel<TF32, FP>;
+    auto kern = rowstream_conv_kernel<TF32, FP, DIRECT>;
     static bool attr_done[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1080,9 +1120,10 @@ static ollie_status launch_rowstream_t(const CUtensorMap &tx, const RsArgs &a, c
 }
 
 static ollie_status run_rowstream(const ollie_conv_shape *s, bool tf32, int transposed, const void *x, const void *wp,
-                                  void *y, int64_t OH, int64_t OW, cudaStream_t stream, const EpiArgs *epi = nullptr) {
+                                  void *y, int64_t OH, int64_t OW, cudaStream_t stream, const EpiArgs *epi = nullptr,
+                                  int mode = -1) {
     RsArgs a;
-    if (!plan_rowstream(s, tf32, transposed, OH, OW, &a)) return fail(OLLIE_E_UNSUPPORTED, "no row-streaming plan for this shape");
+    if (!plan_rowstream(s, tf32, transposed, OH, OW, &a, mode)) return fail(OLLIE_E_UNSUPPORTED, "no row-streaming plan for this shape");
     a.wprep = wp;
     a.y = y;
     a.epi = epi ? *epi : EpiArgs{};
@@ -1111,6 +1152,7 @@ static ollie_status run_rowstream(const ollie_conv_shape *s, bool tf32, int tran
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled (row stream) failed (%d)", (int)r);
     }
+    if (a.direct) return tf32 ? launch_rowstream_t<true, 16, true>(tx, a, stream) : launch_rowstream_t<false, 16, true>(tx, a, stream);
     switch (a.Fp) {
         case 4: return tf32 ? launch_rowstream_t<true, 4>(tx, a, stream) : launch_rowstream_t<false, 4>(tx, a, stream);
         case 8: return tf32 ? launch_rowstream_t<true, 8>(tx, a, stream) : launch_rowstream_t<false, 8>(tx, a, stream);
@@ -1301,13 +1343,12 @@ static bool is_identity_offset_add(const ollie_conv_shape *s, int transposed) {
 static int tuned_choice(const ollie_conv_shape *s, bool tf32, int transposed);   // autotune result (0 none)
 
 static int resolve_plan(const ollie_conv_shape *s, ollie_dtype dtype, int plan, int transposed) {
-    if (plan == OLLIE_PLAN_FUSED || plan == OLLIE_PLAN_UNFUSED || plan == OLLIE_PLAN_GEMM_RED ||
-        plan == OLLIE_PLAN_ROWSTREAM)
+    if (plan == OLLIE_PLAN_FUSED || plan == OLLIE_PLAN_UNFUSED || plan == OLLIE_PLAN_GEMM_RED || is_rowstream_plan(plan))
         return plan;
     const bool tf32 = dtype == OLLIE_TF32;
     const int tc = tuned_choice(s, tf32, transposed);
     if (tc == 3) return OLLIE_PLAN_GEMM_RED;
-    if (tc == 4) return OLLIE_PLAN_ROWSTREAM;
+    if (is_rowstream_plan(tc)) return tc;
     if (is_identity_offset_add(s, transposed)) return tc == 1 ? OLLIE_PLAN_FUSED : OLLIE_PLAN_UNFUSED;
     if (tc == 0 && s->w >= 96) {   // untuned: narrow layers over wide rows stream rows (>= 75% of the lanes busy)
         int64_t OH, OW;
@@ -1394,8 +1435,8 @@ static ollie_status derived_layer(const ollie_conv_shape *s, ollie_dtype dtype, 
                                                       : (size_t)M * (size_t)ldT_of(s) * sizeof(float);
         if ((!ws || ws_bytes < need) && fused_supported(s, tf32, transposed)) rp = OLLIE_PLAN_FUSED;
     }
-    if (rp == OLLIE_PLAN_ROWSTREAM) {
-        st = run_rowstream(s, tf32, transposed, x, wp, y, OH, OW, stream, &epi);
+    if (is_rowstream_plan(rp)) {
+        st = run_rowstream(s, tf32, transposed, x, wp, y, OH, OW, stream, &epi, rowstream_mode_of(rp));
         return st == OLLIE_OK ? ok() : st;
     }
     if (rp == OLLIE_PLAN_FUSED) {
@@ -1992,12 +2033,12 @@ extern "C" ollie_status ollie_plan_describe(const ollie_conv_shape *s, ollie_dty
                  a.XB, a.Yb, a.Xb, a.Yp, a.MT, a.FS, a.f_slices, a.resident, a.nbuf, a.na, a.nb, a.BK, a.kchunks,
                  a.num_tiles, fused_grid(a), fused_smem_bytes(a), a.nclass, a.nph, a.ist, a.max_taps, a.sw128,
                  a.tmem_cols == 256 ? 2 : 1, a.pair, a.grb, a.nsb, a.ksplit, a.ipt, a.tma_y, a.grp8);
-    } else if (rp == OLLIE_PLAN_ROWSTREAM) {
+    } else if (is_rowstream_plan(rp)) {
         RsArgs a;
-        if (!plan_rowstream(s, tf32, transposed, OH, OW, &a)) return fail(OLLIE_E_UNSUPPORTED, "no row-streaming plan");
+        if (!plan_rowstream(s, tf32, transposed, OH, OW, &a, rowstream_mode_of(rp))) return fail(OLLIE_E_UNSUPPORTED, "no row-streaming plan");
         snprintf(buf, len,
-                 "rowstream R=%d S=%d sub=%d N=%d NP=%d ring=%d mtr=%d rowbytes=%d ksteps=%d tmem_rows=%d grid=%d smem=%zu",
-                 a.R, a.S, a.sub, a.N, a.NP, a.ring, a.mtr, a.rowbytes, a.ksteps, a.nt, rowstream_grid(a), rs_smem_bytes(a));
+                 "rowstream %s R=%d S=%d sub=%d N=%d NP=%d ring=%d mtr=%d rowbytes=%d ksteps=%d tmem_rows=%d grid=%d smem=%zu",
+                 a.direct ? "direct" : "ysum", a.R, a.S, a.sub, a.N, a.NP, a.ring, a.mtr, a.rowbytes, a.ksteps, a.nt, rowstream_grid(a), rs_smem_bytes(a));
     } else if (rp == OLLIE_PLAN_GEMM_RED) {
         snprintf(buf, len, "gemm_red BN=%d (%s as fp32 L2 reductions in the GEMM epilogue) + finish",
                  gemm_bn(s->n * s->h * s->w, s->r * s->s * s->f), transposed ? "selective add" : "OffsetAdd");
@@ -2091,7 +2132,8 @@ static ollie_status autotune_impl(const ollie_conv_shape *s, ollie_dtype dtype, 
                 if (d[0] == 'f' && idx >= 0 && idx < (int)cands.size()) { e->args = cands[idx]; e->tuned = 1; hit = true; }
                 else if (d[0] == 'u' && unfused_ok) { e->tuned = 2; hit = true; }
                 else if (d[0] == 'r') { e->tuned = 3; hit = true; }
-                else if (d[0] == 's' && rowstream_supported(s, tf32, transposed, OH, OW)) { e->tuned = 4; hit = true; }
+                else if (d[0] == 's' && rowstream_supported(s, tf32, transposed, OH, OW, 0)) { e->tuned = OLLIE_PLAN_ROWSTREAM_YSUM; hit = true; }
+                else if (d[0] == 'd' && rowstream_supported(s, tf32, transposed, OH, OW, 1)) { e->tuned = OLLIE_PLAN_ROWSTREAM_DIRECT; hit = true; }
             }
             fclose(fp);
             if (hit) {
@@ -2164,30 +2206,35 @@ static ollie_status autotune_impl(const ollie_conv_shape *s, ollie_dtype dtype, 
     const bool red_ok = red_supported(s, transposed) && ws && ws_bytes >= red_acc_bytes(s, OH, OW) && aligned16(ws);
     if (red_ok)
         t_red = time_it([&] { return run_gemm_red(s, transposed, tf32, x, wp, (float *)ws, y, OH, OW, stream, nullptr); });
-    float t_rs = 1e30f;
-    if (rowstream_supported(s, tf32, transposed, OH, OW))
-        t_rs = time_it([&] { return run_rowstream(s, tf32, transposed, x, wp, y, OH, OW, stream); });
+    float t_rs = 1e30f, t_rd = 1e30f;     // the two row-streaming forms (ysum, direct)
+    if (rowstream_supported(s, tf32, transposed, OH, OW, 0))
+        t_rs = time_it([&] { return run_rowstream(s, tf32, transposed, x, wp, y, OH, OW, stream, nullptr, 0); });
+    if (rowstream_supported(s, tf32, transposed, OH, OW, 1))
+        t_rd = time_it([&] { return run_rowstream(s, tf32, transposed, x, wp, y, OH, OW, stream, nullptr, 1); });
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    const bool any_timed = best < 1e29f || t_unf < 1e29f || t_red < 1e29f || t_rs < 1e29f;
+    const bool any_timed = best < 1e29f || t_unf < 1e29f || t_red < 1e29f || t_rs < 1e29f || t_rd < 1e29f;
     {
         std::lock_guard<std::mutex> g(g_plan_mu);
         if (!cands.empty()) e->args = cands[best_k >= 0 ? best_k : 0];
         // record a decision only when some plan actually ran and was timed: a failed tuning leaves
         // AUTO to the cost model instead of pinning it to an unmeasured plan
         if (any_timed) {
-            const float t_min = std::min(std::min(best, t_unf), std::min(t_red, t_rs));
-            if (t_rs == t_min) e->tuned = 4;
+            const float t_min = std::min(std::min(std::min(best, t_unf), std::min(t_red, t_rs)), t_rd);
+            if (t_rd == t_min) e->tuned = OLLIE_PLAN_ROWSTREAM_DIRECT;
+            else if (t_rs == t_min) e->tuned = OLLIE_PLAN_ROWSTREAM_YSUM;
             else if (t_red == t_min) e->tuned = 3;
             else e->tuned = (t_unf == t_min || best_k < 0) ? 2 : 1;
         }
     }
-    if (best_us) *best_us = 1e3f * std::min(std::min(best, t_unf), std::min(t_red, t_rs));
+    if (best_us) *best_us = 1e3f * std::min(std::min(std::min(best, t_unf), std::min(t_red, t_rs)), t_rd);
     if (!any_timed) return fail(OLLIE_E_UNSUPPORTED, "no runnable plan to tune");
     if (tune_file) {
         if (FILE *fp = fopen(tune_file, "a")) {
             const int t = e->tuned;
-            fprintf(fp, "%s %s %d\n", key, t == 1 ? "f" : t == 2 ? "u" : t == 3 ? "r" : "s", t == 1 ? best_k : 0);
+            fprintf(fp, "%s %s %d\n", key,
+                    t == 1 ? "f" : t == 2 ? "u" : t == 3 ? "r" : t == OLLIE_PLAN_ROWSTREAM_DIRECT ? "d" : "s",
+                    t == 1 ? best_k : 0);
             fclose(fp);
         }
     }

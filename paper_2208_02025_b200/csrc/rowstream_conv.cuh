@@ -38,6 +38,8 @@
 #include "sm100_ptx.cuh"
 #include "epilogue.cuh"
 
+#include <type_traits>
+
 namespace ollie {
 
 constexpr int RS_THREADS = 384;       // warps 0-3: TMA, MMA, TMEM, idle; 4-11: two epilogue groups
@@ -51,6 +53,7 @@ struct RsArgs {
     int32_t R, S, pad_y, pad_x;        // the stride-1 program: output row y reads input rows y - pad_y + i
     int32_t sub;                       // sigma of a ConvTranspose2d in sub-pixel form (1 for Conv2d)
     int32_t tr;                        // 1: ConvTranspose2d (weights re-indexed by class), 0: Conv2d
+    int32_t direct;                    // 1: direct form (N = f, every tap an A shift, one accumulator per OUTPUT row)
     int32_t OHc, OWc;                  // output grid of the stride-1 program (class grid for sub > 1)
     int32_t OH, OW;                    // the layer's output (clipping of the interleaved classes)
     int32_t Fp, N, NP, acc_cols;       // Fp = sub^2 * F columns per kernel row; N = R * Fp -> NP (mult. of 16)
@@ -68,7 +71,7 @@ struct RsArgs {
 };
 
 // shared-memory carve-up (host and device agree): ring | B tiles (one per kernel column) | barriers
-__host__ __device__ inline int rs_b_bytes(const RsArgs &a) { return a.S * a.NP * a.rowbytes; }
+__host__ __device__ inline int rs_b_bytes(const RsArgs &a) { return (a.direct ? a.R * a.S : a.S) * a.NP * a.rowbytes; }
 __host__ __device__ inline int rs_bar_bytes(const RsArgs &a) { return 8 * (2 * a.ring + 2 * a.nt) + 16; }
 __host__ __device__ inline size_t rs_smem_bytes(const RsArgs &a) {
     return 1024 + (size_t)a.ring * a.slot_bytes + rs_b_bytes(a) + rs_bar_bytes(a);
@@ -102,6 +105,33 @@ __device__ __forceinline__ void rs_store1(void *y, int64_t e, float v) {
     else reinterpret_cast<uint16_t *>(y)[e] = float_to_bf16_rne(v);
 }
 
+// Y[e0 .. e0 + kN) = v[0 .. kN) for one pixel (kN compile-time, the pixel's kN * ES bytes are
+// aligned to their size's largest power-of-two divisor): the widest vector stores that alignment
+// allows (16 / 8 / 4 bytes) -- a 12-channel bf16 pixel leaves as three 8-byte stores, not twelve
+// 2-byte ones (the LSU cost of the narrow-f epilogues is per store instruction).
+template <bool kTF32, int kN>
+__device__ __forceinline__ void rs_store_pixel(void *y, int64_t e0, const float *v) {
+    constexpr int ES = kTF32 ? 4 : 2, B = kN * ES;
+    constexpr int VB = (B % 16 == 0) ? 16 : (B % 8 == 0) ? 8 : (B % 4 == 0) ? 4 : ES;
+    constexpr int VE = VB / ES;                          // elements per store
+    uint8_t *base = reinterpret_cast<uint8_t *>(y) + e0 * ES;
+#pragma unroll
+    for (int f = 0; f < kN; f += VE) {
+        uint32_t w[4];
+        if constexpr (kTF32) {
+#pragma unroll
+            for (int u = 0; u < VE; ++u) w[u] = __float_as_uint(v[f + u]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < VE / 2; ++u) w[u] = pack_bf16x2_rn(v[f + 2 * u], v[f + 2 * u + 1]);
+        }
+        if constexpr (VB == 16) *reinterpret_cast<uint4 *>(base + f * ES) = make_uint4(w[0], w[1], w[2], w[3]);
+        else if constexpr (VB == 8) *reinterpret_cast<uint2 *>(base + f * ES) = make_uint2(w[0], w[1]);
+        else if constexpr (VB == 4) *reinterpret_cast<uint32_t *>(base + f * ES) = w[0];
+        else rs_store1<kTF32>(y, e0 + f, v[f]);
+    }
+}
+
 // tcgen05.ld of kFp consecutive fp32 columns (kFp in {4, 8, 12, 16}) into v[0, kFp)
 template <int kFp>
 __device__ __forceinline__ void rs_tmem_ld(uint32_t taddr, uint32_t *v) {
@@ -119,7 +149,65 @@ __device__ __forceinline__ void rs_tmem_ld(uint32_t taddr, uint32_t *v) {
     }
 }
 
-template <bool kTF32, int kFp>
+// MMAs of one M-tile of one input row: kS column shifts x kKS k-steps, D (+)= shift_j(A) W'_j.
+// Called by the converged MMA warp; one elected lane issues each MMA (umma_elect_lohi) with the
+// warp-uniform descriptor words plus compile-time offsets.  The shift / k-step counts are template
+// parameters: the same walk with runtime bounds (the _rt fallback) puts a data-dependent branch
+// before every MMA, and ptxas then re-converges the warp around each one -- measured on B200 at
+// ~205 cycles per MMA against ~25-65 for the straight-line form (tools/mma_rate.cu: the tensor
+// core itself takes ~40 cycles per 128 x 16 x 16 MMA, its (128 + N) x 32-byte SMEM operand read).
+template <bool kTF32, int kS, int kKS>
+__device__ __forceinline__ void rs_issue_shifts(uint32_t d, uint32_t alo, uint32_t blo, uint32_t hi, uint32_t a_step,
+                                                uint32_t b_step, uint32_t idesc, uint32_t acc0) {
+#pragma unroll
+    for (int j = 0; j < kS; ++j)
+#pragma unroll
+        for (int k = 0; k < kKS; ++k)
+            umma_elect_lohi<kTF32>(d, alo + (uint32_t)j * a_step + 2u * k, hi, blo + (uint32_t)j * b_step + 2u * k, hi, idesc,
+                                   (j == 0 && k == 0) ? acc0 : 1u);
+}
+template <bool kTF32>
+__device__ __forceinline__ void rs_issue_shifts_rt(uint32_t d, uint32_t alo, uint32_t blo, uint32_t hi, uint32_t a_step,
+                                                   uint32_t b_step, uint32_t idesc, uint32_t acc0, int S, int ksteps) {
+#pragma unroll
+    for (int j = 0; j < RS_MAX_S; ++j) {
+        if (j < S) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k < ksteps)
+                    umma_elect_lohi<kTF32>(d, alo + (uint32_t)j * a_step + 2u * k, hi, blo + (uint32_t)j * b_step + 2u * k,
+                                           hi, idesc, (j == 0 && k == 0) ? acc0 : 1u);
+        }
+    }
+}
+template <bool kTF32, int kS, int kKS>
+__device__ __forceinline__ void rs_issue(uint32_t d, uint32_t alo, uint32_t blo, uint32_t hi, uint32_t a_step,
+                                         uint32_t b_step, uint32_t idesc, uint32_t acc0, int S, int ksteps) {
+    if constexpr (kS > 0) rs_issue_shifts<kTF32, kS, kKS>(d, alo, blo, hi, a_step, b_step, idesc, acc0);
+    else rs_issue_shifts_rt<kTF32>(d, alo, blo, hi, a_step, b_step, idesc, acc0, S, ksteps);
+}
+template <int v>
+using rs_ic = std::integral_constant<int, v>;
+// Runs body(rs_ic<S>, rs_ic<ksteps>) for the (S, ksteps) pairs the planner produces most (1x1, 3x3,
+// 5x5 programs; 1-4 channel chunks), else body(rs_ic<0>, rs_ic<0>) (runtime bounds).
+template <typename Body>
+__device__ __forceinline__ void rs_dispatch_shifts(int S, int ksteps, Body &&body) {
+    switch (S * 8 + ksteps) {
+        case 1 * 8 + 1: body(rs_ic<1>{}, rs_ic<1>{}); break;
+        case 1 * 8 + 2: body(rs_ic<1>{}, rs_ic<2>{}); break;
+        case 1 * 8 + 3: body(rs_ic<1>{}, rs_ic<3>{}); break;
+        case 1 * 8 + 4: body(rs_ic<1>{}, rs_ic<4>{}); break;
+        case 3 * 8 + 1: body(rs_ic<3>{}, rs_ic<1>{}); break;
+        case 3 * 8 + 2: body(rs_ic<3>{}, rs_ic<2>{}); break;
+        case 3 * 8 + 4: body(rs_ic<3>{}, rs_ic<4>{}); break;
+        case 5 * 8 + 1: body(rs_ic<5>{}, rs_ic<1>{}); break;
+        case 5 * 8 + 2: body(rs_ic<5>{}, rs_ic<2>{}); break;
+        case 5 * 8 + 4: body(rs_ic<5>{}, rs_ic<4>{}); break;
+        default: body(rs_ic<0>{}, rs_ic<0>{}); break;
+    }
+}
+
+template <bool kTF32, int kFp, bool kDirect>
 __global__ void __launch_bounds__(RS_THREADS, 1)
 rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ RsArgs a) {
     constexpr int ES = kTF32 ? 4 : 2;
@@ -142,7 +230,7 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
     if (warp == 0 && lane == 0) tma_prefetch_desc(&tmX);
     if (warp == 1 && lane == 0) {
         for (int i = 0; i < a.ring; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-        for (int i = 0; i < a.nt; ++i) { mbar_init(&afull[i], 1); mbar_init(&aempty[i], 8); }
+        for (int i = 0; i < a.nt; ++i) { mbar_init(&afull[i], 1); mbar_init(&aempty[i], kDirect ? 4 : 8); }
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -152,11 +240,16 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
         // stream, so this overlaps the previous kernel under PDL)
         const int cpr = a.rowbytes / 16, CI = 16 / ES;
         const uint32_t swmask = (uint32_t)cpr - 1;
-        const int total = a.S * a.NP * cpr;
+        const int total = (kDirect ? a.R * a.S : a.S) * a.NP * cpr;
         for (int t = threadIdx.x; t < total; t += RS_THREADS) {
             const int chunk = t % cpr, nrow = (t / cpr) % a.NP, j = t / (cpr * a.NP);
             uint4 v = make_uint4(0u, 0u, 0u, 0u);
-            if (nrow < a.N) {
+            if constexpr (kDirect) {             // tile i*S + j of tap (i, j): rows f < F
+                const int ti = j / a.S, tj = j - ti * a.S, c0 = chunk * CI;
+                if (nrow < a.F && c0 < a.C)
+                    v = __ldg(reinterpret_cast<const uint4 *>(reinterpret_cast<const uint8_t *>(a.wprep) +
+                                                              ((((int64_t)ti * a.S0 + tj) * a.F + nrow) * a.C + c0) * ES));
+            } else if (nrow < a.N) {
                 const int i = nrow / a.Fp, rem = nrow - i * a.Fp;
                 int ki, kj, f;
                 if (!a.tr) {
@@ -220,19 +313,177 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
                 g += s.yhi - s.ylo;
             }
         }
-    } else if (warp == 1) {
+    } else if (kDirect && warp == 1) {
+        // ===== direct form, MMA issuer: accumulator of OUTPUT row y = Sum_{i,j} shift_j(X_{y-p+i}) W'_{i,j} =====
+        const uint32_t idesc = make_idesc(kTF32, 128, (uint32_t)a.NP);
+        const uint64_t dtpl = ((uint64_t)1 << 16) | ((uint64_t)((8u * (uint32_t)a.rowbytes) >> 4) << 32) |
+                              ((uint64_t)1 << 46) | ((uint64_t)a.swz << 61);
+        const uint32_t row16 = (uint32_t)a.rowbytes >> 4, slot16 = (uint32_t)a.slot_bytes >> 4;
+        const uint32_t b16 = smem_u32(sB) >> 4, bt16 = (uint32_t)(a.NP * a.rowbytes) >> 4;
+        const uint32_t lo0 = (uint32_t)dtpl, hi = (uint32_t)(dtpl >> 32), blo = lo0 + b16;
+        const uint32_t ring_a16 = (smem_u32(sRing) >> 4) + (uint32_t)(RS_ZR - a.pad_x) * row16;
+        const uint32_t mt16 = 128u * row16, acc_cols = (uint32_t)a.acc_cols, row_cols = (uint32_t)a.row_cols;
+        const int ring = a.ring, nt = a.nt, ksteps = a.ksteps, S = a.S, R = a.R, mtr = a.mtr, pad_y = a.pad_y;
+        int t = 0;                                      // TMEM slot of the output row
+        uint32_t tph = 0;
+        int next_slot = 0;                              // ring slot of the next loaded row
+        int wslot = 0;                                  // full-wait cursor: next loaded row to wait for
+        uint32_t wph = 0, wseq = 0, seq0 = 0;
+        int rslot = 0;                                  // release cursor: next loaded row to hand back
+        uint32_t rseq = 0;
+        auto wait_upto = [&](uint32_t sq) {
+            while (wseq <= sq) {
+                mbar_wait_warp(&full[wslot], wph);
+                if (++wslot == ring) { wslot = 0; wph ^= 1u; }
+                ++wseq;
+            }
+        };
+        auto release_upto = [&](uint32_t sq_end) {     // rows with sequence < sq_end
+            while (rseq < sq_end) {
+                wait_upto(rseq);
+                umma_commit_elect(&empty[rslot]);       // retires with the MMAs that read the row
+                __syncwarp();
+                if (++rslot == ring) rslot = 0;
+                ++rseq;
+            }
+        };
+        rs_dispatch_shifts(S, ksteps, [&](auto Sc, auto KSc) {
+          constexpr int kS = decltype(Sc)::value, kKS = decltype(KSc)::value;
+          for (int64_t g = g0; g < g1;) {
+            const RsSeg s = rs_seg(a, g, g1);
+            const int slot0 = next_slot;
+            for (int y = s.ylo; y < s.yhi; ++y) {
+                const int rb = y - pad_y;
+                const int i_lo = max(0, s.rlo - rb), i_hi = min(R, s.rhi - rb);
+                if (i_hi > i_lo) wait_upto(seq0 + (uint32_t)(rb + i_hi - 1 - s.rlo));
+                mbar_wait_warp(&aempty[t], tph ^ 1u);
+                tc_fence_after();
+                const uint32_t d0 = tmem_base + (uint32_t)t * row_cols;
+                const int64_t kr = (int64_t)(y - s.ylo) + (g - g0);
+                if ((a.dbg & 8) && a.trace && blockIdx.x == 0 && kr == 5 && lane == 0) a.trace[319] = clock64();
+                if (a.trace && blockIdx.x == 0 && kr < 64 && lane == 0) a.trace[64 + kr] = rs_gtimer();
+                int sl = slot0 + (rb + i_lo - s.rlo);            // ring slot of input row rb + i_lo
+                while (sl >= ring) sl -= ring;
+                for (int i = i_lo; i < i_hi; ++i) {
+                    const uint32_t a0 = lo0 + ring_a16 + (uint32_t)sl * slot16;
+                    const uint32_t bi = blo + (uint32_t)(i * S) * bt16;
+                    for (int h = 0; h < mtr; ++h) {
+                        rs_issue<kTF32, kS, kKS>(d0 + (uint32_t)h * acc_cols, a0 + (uint32_t)h * mt16, bi, hi, row16, bt16,
+                                                 idesc, i == i_lo ? 0u : 1u, S, ksteps);
+                        if ((a.dbg & 8) && a.trace && blockIdx.x == 0 && kr == 5 && lane == 0)
+                            a.trace[320 + (i - i_lo) * mtr + h] = clock64();
+                    }
+                    if (++sl == ring) sl = 0;
+                }
+                __syncwarp();
+                umma_commit_elect(&afull[t]);           // (no valid tap: arrives at once; the epilogue writes 0)
+                __syncwarp();
+                if (a.trace && blockIdx.x == 0 && kr < 64 && lane == 0) a.trace[128 + kr] = rs_gtimer();
+                if (++t == nt) { t = 0; tph ^= 1u; }
+                if (rb >= s.rlo) release_upto(seq0 + (uint32_t)(rb - s.rlo + 1));   // no later output row reads rb
+            }
+            release_upto(seq0 + (uint32_t)(s.rhi - s.rlo));
+            seq0 += (uint32_t)(s.rhi - s.rlo);
+            next_slot = slot0 + (s.rhi - s.rlo);
+            while (next_slot >= ring) next_slot -= ring;
+            g += s.yhi - s.ylo;
+          }
+        });
+    } else if (kDirect && warp >= 4) {
+        // ===== direct form, epilogue: two groups on alternate output rows; one TMEM slot per output row =====
+        const int q = warp & 3;
+        const int gi = (warp - 4) >> 2;
+        pdl_wait();
+        const int nt = a.nt, R = a.R, mtr = a.mtr, pad_y = a.pad_y, OWc = a.OWc, F = a.F, NP = a.NP;
+        const uint32_t row_cols = (uint32_t)a.row_cols, acc_cols = (uint32_t)a.acc_cols;
+        const uint32_t lane0 = tmem_base + ((uint32_t)(q * 32) << 16);
+        const int xq = 32 * q + lane;
+        int t = 0;
+        uint32_t tph = 0, krow = 0;
+        uint32_t v[RS_MAX_NP];
+        for (int64_t g = g0; g < g1;) {
+            const RsSeg s = rs_seg(a, g, g1);
+            const int64_t img_el = (int64_t)s.img * a.OH;
+            for (int y = s.ylo; y < s.yhi; ++y, ++krow) {
+                const int tt = t;
+                const uint32_t ph = tph;
+                if (++t == nt) { t = 0; tph ^= 1u; }
+                if ((int)(krow & 1u) != gi) continue;
+                const int rb = y - pad_y;
+                const bool any = min(R, s.rhi - rb) > max(0, s.rlo - rb);
+                mbar_wait(&afull[tt], ph);
+                tc_fence_after();
+                if (a.dbg & 1) {                         // ablation: no TMEM reads, no stores
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&aempty[tt]);
+                    continue;
+                }
+                for (int h = 0; h < mtr; ++h) {
+                    const uint32_t tb = lane0 + (uint32_t)tt * row_cols + (uint32_t)h * acc_cols;
+#pragma unroll
+                    for (int c = 0; c < RS_MAX_NP; c += 16)
+                        if (c < NP) tmem_ld_32x32b_x16(tb + (uint32_t)c, *reinterpret_cast<uint32_t(*)[16]>(&v[c]));
+                    tmem_ld_wait();
+                    if (h == mtr - 1) {                  // the row's accumulator is read: hand the slot back
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&aempty[tt]);
+                    }
+                    const int x = 128 * h + xq;
+                    if (x >= OWc) continue;
+                    if (!any) {
+#pragma unroll
+                        for (int f = 0; f < RS_MAX_NP; ++f) v[f] = 0u;
+                    }
+                    float *out = reinterpret_cast<float *>(v);   // the accumulator values, in place
+                    const int64_t e0 = ((img_el + y) * a.OW + x) * F;
+                    if (a.epi.on) epi_apply<!kTF32, RS_MAX_NP>(a.epi, out, e0, 0, F);
+                    if (((F * ES) % 16) == 0) {               // groups of 16 bytes
+                        constexpr int G = 16 / ES;
+#pragma unroll
+                        for (int f = 0; f < RS_MAX_NP; f += G)
+                            if (f < F) rs_store_pixel<kTF32, G>(a.y, e0 + f, out + f);
+                    } else if (((F * ES) % 8) == 0) {
+                        constexpr int G = 8 / ES;
+#pragma unroll
+                        for (int f = 0; f < RS_MAX_NP; f += G)
+                            if (f < F) rs_store_pixel<kTF32, G>(a.y, e0 + f, out + f);
+                    } else if (((F * ES) % 4) == 0) {
+                        constexpr int G = 4 / ES;
+#pragma unroll
+                        for (int f = 0; f < RS_MAX_NP; f += G)
+                            if (f < F) rs_store_pixel<kTF32, G>(a.y, e0 + f, out + f);
+                    } else {
+#pragma unroll
+                        for (int f = 0; f < RS_MAX_NP; ++f)
+                            if (f < F) rs_store1<kTF32>(a.y, e0 + f, out[f]);
+                    }
+                }
+                if (a.trace && blockIdx.x == 0 && lane == 0 && q == 0) {
+                    const int64_t kr = (int64_t)(y - s.ylo) + (g - g0);
+                    if (kr < 64) a.trace[192 + kr] = rs_gtimer();
+                }
+            }
+            g += s.yhi - s.ylo;
+        }
+    } else if (!kDirect && warp == 1) {
         // ===== MMA issuer (converged warp, one elected lane issues): D_r = Sum_j shift_j(X_r) W'_j =====
         const uint32_t idesc = make_idesc(kTF32, 128, (uint32_t)a.NP);
         const uint64_t dtpl = ((uint64_t)1 << 16) | ((uint64_t)((8u * (uint32_t)a.rowbytes) >> 4) << 32) |
                               ((uint64_t)1 << 46) | ((uint64_t)a.swz << 61);
         const uint32_t row16 = (uint32_t)a.rowbytes >> 4, slot16 = (uint32_t)a.slot_bytes >> 4;
         const uint32_t b16 = smem_u32(sB) >> 4, bj16 = (uint32_t)(a.NP * a.rowbytes) >> 4;
+        // descriptor words: lo = start address >> 4 (14 bits, smem < 256 KB) | LBO; hi = SBO, version, swizzle
+        const uint32_t lo0 = (uint32_t)dtpl, hi = (uint32_t)(dtpl >> 32), blo = lo0 + b16;
         const uint32_t ring_a16 = (smem_u32(sRing) >> 4) + (uint32_t)(RS_ZR - a.pad_x) * row16;
         const uint32_t mt16 = 128u * row16, acc_cols = (uint32_t)a.acc_cols, row_cols = (uint32_t)a.row_cols;
         const int ring = a.ring, nt = a.nt, ksteps = a.ksteps, S = a.S, mtr = a.mtr;
         int slot = 0, t = 0;
         uint32_t ph = 0, tph = 0, seq = 0;
-        for (int64_t g = g0; g < g1;) {
+        rs_dispatch_shifts(S, ksteps, [&](auto Sc, auto KSc) {
+          constexpr int kS = decltype(Sc)::value, kKS = decltype(KSc)::value;
+          for (int64_t g = g0; g < g1;) {
             const RsSeg s = rs_seg(a, g, g1);
             for (int r = s.rlo; r < s.rhi; ++r, ++seq) {
                 mbar_wait_warp(&full[slot], ph);
@@ -240,26 +491,11 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
                 mbar_wait_warp(&aempty[t], tph ^ 1u);
                 tc_fence_after();
                 const uint32_t d0 = tmem_base + (uint32_t)t * row_cols;
-                const uint32_t a0 = ring_a16 + (uint32_t)slot * slot16;
-                // One elected thread issues the row.  The (shift, k-step) walk is unrolled with compile-time
-                // bounds so every MMA gets its own descriptor registers: rewriting the registers an in-flight
-                // tcgen05.mma still reads stalls the issue (a rolled loop ran at ~230 cycles per MMA).
-                if (elect_one()) {
-                    for (int h = 0; h < mtr; ++h) {
-                        const uint32_t dh = d0 + (uint32_t)h * acc_cols, ah = a0 + (uint32_t)h * mt16;
-#pragma unroll
-                        for (int j = 0; j < RS_MAX_S; ++j) {
-                            if (j < S) {
-#pragma unroll
-                                for (int k = 0; k < 4; ++k)
-                                    if (k < ksteps)
-                                        umma<kTF32>(dh, dtpl | (uint64_t)((ah + (uint32_t)j * row16 + 2u * k) & 0x3FFF),
-                                                    dtpl | (uint64_t)((b16 + (uint32_t)j * bj16 + 2u * k) & 0x3FFF), idesc,
-                                                    (j == 0 && k == 0) ? 0u : 1u);
-                            }
-                        }
-                    }
-                }
+                const uint32_t a0 = lo0 + ring_a16 + (uint32_t)slot * slot16;
+                // the converged warp walks the row's (M-tile, shift, k-step) MMAs (rs_issue_shifts)
+                for (int h = 0; h < mtr; ++h)
+                    rs_issue<kTF32, kS, kKS>(d0 + (uint32_t)h * acc_cols, a0 + (uint32_t)h * mt16, blo, hi, row16, bj16,
+                                             idesc, 0u, S, ksteps);
                 __syncwarp();
                 umma_commit_elect(&afull[t]);
                 umma_commit_elect(&empty[slot]);         // the slot returns to the producer when they retire
@@ -269,8 +505,9 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
                 if (++t == nt) { t = 0; tph ^= 1u; }
             }
             g += s.yhi - s.ylo;
-        }
-    } else if (warp >= 4) {
+          }
+        });
+    } else if (!kDirect && warp >= 4) {
         // ===== epilogue: Y[y] = Sum_i column group i of D_{y - pad_y + i}; element-wise ops; stores =====
         // Two groups of 4 warps: group gi takes the CTA's output rows k with k % 2 == gi (one warp per SM
         // sub-partition runs this loop at dependent-instruction latency: two rows in flight per
@@ -284,7 +521,14 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
         const uint32_t lane0 = tmem_base + ((uint32_t)(q * 32) << 16);
         const int xq = 32 * q + lane;
         const int64_t OWF = (int64_t)a.OW * F;
-        uint32_t v[RS_MAX_NP];
+        // The kernel-row count is a compile-time constant for the common programs (r' = 1, 3, 5):
+        // the R TMEM loads and the row sum are then straight-line code with the image-edge rows
+        // masked by a select, not branched around (a tcgen05.ld is warp-collective: a branch around
+        // it makes ptxas re-converge the warp per load -- measured ~480 cycles to issue one row's loads).
+        auto epilogue = [&](auto Rc) {
+        constexpr int kR = decltype(Rc)::value;          // 0: runtime R (generic shapes)
+        constexpr int kRI = kR > 0 ? kR : RS_MAX_NP / kFp;
+        uint32_t v[kRI * kFp];
         int tb = 0;                                      // TMEM slot of the run's first loaded row (rlo)
         uint32_t seq0 = 0;                               // sequence number of the run's first loaded row
         uint32_t n_c = 0, ph_c = 0;                      // cursor: newest row waited for (seq, slot, phase)
@@ -306,6 +550,9 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
             const int64_t img_el = (int64_t)s.img * a.OH;
             for (int y = s.ylo; y < s.yhi; ++y, ++krow) {
                 if ((int)(krow & 1u) != gi) continue;
+                // debug-only phase timeline of CTA 0, warp 4, output row 4 (OLLIE_RS_DBG bit 2)
+                const bool ptr = (a.dbg & 4) && a.trace && blockIdx.x == 0 && warp == 4 && lane == 0 && krow == 4;
+                if (ptr) a.trace[256] = clock64();
                 const int rb = y - pad_y;                // input row of kernel row 0
                 const int rtop = min(rb + R - 1, s.rhi - 1);
                 if (rtop >= s.rlo) {                     // D of every row up to rtop is complete (in-order commits)
@@ -317,21 +564,31 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
                     mbar_wait(&afull[t_c], ph_c);
                     tc_fence_after();
                 }
+                if (ptr) a.trace[257] = clock64();
                 // TMEM slot of row rb + i: (tb + rb - rlo + i) mod nt (rb - rlo in [-pad_y, ...])
                 int t0 = tb + (rb - s.rlo);
                 while (t0 < 0) t0 += nt;
                 while (t0 >= nt) t0 -= nt;
+                uint32_t vmask = 0;                      // kernel rows i whose input row rb + i exists
+#pragma unroll
+                for (int i = 0; i < kRI; ++i)
+                    if ((kR > 0 || i < R) && rb + i >= s.rlo && rb + i < s.rhi) vmask |= 1u << i;
                 for (int h = 0; h < mtr; ++h) {
                     const uint32_t lanebase = lane0 + (uint32_t)h * acc_cols;
-                    int ti = t0;
 #pragma unroll
-                    for (int i = 0; i < RS_MAX_NP / kFp; ++i) {
-                        const int r = rb + i;
-                        if (i < R && r >= s.rlo && r < s.rhi)
+                    for (int i = 0; i < kRI; ++i) {
+                        int ti = t0 + i;                     // TMEM slot of row rb + i (i < R < nt)
+                        if (ti >= nt) ti -= nt;
+                        if constexpr (kR > 0) {
                             rs_tmem_ld<kFp>(lanebase + (uint32_t)ti * row_cols + (uint32_t)(i * kFp), &v[i * kFp]);
-                        if (++ti == nt) ti = 0;
+                        } else {
+                            if (i < R && ((vmask >> i) & 1u))
+                                rs_tmem_ld<kFp>(lanebase + (uint32_t)ti * row_cols + (uint32_t)(i * kFp), &v[i * kFp]);
+                        }
                     }
+                    if (ptr) a.trace[260 + 4 * h] = clock64();
                     tmem_ld_wait();
+                    if (ptr) a.trace[261 + 4 * h] = clock64();
                     // the row's last TMEM reads are done: hand the slots back before the stores (this
                     // group's next row, y + 2, reads rows >= rb + 2), shortening the MMA <-> epilogue chain
                     if (h == mtr - 1) release_upto(rb + 1);
@@ -339,30 +596,20 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
 #pragma unroll
                     for (int f = 0; f < kFp; ++f) out[f] = 0.f;
 #pragma unroll
-                    for (int i = 0; i < RS_MAX_NP / kFp; ++i) {
-                        const int r = rb + i;
-                        if (i < R && r >= s.rlo && r < s.rhi) {
+                    for (int i = 0; i < kRI; ++i) {
+                        const bool ok = (vmask >> i) & 1u;   // edge rows: garbage / stale TMEM, selected out
 #pragma unroll
-                            for (int f = 0; f < kFp; ++f) out[f] += __uint_as_float(v[i * kFp + f]);
-                        }
+                        for (int f = 0; f < kFp; ++f) out[f] += ok ? __uint_as_float(v[i * kFp + f]) : 0.f;
                     }
+                    if (ptr) a.trace[262 + 4 * h] = clock64();
                     const int x = 128 * h + xq;              // output column of this lane
                     if (x >= OWc) continue;
                     if (sub == 1) {
                         const int64_t e0 = ((img_el + y) * a.OW + x) * F;
                         if (a.epi.on) epi_apply<!kTF32, kFp>(a.epi, out, e0, 0, F);
-                        if (!kTF32 && F == kFp && (kFp % 8) == 0) {
-                            uint16_t *yp = reinterpret_cast<uint16_t *>(a.y) + e0;
-#pragma unroll
-                            for (int f = 0; f < kFp; f += 8)
-                                *reinterpret_cast<uint4 *>(yp + f) =
-                                    make_uint4(pack_bf16x2_rn(out[f], out[f + 1]), pack_bf16x2_rn(out[f + 2], out[f + 3]),
-                                               pack_bf16x2_rn(out[f + 4], out[f + 5]), pack_bf16x2_rn(out[f + 6], out[f + 7]));
-                        } else if (kTF32 && F == kFp && (kFp % 4) == 0) {
-                            float *yp = reinterpret_cast<float *>(a.y) + e0;
-#pragma unroll
-                            for (int f = 0; f < kFp; f += 4)
-                                *reinterpret_cast<float4 *>(yp + f) = make_float4(out[f], out[f + 1], out[f + 2], out[f + 3]);
+                        if (F == kFp) {
+                            rs_store_pixel<kTF32, kFp>(a.y, e0, out);
+                            if (ptr) a.trace[263 + 4 * h] = clock64();
                         } else {
 #pragma unroll
                             for (int f = 0; f < kFp; ++f)
@@ -417,6 +664,19 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
             tb += s.rhi - s.rlo;
             while (tb >= nt) tb -= nt;
             g += s.yhi - s.ylo;
+        }
+        };
+        switch (R) {
+            case 1: epilogue(rs_ic<1>{}); break;
+            case 3:
+                if constexpr (3 * kFp <= RS_MAX_NP) epilogue(rs_ic<3>{});
+                else epilogue(rs_ic<0>{});
+                break;
+            case 5:
+                if constexpr (5 * kFp <= RS_MAX_NP) epilogue(rs_ic<5>{});
+                else epilogue(rs_ic<0>{});
+                break;
+            default: epilogue(rs_ic<0>{}); break;
         }
     }
 

@@ -3,6 +3,10 @@
 row OffsetAdd over the TMEM accumulators of consecutive input rows in the epilogue -- against the
 fp64 oracle's direct Conv2d / scatter-form ConvTranspose2d.
 
+Both forms of the kernel run every case they plan: "ysum" (kernel rows on N, the row OffsetAdd in
+the epilogue) and "direct" (N = f, all r*s taps as A-row shifts, one accumulator per output row;
+Conv2d only, which also takes the wide-f 1x1 / 3x3 layers of RS_DIRECT_LAYERS).
+
 Integer mode is bit-exact; random data meets the bf16 / TF32 bars.  The shapes cover image
 rows over several 128-pixel M-tiles (w up to 300, two TMA boxes per row), ragged widths, every
 kernel-variant width (stride^2 * f = 4, 8, 12, 16), 32/64/128-byte pixel rows (c = 8..64 bf16,
@@ -37,6 +41,18 @@ RS_LAYERS = [
     L("rs_tf32_deconv", 1, 8, 7, 20, 1, 9, 9, pad=4, stride=2, output_padding=1, transposed=True, dtype="tf32"),
     L("rs_many_rows", 37, 16, 11, 16, 16, 3, 3, pad=1),                      # 407 rows: runs cross images
 ]
+# shapes only the direct form (N = f, all r*s taps as A shifts) plans
+RS_DIRECT_LAYERS = [
+    L("rd_1x1_12to56", 2, 16, 7, 200, 56, 1, 1),                             # FSRCNN expand (c padded 12 -> 16)
+    L("rd_1x1_56to12", 1, 56, 9, 150, 12, 1, 1),                             # FSRCNN shrink, 112-byte pixels
+    L("rd_3x3_c64_f64", 1, 64, 6, 130, 64, 3, 3, pad=1),                     # 4 K steps, 36 MMAs per M-tile
+    L("rd_f3_odd", 2, 32, 5, 40, 3, 3, 3, pad=1),                            # f = 3: scalar stores
+    L("rd_5x5_f24", 1, 16, 9, 70, 24, 5, 5, pad=2),                          # NP 32, 25 taps
+    L("rd_w400_f16", 1, 8, 4, 400, 16, 3, 3, pad=1),                         # 4 M-tiles, 2 TMA boxes
+    L("rd_tf32_1x1", 2, 16, 5, 129, 40, 1, 1, dtype="tf32"),
+    L("rd_pad0_top", 3, 16, 4, 20, 16, 3, 3, pad=0),                         # OH < H: runs skip rows
+]
+FORMS = ["ysum", "direct"]
 
 
 @pytest.fixture(scope="module")
@@ -45,9 +61,21 @@ def O():
     return ollie
 
 
-def _run(O, lay, x, w, **epi):
+def _plan(O, form):
+    return {"ysum": O.PLAN_ROWSTREAM_YSUM, "direct": O.PLAN_ROWSTREAM_DIRECT, "auto": O.PLAN_ROWSTREAM}[form]
+
+
+def _plannable(O, lay, form):
     from paper_2208_02025_b200 import DerivedConv
-    conv = DerivedConv.from_layer(lay, plan=O.PLAN_ROWSTREAM)
+    try:
+        return DerivedConv.from_layer(lay, plan=_plan(O, form)).resolved_plan() == "rowstream"
+    except O.OllieError:
+        return False
+
+
+def _run(O, lay, x, w, form="auto", **epi):
+    from paper_2208_02025_b200 import DerivedConv
+    conv = DerivedConv.from_layer(lay, plan=_plan(O, form))
     assert conv.resolved_plan() == "rowstream"
     conv.prepare(_dev(w))
     y = torch.full(conv.out_shape(), float("nan"), dtype=syn.torch_dtype(lay.dtype), device="cuda")
@@ -56,37 +84,55 @@ def _run(O, lay, x, w, **epi):
     return y.float().cpu().numpy()
 
 
-@pytest.mark.parametrize("lay", RS_LAYERS, ids=[l.name for l in RS_LAYERS])
-def test_rowstream_integer_exact(O, lay):
+ALL = RS_LAYERS + RS_DIRECT_LAYERS
+
+
+@pytest.mark.parametrize("form", FORMS)
+@pytest.mark.parametrize("lay", ALL, ids=[l.name for l in ALL])
+def test_rowstream_integer_exact(O, lay, form):
+    if not _plannable(O, lay, form):
+        pytest.skip(f"{form} form does not plan {lay.name}")
     x, w = syn.layer_inputs(lay, 300, exact_int=True)
-    got = _run(O, lay, x, w)
+    got = _run(O, lay, x, w, form)
     assert np.array_equal(got, _round_like(_oracle_layer(lay, x, w), lay.dtype))
 
 
-@pytest.mark.parametrize("lay", RS_LAYERS, ids=[l.name for l in RS_LAYERS])
-def test_rowstream_random(O, lay):
+@pytest.mark.parametrize("form", FORMS)
+@pytest.mark.parametrize("lay", ALL, ids=[l.name for l in ALL])
+def test_rowstream_random(O, lay, form):
+    if not _plannable(O, lay, form):
+        pytest.skip(f"{form} form does not plan {lay.name}")
     x, w = syn.layer_inputs(lay, 301)
-    got = _run(O, lay, x, w)
+    got = _run(O, lay, x, w, form)
     assert _max_rel(got, _oracle_layer(lay, x, w)) <= TOL[lay.dtype]
 
 
-@pytest.mark.parametrize("name", ["rs_map_3x3_16", "rs_deconv_9x9", "rs_dcgan_64to3"])
+def test_rowstream_direct_covers_every_conv_case(O):
+    """Every stride-1 Conv2d case of the table plans in the direct form too (so both forms are
+    exercised on them), and the direct-only table is plannable direct."""
+    for lay in ALL:
+        if not lay.transposed:
+            assert _plannable(O, lay, "direct"), lay.name
+
+
+@pytest.mark.parametrize("name,form", [("rs_map_3x3_16", "ysum"), ("rs_map_3x3_16", "direct"), ("rs_deconv_9x9", "ysum"),
+                                       ("rs_dcgan_64to3", "ysum"), ("rd_1x1_12to56", "direct"), ("rd_f3_odd", "direct")])
 @pytest.mark.parametrize("act", [1, 2])
-def test_rowstream_epilogue_exact(O, name, act):
-    lay = next(l for l in RS_LAYERS if l.name == name)
+def test_rowstream_epilogue_exact(O, name, form, act):
+    lay = next(l for l in ALL if l.name == name)
     x, w = syn.layer_inputs(lay, 302, exact_int=True)
     g = torch.Generator().manual_seed(5)
     bias = torch.randint(-8, 9, (lay.f,), generator=g).float()
     res = torch.randint(-4, 5, (lay.n, lay.oh, lay.ow, lay.f), generator=g).to(syn.torch_dtype(lay.dtype))
     alpha = torch.full((lay.f,), 0.25)
-    got = _run(O, lay, x, w, bias=_dev(bias), residual=_dev(res), act=act, alpha=_dev(alpha))
+    got = _run(O, lay, x, w, form, bias=_dev(bias), residual=_dev(res), act=act, alpha=_dev(alpha))
     ref = oracle.epilogue(_oracle_layer(lay, x, w), bias.numpy(), res, "relu" if act == 1 else "prelu", alpha.numpy())
     assert np.array_equal(got, _round_like(ref, lay.dtype))
 
 
 def test_rowstream_unsupported_is_a_status(O):
     from paper_2208_02025_b200 import DerivedConv
-    lay = L("too_wide", 1, 64, 8, 8, 64, 3, 3, pad=1)        # s * f = 192 columns > 64
+    lay = L("too_wide", 1, 64, 8, 8, 96, 3, 3, pad=1)        # f = 96 > 64 (either form)
     conv = DerivedConv.from_layer(lay, plan=O.PLAN_ROWSTREAM)
     x, w = syn.layer_inputs(lay, 303, exact_int=True)
     conv.prepare(_dev(w))

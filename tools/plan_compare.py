@@ -19,7 +19,7 @@ from paper_2208_02025_b200.stack import DerivedStack
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "fsrcnn"
 names = sys.argv[2:] or ["auto", "fused", "unfused", "rowstream"]
-PLANS = {"auto": O.PLAN_AUTO, "fused": O.PLAN_FUSED, "unfused": O.PLAN_UNFUSED, "rowstream": O.PLAN_ROWSTREAM}
+PLANS = {"auto": O.PLAN_AUTO, "fused": O.PLAN_FUSED, "unfused": O.PLAN_UNFUSED, "rowstream": O.PLAN_ROWSTREAM, "rs_ysum": O.PLAN_ROWSTREAM_YSUM, "rs_direct": O.PLAN_ROWSTREAM_DIRECT}
 layers = syn.CONFIGS[cfg]
 chained = cfg in ("fsrcnn", "dcgan")
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")

@@ -13,14 +13,14 @@ from paper_2208_02025_b200.stack import DerivedStack
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="resnet18")
 ap.add_argument("--layer", type=int, default=-1, help="-1: all layers of the config")
-ap.add_argument("--plan", default="auto", choices=["auto", "fused", "unfused", "rowstream"])
+ap.add_argument("--plan", default="auto", choices=["auto", "fused", "unfused", "rowstream", "rs_ysum", "rs_direct"])
 ap.add_argument("--iters", type=int, default=3)
 a = ap.parse_args()
 layers = syn.CONFIGS[a.config]
 if a.layer >= 0:
     layers = [layers[a.layer]]
 chained = a.config in ("fsrcnn", "dcgan") and a.layer < 0
-plan = {"auto": O.PLAN_AUTO, "fused": O.PLAN_FUSED, "unfused": O.PLAN_UNFUSED, "rowstream": O.PLAN_ROWSTREAM}[a.plan]
+plan = {"auto": O.PLAN_AUTO, "fused": O.PLAN_FUSED, "unfused": O.PLAN_UNFUSED, "rowstream": O.PLAN_ROWSTREAM, "rs_ysum": O.PLAN_ROWSTREAM_YSUM, "rs_direct": O.PLAN_ROWSTREAM_DIRECT}[a.plan]
 st = DerivedStack(layers, chained)
 for sl in st.layers:          # the requested plan where the layer admits it, else AUTO
     try:

@@ -81,6 +81,45 @@ __global__ void __launch_bounds__(256, 1) stream_rows_pc(const __grid_constant__
     __syncthreads();
 }
 
+// NPROD producer warps in one CTA (lane 0 of warps 0..NPROD-1), each streaming every NPROD-th op through
+// its own share of the ring: is a CTA's TMA rate a per-warp or a per-CTA (per-SM) limit?
+template <int NPROD>
+__global__ void __launch_bounds__(128, 1) stream_rows_mp(const __grid_constant__ CUtensorMap tm, int rows_total, int W,
+                                                        int wbox, int nst, int box_bytes, long long *cyc) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full[64];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NPROD * nst; ++i) mbar_init(&full[i], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const int r0 = (int)((long long)rows_total * blockIdx.x / gridDim.x);
+    const int r1 = (int)((long long)rows_total * (blockIdx.x + 1) / gridDim.x);
+    const int nb = W / wbox;
+    const int nops = (r1 - r0) * nb;
+    if (warp < NPROD && lane == 0) {
+        uint64_t *fb = full + warp * nst;
+        uint8_t *sm = smem + (size_t)warp * nst * box_bytes;
+        int issued = 0, done = 0, mine = 0;
+        for (int op = warp; op < nops; op += NPROD) ++mine;
+        auto issue = [&](int j) {      // j-th op of this warp
+            const int op = warp + j * NPROD, s = j % nst;
+            const int row = r0 + op / nb, b = op % nb;
+            mbar_arrive_expect_tx(&fb[s], box_bytes);
+            tma_load_4d(sm + (size_t)s * box_bytes, &tm, &fb[s], 0, b * wbox, row, 0);
+        };
+        for (; issued < nst && issued < mine; ++issued) issue(issued);
+        for (; done < mine; ++done) {
+            mbar_wait(&fb[done % nst], (done / nst) & 1);
+            if (issued < mine) issue(issued++);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) cyc[blockIdx.x] = 0;
+}
+
 int main() {
     const int W = 256, H = 16384;   // 16384 rows of 256 pixels (FSRCNN: 64 images x 256 rows)
     int sms = 0;
@@ -90,7 +129,7 @@ int main() {
     long long *cyc;
     cudaMalloc(&cyc, sizeof(long long) * 1024);
     struct Cfg { int C, cbox, wbox, hbox; };
-    const Cfg cfgs[] = {{16, 16, 256, 1}, {56, 64, 256, 1}};
+    const Cfg cfgs[] = {{16, 16, 256, 1}};
     for (const Cfg &c : cfgs) {
         const size_t bytes = (size_t)H * W * c.C * 2;
         void *x;
@@ -138,6 +177,43 @@ int main() {
             }
         }
         cudaFree(x);
+    }
+    {   // multi-producer test: C=16 box {16,256,1} (8 KB) and C=64 box {64,128,1} (16 KB)
+        for (int C : {16, 64}) {
+            const int W = 256, H = 16384, wbox = C == 16 ? 256 : 128;
+            const size_t bytes = (size_t)H * W * C * 2;
+            void *x; cudaMalloc(&x, bytes); cudaMemset(x, 1, bytes);
+            CUtensorMap tm;
+            cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, 1};
+            cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+            cuuint32_t box[4] = {(cuuint32_t)C, (cuuint32_t)wbox, 1, 1};
+            cuuint32_t estr[4] = {1, 1, 1, 1};
+            cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, x, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   C == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            const int box_bytes = C * 2 * wbox;
+            for (int np : {1, 2, 4}) {
+                const int nst = 4;
+                const size_t sm = (size_t)np * nst * box_bytes + 1024;
+                auto run = [&]() {
+                    if (np == 1) stream_rows_mp<1><<<sms, 128, sm>>>(tm, H, W, wbox, nst, box_bytes, cyc);
+                    if (np == 2) stream_rows_mp<2><<<sms, 128, sm>>>(tm, H, W, wbox, nst, box_bytes, cyc);
+                    if (np == 4) stream_rows_mp<4><<<sms, 128, sm>>>(tm, H, W, wbox, nst, box_bytes, cyc);
+                };
+                cudaFuncSetAttribute(stream_rows_mp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+                cudaFuncSetAttribute(stream_rows_mp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+                cudaFuncSetAttribute(stream_rows_mp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+                run();
+                cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+                cudaEventRecord(e0);
+                for (int it = 0; it < 3; ++it) run();
+                cudaEventRecord(e1); cudaEventSynchronize(e1);
+                float ms; cudaEventElapsedTime(&ms, e0, e1);
+                printf("multi-producer C=%d box %d B: %d producer warps x %d stages: %7.1f us  %6.0f GB/s  err=%s\n", C, box_bytes, np, nst,
+                       ms * 1e3 / 3, bytes / (ms * 1e-3 / 3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+            }
+            cudaFree(x);
+        }
     }
     return 0;
 }
