@@ -159,6 +159,28 @@ __global__ void __launch_bounds__(256) selective_add_kernel(OffsetAddArgs a) {
         for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
         const int64_t th = oh + a.pad, tw = ow + a.pad;
         const float *Tb = a.T + (b * a.h) * a.w * a.ldT + fv * VEC;
+        if (VEC == 4 && a.r <= 2 * st && a.s <= 2 * st) {
+            // at most 2 x 2 selected taps (4x4 / 3x3 kernels at stride 2): issue the four
+            // predicated 16-byte loads before summing, in the same (i, j) order as below
+            float4 tv[4];
+            const int64_t i0 = th % st, j0 = tw % st;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t i = i0 + (q >> 1) * st, j = j0 + (q & 1) * st;
+                const int64_t ih = (th - i) / st, iw = (tw - j) / st;
+                const bool in = i < a.r && i <= th && ih < a.h && j < a.s && j <= tw && iw < a.w;
+                tv[q] = in ? ld_stream_f4(Tb + (ih * a.w + iw) * a.ldT + (i * a.s + j) * a.f)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                acc[0] += tv[q].x;
+                if constexpr (VEC == 4) { acc[1] += tv[q].y; acc[2] += tv[q].z; acc[3] += tv[q].w; }
+            }
+            if (a.epi.on) epi_apply<kOutBF16, VEC>(a.epi, acc, px * a.f + fv * VEC, (int)(fv * VEC), VEC);
+            store_y<VEC, kOutBF16>(a.y, px * a.f + fv * VEC, acc);
+            continue;
+        }
         // th = oh + p >= 0, so th % st is the smallest selected kernel row; rows past th
         // would need a negative input row, and the input row falls as i grows.
         for (int64_t i = th % st; i < a.r && i <= th; i += st) {

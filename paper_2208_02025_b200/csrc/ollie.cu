@@ -1964,7 +1964,9 @@ extern "C" ollie_status ollie_eop_eval(const ollie_eop *eop, const void *const *
             const int64_t vec_per_row = (fe.inner + 7) / 8;
             const int64_t blocks = std::min<int64_t>(ceil_div((int64_t)fe.rows * vec_per_row, 256), (int64_t)num_sms() * 32);
             const unsigned gb = (unsigned)std::max<int64_t>(blocks, 1);
-            if (fe.in_bf16 == fe.out_bf16 && fe.inner <= 64 && fe.inner * (fe.in_bf16 ? 2 : 4) % 16 == 0 && aligned16(fe.out)) {
+            static const int rows_mode = [] { const char *e = getenv("OLLIE_EOP_ROWS"); return e ? atoi(e) : 1; }();
+            if (rows_mode && fe.in_bf16 == fe.out_bf16 && fe.inner <= 64 && fe.inner * (fe.in_bf16 ? 2 : 4) % 16 == 0 &&
+                aligned16(fe.out)) {
                 // narrow 16-byte-multiple rows: one thread per row
                 const int64_t rb = std::min<int64_t>(ceil_div((int64_t)fe.rows, 256), (int64_t)num_sms() * 32);
                 const unsigned g = (unsigned)std::max<int64_t>(rb, 1);

@@ -380,7 +380,8 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
                 __syncwarp();
                 if (a.trace && blockIdx.x == 0 && kr < 64 && lane == 0) a.trace[128 + kr] = rs_gtimer();
                 if (++t == nt) { t = 0; tph ^= 1u; }
-                if (rb >= s.rlo) release_upto(seq0 + (uint32_t)(rb - s.rlo + 1));   // no later output row reads rb
+                // no later output row reads rb (rows below the image, rb >= rhi, were never loaded)
+                if (rb >= s.rlo) release_upto(seq0 + (uint32_t)min(rb - s.rlo + 1, s.rhi - s.rlo));
             }
             release_upto(seq0 + (uint32_t)(s.rhi - s.rlo));
             seq0 += (uint32_t)(s.rhi - s.rlo);

@@ -38,7 +38,9 @@ y = auto.new_output()
 auto(xd, y)
 print(f"{lay.name} auto {graph_time(lambda s: auto(xd, y, s.cuda_stream)):.2f} us  {auto.resolved_plan()}")
 res = []
-for mt, fs, rs, pr, ks in itertools.product((1, 2, 4), (32, 64, 128, 256), (0, 1), (0, 1), (1, 2, 4)):
+G8S = tuple(int(v) for v in os.environ.get("G8S", "-1").split(","))
+for mt, fs, rs, pr, ks, g8 in itertools.product((1, 2, 4), (32, 64, 128, 256), (0, 1), (0, 1), (1, 2, 4), G8S):
+    O._lib.ollie_debug_force_grp8(g8)
     O._lib.ollie_debug_force_plan(mt, fs, rs)
     O._lib.ollie_debug_force_pair(pr)
     O._lib.ollie_debug_force_ksplit(ks)
@@ -52,6 +54,7 @@ for mt, fs, rs, pr, ks in itertools.product((1, 2, 4), (32, 64, 128, 256), (0, 1
 O._lib.ollie_debug_force_plan(0, 0, -1)
 O._lib.ollie_debug_force_pair(-1)
 O._lib.ollie_debug_force_ksplit(-1)
+O._lib.ollie_debug_force_grp8(-1)
 res.sort()
-for t, d in res[:6]:
+for t, d in res[:int(os.environ.get("TOP", "6"))]:
     print(f"   {t:7.2f} us  {d}")
