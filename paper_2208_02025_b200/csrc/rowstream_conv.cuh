@@ -549,7 +549,13 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
                 }
             };
             const int64_t img_el = (int64_t)s.img * a.OH;
-            for (int y = s.ylo; y < s.yhi; ++y, ++krow) {
+            // TMEM slot of input row rb = y - pad_y: (tb + rb - rlo) mod nt, reduced once per run and then
+            // advanced by one per output row (a per-row reduction loop of ~(rb - rlo) / nt iterations ran
+            // at branch-resolve latency and was the largest item of the epilogue's row time)
+            int t0y = tb + (s.ylo - pad_y - s.rlo);
+            while (t0y < 0) t0y += nt;
+            while (t0y >= nt) t0y -= nt;
+            for (int y = s.ylo; y < s.yhi; ++y, ++krow, t0y = (t0y + 1 == nt) ? 0 : t0y + 1) {
                 if ((int)(krow & 1u) != gi) continue;
                 // debug-only phase timeline of CTA 0, warp 4, output row 4 (OLLIE_RS_DBG bit 2)
                 const bool ptr = (a.dbg & 4) && a.trace && blockIdx.x == 0 && warp == 4 && lane == 0 && krow == 4;
@@ -567,9 +573,7 @@ rowstream_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_cons
                 }
                 if (ptr) a.trace[257] = clock64();
                 // TMEM slot of row rb + i: (tb + rb - rlo + i) mod nt (rb - rlo in [-pad_y, ...])
-                int t0 = tb + (rb - s.rlo);
-                while (t0 < 0) t0 += nt;
-                while (t0 >= nt) t0 -= nt;
+                const int t0 = t0y;
                 uint32_t vmask = 0;                      // kernel rows i whose input row rb + i exists
 #pragma unroll
                 for (int i = 0; i < kRI; ++i)
