@@ -298,58 +298,74 @@ __global__ void __launch_bounds__(256) tap_fold_kernel(TapFoldArgs a) {
 }
 
 // Row-tiled form: one CTA per output row (b, oy) stages the r input rows the row reads
-// (oy*st - p + i*d, zero outside the image) in shared memory with coalesced loads, then writes the
-// row's OW * KP outputs as consecutive 16-byte chunks (lane t -> chunk t: fully coalesced stores).
+// (oy*st - p + i*d, zero outside the image) in shared memory, then writes the row's OW * KP outputs
+// as consecutive 16-byte chunks (lane t -> chunk t: fully coalesced stores).  The staged rows carry
+// zero halo columns on both sides (row pitch rpitch elements, image column 0 at element `roff`,
+// 16-byte aligned) and one zero cell past the last row, so an output element is ONE shared-memory
+// read at addr_e + ox * step_e with no bounds test: a thread's k-chunk is fixed, (addr_e, step_e) are
+// decoded once (k >= r*s*c: the zero cell, step 0).  ncu on the earlier form (per-element bounds
+// tests, a division per staged element): 227 instructions per 16-byte output chunk, issue-bound.
+struct TapFoldRows {
+    int32_t roff, rpitch;       // image column 0 of a staged row (elements, multiple of 16 bytes); row pitch
+    int32_t zcell;              // element index of the zero cell
+    int32_t vec;                // 1: staged rows are filled with 16-byte loads / stores
+};
+
 template <bool kF32>
-__global__ void __launch_bounds__(256) tap_fold_rows_kernel(TapFoldArgs a) {
+__global__ void __launch_bounds__(256) tap_fold_rows_kernel(TapFoldArgs a, TapFoldRows g) {
     constexpr int VE = kF32 ? 4 : 8;
     using E = typename std::conditional<kF32, uint32_t, uint16_t>::type;
     extern __shared__ uint8_t tf_smem[];
-    E *rows = reinterpret_cast<E *>(tf_smem);        // [R][W * C]
+    E *rows = reinterpret_cast<E *>(tf_smem);        // [R][rpitch] + the zero cell
     pdl_wait();
     const E *x = reinterpret_cast<const E *>(a.x);
     const int WC = a.W * a.C;
     const int cpp = a.KP / VE;                       // 16-byte chunks per output pixel
     const int chunks = a.OW * cpp;
-    int off[VE], jd[VE];                             // smem offset (without the pixel) and column shift per element
-    bool kv[VE];
+    int addr[VE], step[VE];
     {
         const int k0 = (threadIdx.x % cpp) * VE;
         int c = k0 % a.C, tap = k0 / a.C;
         int j = tap % a.S, i = tap / a.S;
 #pragma unroll
         for (int e = 0; e < VE; ++e) {
-            kv[e] = k0 + e < a.RSC;
-            off[e] = i * WC + c;
-            jd[e] = j * a.dil;
+            const bool kv = k0 + e < a.RSC;
+            addr[e] = kv ? i * g.rpitch + g.roff + (j * a.dil - a.pad) * a.C + c : g.zcell;
+            step[e] = kv ? a.st * a.C : 0;
             if (++c == a.C) {
                 c = 0;
                 if (++j == a.S) { j = 0; ++i; }
             }
         }
     }
+    // the halo columns and the zero cell are never written with data: zero them once
+    for (int t = threadIdx.x; t < a.R * g.rpitch + 1; t += blockDim.x) {
+        const int col = t % g.rpitch;
+        if (t == g.zcell || col < g.roff || col >= g.roff + WC) rows[t] = (E)0;
+    }
     for (int64_t row = blockIdx.x; row < a.items; row += gridDim.x) {   // items = n * OH output rows
         const int oy = (int)(row % a.OH);
         const int64_t b = row / a.OH;
         __syncthreads();                             // the previous row's readers are done
-        for (int t = threadIdx.x; t < a.R * WC; t += blockDim.x) {
-            const int i = t / WC, e = t - i * WC;
+        for (int i = 0; i < a.R; ++i) {
             const int iy = oy * a.st - a.pad + i * a.dil;
-            rows[t] = (iy >= 0 && iy < a.H) ? __ldg(x + (b * a.H + iy) * (int64_t)WC + e) : (E)0;
+            const bool in = iy >= 0 && iy < a.H;
+            E *dst = rows + i * g.rpitch + g.roff;
+            const E *src = x + (b * a.H + iy) * (int64_t)WC;
+            if (g.vec) {
+                for (int t = threadIdx.x; t < WC / VE; t += blockDim.x)
+                    reinterpret_cast<uint4 *>(dst)[t] = in ? __ldg(reinterpret_cast<const uint4 *>(src) + t) : make_uint4(0, 0, 0, 0);
+            } else {
+                for (int t = threadIdx.x; t < WC; t += blockDim.x) dst[t] = in ? __ldg(src + t) : (E)0;
+            }
         }
         __syncthreads();
         E *orow = reinterpret_cast<E *>(a.out) + row * (int64_t)a.OW * a.KP;
         for (int ch = threadIdx.x; ch < chunks; ch += blockDim.x) {
-            // the thread's k-chunk is fixed (blockDim % (KP / VE) == 0, host-checked): its (i, j, c)
-            // offsets were decoded once, only the pixel moves
             const int ox = ch / cpp;
-            const int xo = ox * a.st - a.pad;
             E v[VE];
 #pragma unroll
-            for (int e = 0; e < VE; ++e) {
-                const int ix = xo + jd[e];
-                v[e] = (kv[e] && ix >= 0 && ix < a.W) ? rows[off[e] + ix * a.C] : (E)0;
-            }
+            for (int e = 0; e < VE; ++e) v[e] = rows[addr[e] + ox * step[e]];
             uint4 pk;
             if constexpr (kF32) pk = make_uint4(v[0], v[1], v[2], v[3]);
             else

@@ -1295,12 +1295,26 @@ extern "C" ollie_status ollie_tap_fold(const ollie_conv_shape *shape, ollie_dtyp
     a.OH = (int)OH; a.OW = (int)OW; a.KP = (int)kp; a.RSC = (int)rsc;
     const int ve = 16 / es;
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t rows_smem = (size_t)shape->r * shape->w * shape->c * es;
-    if (rows_smem <= 48 * 1024 && 256 % (kp / ve) == 0) {   // row-tiled: r input rows in smem, coalesced stores
+    // row-tiled: the r input rows in smem with zero halo columns (left: every column a tap reads left of
+    // the image, rounded up to 16 bytes; right: past the last image column), coalesced stores
+    TapFoldRows tr{};
+    {
+        const int64_t lo = std::min<int64_t>(0, -(int64_t)shape->pad);                              // leftmost column read
+        const int64_t hi = std::max<int64_t>(shape->w - 1, (OW - 1) * shape->stride - shape->pad +
+                                                               (shape->s - 1) * (int64_t)shape->dilation);
+        const int64_t roff = ceil_div(-lo * shape->c, ve) * ve;
+        const int64_t rpitch = ceil_div(roff + (hi + 1) * shape->c, ve) * ve;
+        tr.roff = (int)std::min<int64_t>(roff, INT32_MAX);
+        tr.rpitch = (int)std::min<int64_t>(rpitch, INT32_MAX);
+        tr.zcell = (int)std::min<int64_t>(shape->r * rpitch, INT32_MAX);
+        tr.vec = ((shape->w * shape->c) % ve == 0 && aligned16(x_nhwc)) ? 1 : 0;
+    }
+    const size_t rows_smem = ((size_t)tr.zcell + 1) * es;
+    if (rows_smem <= 48 * 1024 && 256 % (kp / ve) == 0 && (int64_t)tr.zcell < INT32_MAX) {
         a.items = shape->n * OH;
         const unsigned g1 = (unsigned)std::max<int64_t>(std::min<int64_t>(a.items, (int64_t)num_sms() * 64), 1);
-        if (es == 2) CUDA_TRY(launch(tap_fold_rows_kernel<false>, dim3(g1), dim3(256), rows_smem, s, a));
-        else CUDA_TRY(launch(tap_fold_rows_kernel<true>, dim3(g1), dim3(256), rows_smem, s, a));
+        if (es == 2) CUDA_TRY(launch(tap_fold_rows_kernel<false>, dim3(g1), dim3(256), rows_smem, s, a, tr));
+        else CUDA_TRY(launch(tap_fold_rows_kernel<true>, dim3(g1), dim3(256), rows_smem, s, a, tr));
         CHECK_LAUNCH();
         return ok();
     }

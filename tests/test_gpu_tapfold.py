@@ -15,6 +15,10 @@ FOLD = [  # (n, h, w, c, r, s, pad, stride, dil, kp, dtype)
     (2, 9, 11, 1, 5, 5, 2, 1, 1, 32, "bf16"), (1, 7, 8, 3, 3, 3, 1, 2, 1, 32, "bf16"),
     (2, 6, 9, 2, 3, 3, 2, 1, 2, 24, "bf16"), (1, 5, 5, 1, 9, 9, 4, 1, 1, 88, "bf16"),
     (1, 6, 7, 1, 5, 5, 2, 1, 1, 28, "tf32"), (3, 4, 4, 3, 2, 2, 0, 1, 1, 16, "bf16"),
+    # 16-byte staged rows (w * c a multiple of 8 bf16 / 4 fp32), halos wider than the pad, FSRCNN width
+    (2, 5, 16, 1, 5, 5, 2, 1, 1, 32, "bf16"), (1, 6, 24, 2, 3, 3, 1, 2, 2, 24, "bf16"),
+    (1, 3, 256, 1, 5, 5, 2, 1, 1, 32, "bf16"), (1, 4, 1, 1, 3, 3, 1, 1, 1, 16, "bf16"),
+    (1, 5, 8, 4, 3, 3, 3, 1, 1, 40, "tf32"), (2, 7, 8, 1, 9, 9, 4, 2, 1, 88, "bf16"),
 ]
 
 
