@@ -1,0 +1,103 @@
+// mma_sbo.cu -- tcgen05.mma (kind::f16, M=128) rate for the fused conv kernel's A-operand layouts:
+// the 8-row-group stride SBO (1024 B = consecutive patch rows; Xb * 128 B = the grp8 lane layout),
+// the tap row offsets of a patch of width xb ({0,1,2,xb,xb+1,...} rows), and MT accumulators.
+// One CTA per SM, a converged issuer warp (one elected lane), 9 taps x 4 k-steps per accumulator
+// per chunk, random bf16 data.  Prints cycles per MMA.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/mma_sbo tools/mma_sbo.cu
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+#include "../paper_2208_02025_b200/csrc/sm100_ptx.cuh"
+
+using namespace ollie;
+
+__global__ void __launch_bounds__(128, 1) bench(int N, int chunks, int sbo, int xb, int mt, int bpertap, long long *out) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    for (int i = threadIdx.x; i < 190 * 1024 / 4; i += blockDim.x) {
+        uint32_t h = (uint32_t)i * 2654435761u + blockIdx.x;
+        h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+        uint32_t lo = ((h & 1) << 15) | ((126u + ((h >> 1) % 3)) << 7) | ((h >> 3) & 0x7F);
+        uint32_t hi = (((h >> 10) & 1) << 15) | ((126u + ((h >> 11) % 3)) << 7) | ((h >> 14) & 0x7F);
+        reinterpret_cast<uint32_t *>(smem)[i] = lo | (hi << 16);
+    }
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x < 32) tmem_alloc<512>(&tslot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xffffffffu, tslot, 0);
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0);
+    if (warp == 1) {
+        const uint32_t idesc = make_idesc(false, 128, (uint32_t)N);
+        const uint64_t tpl = ((uint64_t)1 << 16) | ((uint64_t)((uint32_t)sbo >> 4) << 32) | ((uint64_t)1 << 46) |
+                             ((uint64_t)2 << 61);
+        const uint32_t a16 = smem_u32(smem) >> 4, b16 = smem_u32(smem + 100 * 1024) >> 4;
+        const uint64_t da0 = tpl | a16, db0 = tpl | b16;
+        const uint64_t dbn = (((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
+                              ((uint64_t)2 << 61)) | b16;
+        const uint32_t mstride16 = (uint32_t)(16 * xb) * 8u;    // stacked M-tiles: 16 rows of xb patch rows
+        __syncwarp();
+        const long long s0 = clock64();
+        for (int c = 0; c < chunks; ++c) {
+            if (elect_one()) {
+                for (int m = 0; m < mt; ++m) {
+                    const uint32_t dm = tmem + (uint32_t)(m * N);
+#pragma unroll
+                    for (int t = 0; t < 9; ++t) {
+                        const uint64_t da = da0 + (uint64_t)(((t / 3) * xb + (t % 3)) * 8) + (uint64_t)(m * mstride16);
+                        const uint64_t db = dbn + (uint64_t)(bpertap ? t * N * 8 : 0);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) umma<false>(dm, da + 2 * k, db + 2 * k, idesc, (c | t | k) ? 1u : 0u);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        (void)db0;
+        umma_commit_elect(&bar);
+        mbar_wait(&bar, 0);
+        if ((threadIdx.x & 31) == 0) out[blockIdx.x] = clock64() - s0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) { tc_fence_after(); tmem_dealloc<512>(tmem); }
+}
+
+int main() {
+    long long *d;
+    cudaMalloc(&d, 148 * sizeof(long long));
+    cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    struct Cfg { int N, sbo, xb, mt, bpt; const char *what; };
+    const Cfg cfgs[] = {
+        {64, 1024, 16, 1, 1, "SBO 1024, patch width 16 (microbenchmark layout)"},
+        {64, 1024, 10, 1, 1, "SBO 1024, patch width 10 (lanes over consecutive rows)"},
+        {64, 1280, 10, 1, 1, "SBO 1280 = grp8 with Xb = 10"},
+        {64, 1536, 12, 1, 1, "SBO 1536 = grp8 with Xb = 12 (CSRNet)"},
+        {64, 1280, 10, 2, 1, "grp8 Xb = 10, MT = 2"},
+        {64, 1024, 10, 2, 1, "SBO 1024, Xb = 10, MT = 2"},
+        {64, 1280, 10, 1, 0, "grp8 Xb = 10, one B tile for all taps"},
+        {128, 1024, 16, 1, 1, "N = 128, SBO 1024"},
+        {128, 1280, 10, 1, 1, "N = 128, grp8 Xb = 10"},
+        {256, 1280, 10, 1, 1, "N = 256, grp8 Xb = 10"},
+        {32, 1024, 16, 1, 1, "N = 32, SBO 1024"},
+        {32, 1280, 10, 1, 1, "N = 32, grp8 Xb = 10"},
+    };
+    for (const Cfg &c : cfgs) {
+        const int chunks = 64;
+        bench<<<148, 128, 200 * 1024>>>(c.N, chunks, c.sbo, c.xb, c.mt, c.bpt, d);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+        long long h[148];
+        cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+        long long mx = 0;
+        for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+        const double nm = (double)chunks * c.mt * 36;
+        printf("N=%3d %-55s %6.1f cyc/mma (math bound %5.1f)\n", c.N, c.what, mx / nm, 128.0 * c.N * 16 * 2 / 8192.0);
+    }
+    return 0;
+}
