@@ -55,10 +55,11 @@ def test_g2bmm_random_tolerance(O, g, form):
     assert _max_rel(got[..., :nw], oracle.g2bmm(a, b, g.W, g.d)) <= TOL[g.dtype]
 
 
-def test_g2bmm_padded_pitch_leaves_padding(O):
+@pytest.mark.parametrize("ldo", [48, 39, 34])          # 16-byte rows; odd pitches (edge-chunk stores)
+def test_g2bmm_padded_pitch_leaves_padding(O, ldo):
     g = CASES[1]
     a, b = syn.g2bmm_inputs(g, 702, exact_int=True)
-    got, nw = _run(O, g, a, b, 0, ldo=48)
+    got, nw = _run(O, g, a, b, 0, ldo=ldo)
     assert np.array_equal(got[..., :nw], _round_like(oracle.g2bmm(a, b, g.W, g.d), g.dtype))
     assert np.isnan(got[..., nw:]).all()
 

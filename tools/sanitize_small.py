@@ -83,5 +83,35 @@ for form in (0, 1):
     for ldo in (41, 48):
         out = torch.empty(1, 300, ldo, dtype=torch.bfloat16, device="cuda")
         O.g2bmm(1, 300, 64, 20, 3, O.BF16, a.cuda(), b.cuda(), out, ldo, form)
+# round 2: row-streaming (ysum / direct, Conv2d and a sub-pixel ConvT; a 1x1 pad-1 layer whose bottom
+# output row reads no input row), grp8 lanes, the tap-fold eOperator, the 2x2 selective-add fast path
+for lay, plans in ((syn.Layer("rs3", 2, 16, 6, 20, 12, 3, 3, pad=1), (O.PLAN_ROWSTREAM_YSUM, O.PLAN_ROWSTREAM_DIRECT)),
+                   (syn.Layer("rs1p", 3, 64, 5, 19, 8, 1, 1, pad=1), (O.PLAN_ROWSTREAM_YSUM, O.PLAN_ROWSTREAM_DIRECT)),
+                   (syn.Layer("rst", 1, 64, 5, 9, 1, 9, 9, pad=4, stride=2, output_padding=1, transposed=True),
+                    (O.PLAN_ROWSTREAM,))):
+    x, w = syn.layer_inputs(lay, 9)
+    for plan in plans:
+        try:
+            DerivedConv.from_layer(lay, plan=plan, autotune=False).prepare(w.cuda())(x.cuda())
+            torch.cuda.synchronize()
+            print("ran rowstream", lay.name, plan, flush=True)
+        except O.OllieError as e:
+            if e.status != O.E_UNSUPPORTED:
+                raise
+O._lib.ollie_debug_force_grp8(1)
+lay = syn.Layer("g8", 2, 64, 10, 13, 64, 3, 3, pad=2, dilation=2)
+x, w = syn.layer_inputs(lay, 10)
+DerivedConv.from_layer(lay, plan=O.PLAN_FUSED, autotune=False).prepare(w.cuda())(x.cuda())
+O._lib.ollie_debug_force_grp8(-1)
+for (n, h, w_, c, r, s_, pad, st, kp) in ((2, 7, 16, 1, 5, 5, 2, 1, 32), (1, 6, 9, 3, 3, 3, 1, 2, 32)):
+    shp = O.conv_shape(n, c, h, w_, 1, r, s_, pad, st)
+    oh, ow = O.output_hw(shp, False)
+    xx = torch.randn(n, h, w_, c, device="cuda").to(torch.bfloat16)
+    out = torch.empty(n, oh, ow, kp, dtype=torch.bfloat16, device="cuda")
+    O.tap_fold(shp, O.BF16, xx, kp, out)
+shp = O.conv_shape(2, 32, 5, 6, 16, 4, 4, 1, 2)
+T = torch.randn(2 * 5 * 6, 4 * 4 * 16, device="cuda")
+Y = torch.empty(2, 10, 12, 16, device="cuda", dtype=torch.bfloat16)
+O.offset_add(shp, True, T, 4 * 4 * 16, O.BF16, Y)
 torch.cuda.synchronize()
 print("sanitize run ok")
