@@ -386,6 +386,15 @@ static int nb_cap() {   // B ring depth cap (OLLIE_NB_MAX overrides, for experim
     return v;
 }
 
+static int grb_cap() {   // OLLIE_GRB_MAX caps the kernel rows per weight box (experiments: deeper rings)
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("OLLIE_GRB_MAX");
+        v = e ? std::max(1, atoi(e)) : 64;
+    }
+    return v;
+}
+
 static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transposed, FusedArgs *out, int64_t OH,
                               int64_t OW) {
     const int es = tf32 ? 4 : 2;
@@ -560,7 +569,7 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                     if (occ == 2 && MT * acc_cols > 256) continue;
                     // largest weight box (fewest TMA ops) that fits: grb kernel rows per box
                     int na = 0, nb = 0, grb = 0, kc_tiles = 0, ops_item = 0;
-                    for (int g = max_rows; g >= 1; --g) {
+                    for (int g = std::min(max_rows, grb_cap()); g >= 1; --g) {
                         int kt, oi;
                         box_geom(g, &kt, &oi);
                         const int bst = nsb * g * btile;

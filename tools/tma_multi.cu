@@ -19,7 +19,8 @@ __device__ __forceinline__ void bulk1d(void *dst, const void *src, uint32_t byte
 
 constexpr int WIN = 256 * 1024;
 
-__global__ void __launch_bounds__(512, 1) bench(const uint8_t *g, int tile, int ntiles, int nst, int nprod, long long *out) {
+__global__ void __launch_bounds__(512, 1) bench(const uint8_t *g, int tile, int ntiles, int nst, int nprod, int share,
+                                                long long *out) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t full[8][16], empty[8][16];
@@ -31,7 +32,9 @@ __global__ void __launch_bounds__(512, 1) bench(const uint8_t *g, int tile, int 
         fence_barrier_init();
     }
     __syncthreads();
-    const uint8_t *base = g + (size_t)blockIdx.x * WIN;
+    // share: 0 private windows; 1 every CTA reads the same window in the same order; 2 groups of 32
+    // CTAs share a window (the fused kernel's weight boxes: 4 f-slices over 128 CTAs)
+    const uint8_t *base = g + (size_t)(share == 1 ? 0 : share == 2 ? blockIdx.x / 32 : blockIdx.x) * WIN;
     const int per = ntiles / nprod;
     const long long t0 = clock64();
     const int p = warp / 2;                       // producer p = warp 2p, its consumer = warp 2p + 1
@@ -72,19 +75,21 @@ int main() {
     long long *d;
     cudaMalloc(&d, grid * sizeof(long long));
     cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    for (int tile : {8192, 16384, 32768})
-        for (int nprod : {1, 2, 4}) {
+    for (int share : {0, 1, 2})
+    for (int tile : {8192, 16384, 32768, 65536})
+        for (int nprod : {1, 2}) {
+            if (tile == 65536 && nprod == 2) continue;
             const int nst = std::min(16, (192 * 1024 / nprod) / tile);
             if (nst < 2) continue;
             const int ntiles = 512;
-            for (int rep = 0; rep < 2; ++rep) bench<<<grid, 512, 200 * 1024>>>(g, tile, ntiles, nst, nprod, d);
+            for (int rep = 0; rep < 2; ++rep) bench<<<grid, 512, 200 * 1024>>>(g, tile, ntiles, nst, nprod, share, d);
             cudaError_t e = cudaDeviceSynchronize();
             if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
             std::vector<long long> h(grid);
             cudaMemcpy(h.data(), d, grid * sizeof(long long), cudaMemcpyDeviceToHost);
             long long mx = 0;
             for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
-            printf("tile %5d B, %d producer warp(s) x %2d stages: %6.1f B/clk/SM, %5.0f cyc/op\n", tile, nprod, nst,
+            printf("share %d tile %5d B, %d producer warp(s) x %2d stages: %6.1f B/clk/SM, %5.0f cyc/op\n", share, tile, nprod, nst,
                    (double)ntiles * tile / mx, (double)mx * nprod / ntiles);
         }
     return 0;
