@@ -109,9 +109,18 @@ typedef struct {
  *               P:992-996 applied to both tap dimensions).  Plannable for Conv2d stride 1,
  *               dilation 1, f <= 64, s <= 9, the same channel / width limits.
  *               OLLIE_PLAN_ROWSTREAM runs the planner's form: direct when r*s*ceil(c*es/32)
- *               <= 12 MMAs per M-tile, else ysum (else direct). */
+ *               <= 12 MMAs per M-tile, else ysum (else direct).
+ *   SMALL    -- a8 on CUDA cores for layers of at most 2^22 multiply-adds (the paper's motivating
+ *               example): one thread per output element evaluates the fused program
+ *               Y[m, f] = Sum_{i,j} Sum_c X[m + Delta_ij, c] W'[(i,j,f), c] (traversal merging of
+ *               OffsetAdd o Matmul; ConvTranspose2d: the selected taps of each output,
+ *               P:1575-1580) in fp32, taps in (i, j) order, channels in order -- a single launch with
+ *               no tensor-memory setup, for problems whose tensor-core kernels are launch-latency
+ *               bound.  TF32 layers are computed in full fp32 (within the TF32 bar).  No workspace;
+ *               OLLIE_E_UNSUPPORTED above the size limit.  AUTO measures it for such layers. */
 enum { OLLIE_PLAN_AUTO = 0, OLLIE_PLAN_FUSED = 1, OLLIE_PLAN_UNFUSED = 2, OLLIE_PLAN_GEMM_RED = 3,
-       OLLIE_PLAN_ROWSTREAM = 4, OLLIE_PLAN_ROWSTREAM_YSUM = 5, OLLIE_PLAN_ROWSTREAM_DIRECT = 6 };
+       OLLIE_PLAN_ROWSTREAM = 4, OLLIE_PLAN_ROWSTREAM_YSUM = 5, OLLIE_PLAN_ROWSTREAM_DIRECT = 6,
+       OLLIE_PLAN_SMALL = 7 };
 
 /* ---------------------------------------------------------------------------------
  * Versioning and errors

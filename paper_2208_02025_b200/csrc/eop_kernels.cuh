@@ -198,6 +198,72 @@ __global__ void __launch_bounds__(256) selective_add_kernel(OffsetAddArgs a) {
     }
 }
 
+// OLLIE_PLAN_SMALL: the fused derived program on CUDA cores, one thread per output element
+// (b, oh, ow, f) -- Y[m, f] = Sum_{i,j} Sum_c X[m + Delta_ij, c] W'[(i*S+j)*F + f, c], taps in (i, j)
+// order (Conv2d: in-image taps; ConvTranspose2d, dilation 1: the selected taps i = (oh+p) mod st
+// + st*k of the selective addition), channels in order, fp32.  For layers of a few thousand
+// outputs, where the tensor-core kernels' setup (barriers, TMEM, TMA descriptors) dominates.
+struct SmallConvArgs {
+    const void *x, *w;           // NHWC input, W' [(i*S+j)*F + f][C]
+    void *y;
+    int32_t n, H, W, C, F, R, S, pad, st, dil, OH, OW;
+    int64_t items;               // n * OH * OW * F
+    EpiArgs epi;
+};
+
+template <bool kF32, bool kTr>
+__global__ void __launch_bounds__(256) small_conv_kernel(const __grid_constant__ SmallConvArgs a) {
+    pdl_launch_dependents();
+    pdl_wait();
+    for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < a.items; it += (int64_t)gridDim.x * blockDim.x) {
+        const int f = (int)(it % a.F);
+        int64_t px = it / a.F;
+        const int ow = (int)(px % a.OW);
+        const int64_t t = px / a.OW;
+        const int oh = (int)(t % a.OH);
+        const int64_t b = t / a.OH;
+        float acc = 0.f;
+        for (int i = 0; i < a.R; ++i) {
+            int ih;
+            if constexpr (kTr) {
+                const int th = oh + a.pad - i;
+                if (th < 0 || th % a.st) continue;
+                ih = th / a.st;
+            } else {
+                ih = oh * a.st - a.pad + i * a.dil;
+            }
+            if (ih < 0 || ih >= a.H) continue;
+            for (int j = 0; j < a.S; ++j) {
+                int iw;
+                if constexpr (kTr) {
+                    const int tw = ow + a.pad - j;
+                    if (tw < 0 || tw % a.st) continue;
+                    iw = tw / a.st;
+                } else {
+                    iw = ow * a.st - a.pad + j * a.dil;
+                }
+                if (iw < 0 || iw >= a.W) continue;
+                const int64_t xo = ((b * a.H + ih) * a.W + iw) * a.C;
+                const int64_t wo = ((int64_t)(i * a.S + j) * a.F + f) * a.C;
+                if constexpr (kF32) {
+                    const float *xp = reinterpret_cast<const float *>(a.x) + xo;
+                    const float *wq = reinterpret_cast<const float *>(a.w) + wo;
+                    for (int c = 0; c < a.C; ++c) acc = fmaf(__ldg(xp + c), __ldg(wq + c), acc);
+                } else {
+                    const uint16_t *xp = reinterpret_cast<const uint16_t *>(a.x) + xo;
+                    const uint16_t *wq = reinterpret_cast<const uint16_t *>(a.w) + wo;
+                    for (int c = 0; c < a.C; ++c)
+                        acc = fmaf(bf16_bits_to_float(__ldg(xp + c)), bf16_bits_to_float(__ldg(wq + c)), acc);
+                }
+            }
+        }
+        float v[1] = {acc};
+        if (a.epi.on) epi_apply<!kF32, 1>(a.epi, v, it, f, 1);
+        if constexpr (kF32) reinterpret_cast<float *>(a.y)[it] = v[0];
+        else reinterpret_cast<uint16_t *>(a.y)[it] = float_to_bf16_rne(v[0]);
+    }
+}
+
 // GEMM_RED plan, last step: Y = epilogue(acc) in Y's dtype (acc is the fp32 sum the GEMM's
 // reductions produced; 4 channels per thread).
 template <bool kOutBF16>

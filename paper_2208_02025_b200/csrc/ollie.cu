@@ -1366,11 +1366,13 @@ static bool is_identity_offset_add(const ollie_conv_shape *s, int transposed) {
 static int tuned_choice(const ollie_conv_shape *s, bool tf32, int transposed);   // autotune result (0 none)
 
 static int resolve_plan(const ollie_conv_shape *s, ollie_dtype dtype, int plan, int transposed) {
-    if (plan == OLLIE_PLAN_FUSED || plan == OLLIE_PLAN_UNFUSED || plan == OLLIE_PLAN_GEMM_RED || is_rowstream_plan(plan))
+    if (plan == OLLIE_PLAN_FUSED || plan == OLLIE_PLAN_UNFUSED || plan == OLLIE_PLAN_GEMM_RED || is_rowstream_plan(plan) ||
+        plan == OLLIE_PLAN_SMALL)
         return plan;
     const bool tf32 = dtype == OLLIE_TF32;
     const int tc = tuned_choice(s, tf32, transposed);
     if (tc == 3) return OLLIE_PLAN_GEMM_RED;
+    if (tc == OLLIE_PLAN_SMALL) return OLLIE_PLAN_SMALL;
     if (is_rowstream_plan(tc)) return tc;
     if (is_identity_offset_add(s, transposed)) return tc == 1 ? OLLIE_PLAN_FUSED : OLLIE_PLAN_UNFUSED;
     if (tc == 0 && s->w >= 96) {   // untuned: narrow layers over wide rows stream rows (>= 75% of the lanes busy)
@@ -1430,6 +1432,33 @@ static ollie_status run_gemm_red(const ollie_conv_shape *s, int transposed, bool
     return OLLIE_OK;
 }
 
+// OLLIE_PLAN_SMALL (eop_kernels.cuh small_conv_kernel): layers of at most 2^22 multiply-adds
+static bool small_supported(const ollie_conv_shape *s, int transposed, int64_t OH, int64_t OW) {
+    const int64_t macs = s->n * OH * OW * s->f * s->c * s->r * s->s;
+    return macs <= (1ll << 22) && !(transposed && s->dilation != 1) && s->h < 65536 && s->w < 65536 &&
+           OH < 65536 && OW < 65536 && s->c < 65536 && s->f < 65536 && s->r < 256 && s->s < 256;
+}
+static ollie_status run_small(const ollie_conv_shape *s, bool tf32, int transposed, const void *x, const void *wp, void *y,
+                              int64_t OH, int64_t OW, cudaStream_t stream, const EpiArgs *epi) {
+    if (!small_supported(s, transposed, OH, OW))
+        return fail(OLLIE_E_UNSUPPORTED, "small plan: more than 2^22 multiply-adds (or extents too large)");
+    SmallConvArgs a{};
+    a.x = x; a.w = wp; a.y = y;
+    a.n = (int)s->n; a.H = (int)s->h; a.W = (int)s->w; a.C = (int)s->c; a.F = (int)s->f; a.R = (int)s->r; a.S = (int)s->s;
+    a.pad = s->pad; a.st = s->stride; a.dil = s->dilation; a.OH = (int)OH; a.OW = (int)OW;
+    a.items = s->n * OH * OW * s->f;
+    a.epi = epi ? *epi : EpiArgs{};
+    const unsigned g = (unsigned)std::max<int64_t>(std::min<int64_t>(ceil_div(a.items, 256), (int64_t)num_sms() * 8), 1);
+    if (tf32) {
+        if (transposed) CUDA_TRY(launch(small_conv_kernel<true, true>, dim3(g), dim3(256), 0, stream, a));
+        else CUDA_TRY(launch(small_conv_kernel<true, false>, dim3(g), dim3(256), 0, stream, a));
+    } else {
+        if (transposed) CUDA_TRY(launch(small_conv_kernel<false, true>, dim3(g), dim3(256), 0, stream, a));
+        else CUDA_TRY(launch(small_conv_kernel<false, false>, dim3(g), dim3(256), 0, stream, a));
+    }
+    return OLLIE_OK;
+}
+
 static ollie_status derived_layer(const ollie_conv_shape *s, ollie_dtype dtype, const void *x, const void *wp, void *y,
                                   void *ws, size_t ws_bytes, int plan, cudaStream_t stream, int transposed,
                                   const ollie_epilogue *epilogue = nullptr) {
@@ -1460,6 +1489,10 @@ static ollie_status derived_layer(const ollie_conv_shape *s, ollie_dtype dtype, 
     }
     if (is_rowstream_plan(rp)) {
         st = run_rowstream(s, tf32, transposed, x, wp, y, OH, OW, stream, &epi, rowstream_mode_of(rp));
+        return st == OLLIE_OK ? ok() : st;
+    }
+    if (rp == OLLIE_PLAN_SMALL) {
+        st = run_small(s, tf32, transposed, x, wp, y, OH, OW, stream, &epi);
         return st == OLLIE_OK ? ok() : st;
     }
     if (rp == OLLIE_PLAN_FUSED) {
@@ -2064,6 +2097,10 @@ extern "C" ollie_status ollie_plan_describe(const ollie_conv_shape *s, ollie_dty
         snprintf(buf, len,
                  "rowstream %s R=%d S=%d sub=%d N=%d NP=%d ring=%d mtr=%d rowbytes=%d ksteps=%d tmem_rows=%d grid=%d smem=%zu",
                  a.direct ? "direct" : "ysum", a.R, a.S, a.sub, a.N, a.NP, a.ring, a.mtr, a.rowbytes, a.ksteps, a.nt, rowstream_grid(a), rs_smem_bytes(a));
+    } else if (rp == OLLIE_PLAN_SMALL) {
+        if (!small_supported(s, transposed, OH, OW)) return fail(OLLIE_E_UNSUPPORTED, "no small plan");
+        snprintf(buf, len, "small (fused program on CUDA cores, one thread per output, %lld outputs)",
+                 (long long)(s->n * OH * OW * s->f));
     } else if (rp == OLLIE_PLAN_GEMM_RED) {
         snprintf(buf, len, "gemm_red BN=%d (%s as fp32 L2 reductions in the GEMM epilogue) + finish",
                  gemm_bn(s->n * s->h * s->w, s->r * s->s * s->f), transposed ? "selective add" : "OffsetAdd");
@@ -2159,6 +2196,7 @@ static ollie_status autotune_impl(const ollie_conv_shape *s, ollie_dtype dtype, 
                 else if (d[0] == 'r') { e->tuned = 3; hit = true; }
                 else if (d[0] == 's' && rowstream_supported(s, tf32, transposed, OH, OW, 0)) { e->tuned = OLLIE_PLAN_ROWSTREAM_YSUM; hit = true; }
                 else if (d[0] == 'd' && rowstream_supported(s, tf32, transposed, OH, OW, 1)) { e->tuned = OLLIE_PLAN_ROWSTREAM_DIRECT; hit = true; }
+                else if (d[0] == 'c' && small_supported(s, transposed, OH, OW)) { e->tuned = OLLIE_PLAN_SMALL; hit = true; }
             }
             fclose(fp);
             if (hit) {
@@ -2236,29 +2274,34 @@ static ollie_status autotune_impl(const ollie_conv_shape *s, ollie_dtype dtype, 
         t_rs = time_it([&] { return run_rowstream(s, tf32, transposed, x, wp, y, OH, OW, stream, nullptr, 0); });
     if (rowstream_supported(s, tf32, transposed, OH, OW, 1))
         t_rd = time_it([&] { return run_rowstream(s, tf32, transposed, x, wp, y, OH, OW, stream, nullptr, 1); });
+    float t_sm = 1e30f;                   // the CUDA-core program for tiny layers
+    if (small_supported(s, transposed, OH, OW))
+        t_sm = time_it([&] { return run_small(s, tf32, transposed, x, wp, y, OH, OW, stream, nullptr); });
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    const bool any_timed = best < 1e29f || t_unf < 1e29f || t_red < 1e29f || t_rs < 1e29f || t_rd < 1e29f;
+    const bool any_timed = best < 1e29f || t_unf < 1e29f || t_red < 1e29f || t_rs < 1e29f || t_rd < 1e29f || t_sm < 1e29f;
     {
         std::lock_guard<std::mutex> g(g_plan_mu);
         if (!cands.empty()) e->args = cands[best_k >= 0 ? best_k : 0];
         // record a decision only when some plan actually ran and was timed: a failed tuning leaves
         // AUTO to the cost model instead of pinning it to an unmeasured plan
         if (any_timed) {
-            const float t_min = std::min(std::min(std::min(best, t_unf), std::min(t_red, t_rs)), t_rd);
-            if (t_rd == t_min) e->tuned = OLLIE_PLAN_ROWSTREAM_DIRECT;
+            const float t_min = std::min(std::min(std::min(std::min(best, t_unf), std::min(t_red, t_rs)), t_rd), t_sm);
+            if (t_sm == t_min) e->tuned = OLLIE_PLAN_SMALL;
+            else if (t_rd == t_min) e->tuned = OLLIE_PLAN_ROWSTREAM_DIRECT;
             else if (t_rs == t_min) e->tuned = OLLIE_PLAN_ROWSTREAM_YSUM;
             else if (t_red == t_min) e->tuned = 3;
             else e->tuned = (t_unf == t_min || best_k < 0) ? 2 : 1;
         }
     }
-    if (best_us) *best_us = 1e3f * std::min(std::min(std::min(best, t_unf), std::min(t_red, t_rs)), t_rd);
+    if (best_us) *best_us = 1e3f * std::min(std::min(std::min(std::min(best, t_unf), std::min(t_red, t_rs)), t_rd), t_sm);
     if (!any_timed) return fail(OLLIE_E_UNSUPPORTED, "no runnable plan to tune");
     if (tune_file) {
         if (FILE *fp = fopen(tune_file, "a")) {
             const int t = e->tuned;
             fprintf(fp, "%s %s %d\n", key,
-                    t == 1 ? "f" : t == 2 ? "u" : t == 3 ? "r" : t == OLLIE_PLAN_ROWSTREAM_DIRECT ? "d" : "s",
+                    t == 1 ? "f" : t == 2 ? "u" : t == 3 ? "r" : t == OLLIE_PLAN_ROWSTREAM_DIRECT ? "d" :
+                    t == OLLIE_PLAN_SMALL ? "c" : "s",
                     t == 1 ? best_k : 0);
             fclose(fp);
         }

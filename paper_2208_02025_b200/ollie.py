@@ -25,6 +25,7 @@ OK, E_INVALID, E_UNSUPPORTED, E_WORKSPACE, E_OOB, E_ALIGN, E_CUDA = 0, -1, -2, -
 BF16, TF32, FP32 = 0, 1, 2
 PLAN_AUTO, PLAN_FUSED, PLAN_UNFUSED, PLAN_GEMM_RED, PLAN_ROWSTREAM = 0, 1, 2, 3, 4
 PLAN_ROWSTREAM_YSUM, PLAN_ROWSTREAM_DIRECT = 5, 6
+PLAN_SMALL = 7                      # the fused program on CUDA cores, layers of <= 2^22 multiply-adds
 ATOM_ITER, ATOM_FLOORDIV, ATOM_MOD = 0, 1, 2
 OP_PUSH_ACCESS, OP_PUSH_CONST, OP_ADD, OP_MUL, OP_SUB, OP_NEG, OP_MAX, OP_MIN = range(8)
 MAX_DIMS, MAX_TERMS, MAX_ACCESS, MAX_INSTR, MAX_INPUTS = 8, 8, 8, 32, 8

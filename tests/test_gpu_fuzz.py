@@ -60,7 +60,7 @@ def test_fuzz_all_plans_integer_exact(O, lay):
     x, w = syn.layer_inputs(lay, 900, exact_int=True)
     ref = _round_like(_oracle_layer(lay, x, w), lay.dtype)
     ran = 0
-    for plan in (O.PLAN_AUTO, O.PLAN_FUSED, O.PLAN_UNFUSED, O.PLAN_GEMM_RED):
+    for plan in (O.PLAN_AUTO, O.PLAN_FUSED, O.PLAN_UNFUSED, O.PLAN_GEMM_RED, O.PLAN_SMALL):
         try:
             conv = DerivedConv.from_layer(lay, plan=plan).prepare(_dev(w))
             y = conv(_dev(x))
