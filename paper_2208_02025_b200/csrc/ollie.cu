@@ -386,6 +386,14 @@ static int nb_cap() {   // B ring depth cap (OLLIE_NB_MAX overrides, for experim
     return v;
 }
 
+static int na_cap() {   // OLLIE_NA_MAX: deepest patch ring of streamed fused plans (experiments)
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("OLLIE_NA_MAX");
+        v = e ? std::max(2, std::min(16, atoi(e))) : 3;
+    }
+    return v;
+}
 static int grb_cap() {   // OLLIE_GRB_MAX caps the kernel rows per weight box (experiments: deeper rings)
     static int v = -1;
     if (v < 0) {
@@ -579,7 +587,12 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                             na = (int)std::min<int64_t>(4, (bud - wb) / astage);
                             nb = 1;
                         } else {
-                            na = bud >= 3 * astage + 2 * bst ? 3 : 2;
+                            // patch ring depth: a chunk's patch can only be reloaded once every MMA of
+                            // the chunk two stages back retired, so with whole-chunk stages the depth
+                            // decides how much of the L2 latency the MMAs hide (OLLIE_NA_MAX, default 3)
+                            const int na_hi = std::max(2, std::min(na_cap(), base.kchunks * nph * MT));
+                            na = 2;
+                            while (na < na_hi && bud >= (na + 1) * astage + 2 * bst) ++na;
                             nb = std::min(nb_cap(), (bud - na * astage) / bst);
                             if (nb < 2) continue;
                         }
