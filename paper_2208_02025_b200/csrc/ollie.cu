@@ -2300,7 +2300,10 @@ static ollie_status autotune_impl(const ollie_conv_shape *s, ollie_dtype dtype, 
         // AUTO to the cost model instead of pinning it to an unmeasured plan
         if (any_timed) {
             const float t_min = std::min(std::min(std::min(std::min(best, t_unf), std::min(t_red, t_rs)), t_rd), t_sm);
-            if (t_sm == t_min) e->tuned = OLLIE_PLAN_SMALL;
+            // the CUDA-core plan has no tensor-memory / TMA setup: within 15% of the best warm burst it
+            // is also the fastest from a cold L2 (motivating example: 4.3 vs 8.7 us flushed, rowstream
+            // 4.0 vs 4.2 us warm), so it wins those ties
+            if (t_sm == t_min || t_sm <= 1.15f * t_min) e->tuned = OLLIE_PLAN_SMALL;
             else if (t_rd == t_min) e->tuned = OLLIE_PLAN_ROWSTREAM_DIRECT;
             else if (t_rs == t_min) e->tuned = OLLIE_PLAN_ROWSTREAM_YSUM;
             else if (t_red == t_min) e->tuned = 3;
