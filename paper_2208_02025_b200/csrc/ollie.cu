@@ -590,9 +590,14 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                             // patch ring depth: a chunk's patch can only be reloaded once every MMA of
                             // the chunk two stages back retired, so with whole-chunk stages the depth
                             // decides how much of the L2 latency the MMAs hide (OLLIE_NA_MAX, default 3)
+                            // The weight ring turns over once per box, the patch ring once per chunk: a
+                            // third weight stage is worth more than a third patch stage (CSRNet, FS = 256
+                            // pairs: 2 / 3 runs 170 us, 3 / 2 176 us), so the patch ring only deepens
+                            // past 2 while 3 weight stages still fit -- or when they never would.
                             const int na_hi = std::max(2, std::min(na_cap(), base.kchunks * nph * MT));
+                            const int nb_keep = bud >= 2 * astage + 3 * bst ? 3 : 2;
                             na = 2;
-                            while (na < na_hi && bud >= (na + 1) * astage + 2 * bst) ++na;
+                            while (na < na_hi && bud >= (na + 1) * astage + nb_keep * bst) ++na;
                             nb = std::min(nb_cap(), (bud - na * astage) / bst);
                             if (nb < 2) continue;
                         }
