@@ -269,17 +269,20 @@ __global__ void __launch_bounds__(256) eop_affine_transpose_kernel(const __grid_
     }
 }
 
-// 2-byte transpose with 16-byte global accesses: a block moves a 64 (dt) x 64 (dl) tile.  Reads:
-// 8 lanes cover one 128-byte run along dt (input stride 1) with uint4 loads; writes: 8 lanes cover
-// one 128-byte run along dl (output stride 1) with uint4 stores; the tile goes through shared
-// memory as 16-bit elements (row pitch 66 halves the bank conflicts of the column gathers).
-// Used when both dims are multiples of 8 and both base offsets are 16-byte aligned (host-checked).
+// 2-byte transpose with 16-byte global accesses: a block moves a 64 (dt) x TL (dl) tile, TL = 64 or
+// 128.  Reads: 8 lanes cover one 128-byte run along dt (input stride 1) with uint4 loads, TL / 32
+// runs per thread in flight; writes: TL / 8 lanes cover one output run along dl (output stride 1)
+// with uint4 stores; the tile goes through shared memory as 16-bit elements (row pitch TL + 2 halves
+// the bank conflicts of the column gathers).  Used when both dims are multiples of 8 and both base
+// offsets are 16-byte aligned (host-checked); TL = 128 when the dl extent is a multiple of 128 (four
+// loads in flight per thread instead of two: E-b NCHW -> NHWC).
+template <int TL>
 __global__ void __launch_bounds__(256) eop_affine_transpose16_kernel(const __grid_constant__ AffineEop e) {
     pdl_launch_dependents();
     pdl_wait();
-    __shared__ uint16_t tile[64][66];
+    __shared__ uint16_t tile[64][TL + 2];
     const int dl = e.nd_out - 1, dt = e.dt;
-    const int32_t ns_l = (e.w[dl] + 63) / 64;
+    const int32_t ns_l = (e.w[dl] + TL - 1) / TL;
     const int32_t sl = (int32_t)(blockIdx.x % ns_l), tt = (int32_t)(blockIdx.x / ns_l);
     int32_t rest = (int32_t)blockIdx.y;
     int32_t off = e.base;
@@ -299,28 +302,36 @@ __global__ void __launch_bounds__(256) eop_affine_transpose16_kernel(const __gri
     }
     const uint16_t *in = reinterpret_cast<const uint16_t *>(e.in);
     uint16_t *out = reinterpret_cast<uint16_t *>(e.out);
-    const int c8 = threadIdx.x & 7, r = threadIdx.x >> 3;    // 8 lanes x 16 B = one 128-byte run; 32 runs
-    const int32_t l0 = sl * 64, t0 = tt * 64;
+    const int32_t l0 = sl * TL, t0 = tt * 64;
+    {
+        const int c8 = threadIdx.x & 7, r = threadIdx.x >> 3;     // 8 lanes x 16 B = one 128-byte run; 32 runs
+        uint4 v[TL / 32];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {                           // read 64 runs along dt: rows ol = l0 + rr
-        const int rr = r + 32 * h;
-        const int32_t ol = l0 + rr, ot = t0 + 8 * c8;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (ol < e.w[dl] && ot < e.w[dt]) v = __ldg(reinterpret_cast<const uint4 *>(in + off + e.s[dl] * ol + ot));
-        const uint16_t *hv = reinterpret_cast<const uint16_t *>(&v);
+        for (int h = 0; h < TL / 32; ++h) {                     // read TL runs along dt: rows ol = l0 + rr
+            const int rr = r + 32 * h;
+            const int32_t ol = l0 + rr, ot = t0 + 8 * c8;
+            v[h] = make_uint4(0, 0, 0, 0);
+            if (ol < e.w[dl] && ot < e.w[dt]) v[h] = __ldg(reinterpret_cast<const uint4 *>(in + off + e.s[dl] * ol + ot));
+        }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) tile[8 * c8 + k][rr] = hv[k];
+        for (int h = 0; h < TL / 32; ++h) {
+            const uint16_t *hv = reinterpret_cast<const uint16_t *>(&v[h]);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) tile[8 * c8 + k][r + 32 * h] = hv[k];
+        }
     }
     __syncthreads();
+    constexpr int CPR = TL / 8;                                  // 16-byte chunks per output run
+    const int cq = threadIdx.x % CPR, rq = threadIdx.x / CPR;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {                           // write 64 runs along dl: rows ot = t0 + rr
-        const int rr = r + 32 * h;
-        const int32_t ot = t0 + rr, ol = l0 + 8 * c8;
+    for (int h = 0; h < 64 / (256 / CPR); ++h) {                // write 64 runs along dl: rows ot = t0 + rr
+        const int rr = rq + (256 / CPR) * h;
+        const int32_t ot = t0 + rr, ol = l0 + 8 * cq;
         if (ot >= e.w[dt] || ol >= e.w[dl]) continue;
         uint4 v;
         uint16_t *hv = reinterpret_cast<uint16_t *>(&v);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) hv[k] = tile[rr][8 * c8 + k];
+        for (int k = 0; k < 8; ++k) hv[k] = tile[rr][8 * cq + k];
         *reinterpret_cast<uint4 *>(out + obase + ostr[dt] * ot + ol) = v;
     }
 }

@@ -2067,9 +2067,14 @@ extern "C" ollie_status ollie_eop_eval(const ollie_eop *eop, const void *const *
                        aligned16(fe.in) && aligned16(fe.out);
             for (int d = 0; d < fe.nd_out && v16; ++d)
                 if (d != fe.dt && fe.s[d] % 8 != 0) v16 = false;
-            if (v16) {   // 64 x 64 tiles, 16-byte loads and stores
-                const int64_t strips16 = ceil_div(fe.w[dl], 64) * ceil_div(fe.w[fe.dt], 64);
-                CUDA_TRY(launch(eop_affine_transpose16_kernel, dim3((unsigned)strips16, (unsigned)others), dim3(256), 0, s, fe));
+            if (v16) {   // 64 x 64 / 64 x 128 tiles, 16-byte loads and stores
+                if (fe.w[dl] % 128 == 0) {
+                    const int64_t strips16 = ceil_div(fe.w[dl], 128) * ceil_div(fe.w[fe.dt], 64);
+                    CUDA_TRY(launch(eop_affine_transpose16_kernel<128>, dim3((unsigned)strips16, (unsigned)others), dim3(256), 0, s, fe));
+                } else {
+                    const int64_t strips16 = ceil_div(fe.w[dl], 64) * ceil_div(fe.w[fe.dt], 64);
+                    CUDA_TRY(launch(eop_affine_transpose16_kernel<64>, dim3((unsigned)strips16, (unsigned)others), dim3(256), 0, s, fe));
+                }
                 CHECK_LAUNCH();
                 return ok();
             }

@@ -237,6 +237,9 @@ EOPS = {
     # 16-byte transpose path (bf16, every dim a multiple of 8, partial 64 x 64 tiles)
     "transpose_v16": lambda: (ec.transpose_nchw_to_nhwc(2, 72, 16, 40), [(2, 72, 16, 40)]),
     "transpose_v16_partial": lambda: (ec.transpose_nchw_to_nhwc(1, 136, 24, 104), [(1, 136, 24, 104)]),
+    # 64 x 128 tiles (c a multiple of 128), dt partial
+    "transpose_v16_wide": lambda: (ec.transpose_nchw_to_nhwc(2, 256, 6, 24), [(2, 256, 6, 24)]),
+    "transpose_v16_wide2": lambda: (ec.transpose_nchw_to_nhwc(1, 384, 3, 72), [(1, 384, 3, 72)]),
     "channel_pad_big": lambda: (ec.channel_pad(3, 17, 40, 12, 16), [(3, 17, 40, 12)]),
     "flip_pad": lambda: ({"inputs": [{"shape": [5, 37], "pad": [[2, 1], [0, 3]]}],
                           "scopes": [{"trav": [[0, 8], [0, 40]], "sum": [],
