@@ -222,6 +222,52 @@ __global__ void __launch_bounds__(256) eop_affine_rows_kernel(const __grid_const
     }
 }
 
+// Staged narrow rows (channel pads / crops of NHWC rows: FSRCNN's 1 -> 16, 12 -> 16): two collapsed
+// output dims [rows][inner], input row r at base + r * s0 (s0 <= 128 bytes), every row's valid column
+// interval [jlo, jhi) the same.  A block moves kR rows per pass: the contiguous input span of those rows
+// comes in with 16-byte loads (when aligned) into shared memory, the kR * inner outputs leave as
+// consecutive 16-byte stores (one chunk per thread, fully coalesced on both sides).  The one-thread-
+// per-row kernel above wrote each row's 32 bytes as two strided 16-byte stores and read its elements
+// one by one.
+template <typename E>
+__global__ void __launch_bounds__(256) eop_staged_rows_kernel(const __grid_constant__ AffineEop e, int32_t jlo, int32_t jhi,
+                                                             int32_t kR, int32_t vec_in) {
+    pdl_launch_dependents();
+    pdl_wait();
+    constexpr int VE = 16 / (int)sizeof(E);
+    extern __shared__ uint8_t st_smem[];
+    E *sm = reinterpret_cast<E *>(st_smem);
+    const int32_t s0 = e.s[0], inner = e.inner, cpr = inner / VE;
+    const E *in = reinterpret_cast<const E *>(e.in);
+    E *out = reinterpret_cast<E *>(e.out);
+    for (int32_t row0 = blockIdx.x * kR; row0 < e.rows; row0 += gridDim.x * kR) {
+        const int32_t nr = min(kR, e.rows - row0);
+        const int32_t span = (nr - 1) * s0 + jhi;               // input elements the pass reads
+        const E *src = in + e.base + (int64_t)row0 * s0;
+        __syncthreads();                                         // the previous pass's readers are done
+        if (vec_in) {
+            for (int32_t t = threadIdx.x; t < (span + VE - 1) / VE; t += blockDim.x)
+                reinterpret_cast<uint4 *>(sm)[t] = __ldg(reinterpret_cast<const uint4 *>(src) + t);
+        } else {
+            for (int32_t t = threadIdx.x; t < span; t += blockDim.x) sm[t] = __ldg(src + t);
+        }
+        __syncthreads();
+        E *dst = out + (int64_t)row0 * inner;
+        for (int32_t q = threadIdx.x; q < nr * cpr; q += blockDim.x) {
+            const int32_t r = q / cpr, j0 = (q - r * cpr) * VE;
+            E v[VE];
+#pragma unroll
+            for (int k = 0; k < VE; ++k) {
+                const int32_t j = j0 + k;
+                v[k] = (j >= jlo && j < jhi) ? sm[r * s0 + j] : E(0);
+            }
+            uint4 pk;
+            memcpy(&pk, v, 16);
+            reinterpret_cast<uint4 *>(dst)[q] = pk;
+        }
+    }
+}
+
 // Tiled transpose: the output's innermost dim (dl) is strided in the input and dim dt has input
 // stride 1.  A block moves a 32 (dt) x 128 (dl) strip as four 32 x 32 tiles through shared
 // memory, so both the reads (along dt) and the writes (along dl) are coalesced; same-dtype moves

@@ -2039,6 +2039,35 @@ extern "C" ollie_status ollie_eop_eval(const ollie_eop *eop, const void *const *
             const int64_t blocks = std::min<int64_t>(ceil_div((int64_t)fe.rows * vec_per_row, 256), (int64_t)num_sms() * 32);
             const unsigned gb = (unsigned)std::max<int64_t>(blocks, 1);
             static const int rows_mode = [] { const char *e = getenv("OLLIE_EOP_ROWS"); return e ? atoi(e) : 1; }();
+            // staged rows: [rows][inner] with contiguous input rows and one valid column interval for all rows
+            if (rows_mode && fe.in_bf16 == fe.out_bf16 && fe.nd_out == 2 && fe.s[1] == 1 && fe.s[0] > 0 &&
+                fe.s[0] * (fe.in_bf16 ? 2 : 4) <= 128 && fe.inner * (fe.in_bf16 ? 2 : 4) % 16 == 0 && aligned16(fe.out)) {
+                int32_t jlo = 0, jhi = fe.inner;
+                bool uniform = true;
+                for (int k = 0; k < fe.nd_in && uniform; ++k) {
+                    if (!(fe.chk & (1 << k))) continue;
+                    const int32_t c = fe.a[k][1], b = fe.b[k], n = fe.shape[k];
+                    if (fe.a[k][0] != 0 || (c != 0 && c != 1)) { uniform = false; break; }
+                    if (c == 0) { if (b < 0 || b >= n) jhi = 0; }
+                    else { jlo = std::max(jlo, -b); jhi = std::min(jhi, n - b); }
+                }
+                // the span a pass reads: from row0's element 0 to the last row's column jhi
+                if (uniform && jhi > jlo && jlo >= 0 && fe.base >= 0) {
+                    const int es = fe.in_bf16 ? 2 : 4, ve = 16 / es;
+                    const int32_t kR = std::max(1, 8192 / (fe.inner * es));          // 8 KB of output per pass
+                    const size_t smem = (size_t)(((int64_t)(kR - 1) * fe.s[0] + jhi + ve) * es + 16);
+                    const bool vin = ((int64_t)fe.base * es) % 16 == 0 && ((int64_t)kR * fe.s[0] * es) % 16 == 0 &&
+                                     aligned16(fe.in);
+                    const int64_t passes = ceil_div((int64_t)fe.rows, kR);
+                    const unsigned g = (unsigned)std::max<int64_t>(std::min<int64_t>(passes, (int64_t)num_sms() * 8), 1);
+                    if (smem <= 48 * 1024) {
+                        if (fe.in_bf16) CUDA_TRY(launch(eop_staged_rows_kernel<uint16_t>, dim3(g), dim3(256), smem, s, fe, jlo, jhi, kR, (int32_t)vin));
+                        else CUDA_TRY(launch(eop_staged_rows_kernel<uint32_t>, dim3(g), dim3(256), smem, s, fe, jlo, jhi, kR, (int32_t)vin));
+                        CHECK_LAUNCH();
+                        return ok();
+                    }
+                }
+            }
             if (rows_mode && fe.in_bf16 == fe.out_bf16 && fe.inner <= 64 && fe.inner * (fe.in_bf16 ? 2 : 4) % 16 == 0 &&
                 aligned16(fe.out)) {
                 // narrow 16-byte-multiple rows: one thread per row
