@@ -285,6 +285,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                 const FusedClass &cl = a.cls[tc.cls * a.nph + (q - kc * a.nph)];
                 for (int g = 0; g < cl.ngroups && g < a.nb; ++g) {
                     mbar_wait(&b_empty[bs], bp ^ 1);
+                    if (g == 0) FC_TRACE(26);                        // step 0's weights issued (debug trace)
                     if (leader) mbar_arrive_expect_tx(&b_full[bs], xmul * (uint32_t)a.b_stage_bytes);
                     uint8_t *dstB = sB + bs * a.b_stage_bytes;
                     const int wi = cl.wi0 + g * a.grb * a.westr;
@@ -324,6 +325,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                     if (!a.resident) {
                         for (int g = (item == cid && qi == 0) ? pre_b : 0; g < cl.ngroups; ++g) {
                             mbar_wait(&b_empty[bs], bp ^ 1);
+                            if (item == cid && qi == 1 && g == 0) FC_TRACE(27);   // step 1's weights issued (debug trace)
                             if (leader) mbar_arrive_expect_tx(&b_full[bs], xmul * (uint32_t)a.b_stage_bytes);
                             uint8_t *dstB = sB + bs * a.b_stage_bytes;
                             const int wi = cl.wi0 + g * a.grb * a.westr;

@@ -77,6 +77,10 @@ for k, b in enumerate(bufs):
         steps.append(f"q{qi}: A {rel(8 + 3 * qi).median().item():5.2f} B {rel(9 + 3 * qi).median().item():5.2f} "
                      f"issued {rel(10 + 3 * qi).median().item():5.2f}")
     print("   steps (med us):", " | ".join(steps))
+    # producer side: when each of the first steps' weight boxes could be issued (its b_empty wait returned)
+    bi = [f"q{qi}: {rel(26 + qi).median().item():5.2f}" for qi in range(2) if not (t[:, 26 + qi] == 0).all()]
+    if bi:
+        print("   producer, weights issued (med us):", " | ".join(bi))
     print(f"   barrier check: thread0 saw epilogue flag in {(t[:, 28] == 0xD0E).sum().item()}/{t.shape[0]} CTAs; "
           f"thread128 post-barrier med {rel(29).median().item():5.2f} vs thread0 {rel(31).median().item():5.2f}")
 
