@@ -107,6 +107,7 @@ struct FusedArgs {
     EpiArgs epi;                      // NEXT-3 element-wise epilogue (bias / residual / ReLU / PReLU)
     long long *trace;                 // debug only (nullptr in production): per-CTA timestamps
     int32_t dbg;                      // debug only (0 in production): 1 skip MMAs, 2 tap offsets 0, 4 skip Y stores, 8 B tile 0
+    int32_t split_prod;               // 1: patches issued by warp 0, weight boxes by warp 3
     FusedClass cls[FC_MAX_CLASSES];
 };
 
@@ -246,9 +247,12 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
     if (threadIdx.x == 0) FC_TRACE(0);
     if (threadIdx.x == 0) pdl_launch_dependents();   // the next layer may start its prologue
 
-    if (warp == 0) {
+    if (warp == 0 || (warp == 3 && a.split_prod)) {
         if (lane == 0) {
             // ===== TMA producer: per work item, per channel chunk: 1 patch + the class's weight tiles =====
+            // split_prod: warp 0 issues the patches, warp 3 the weight boxes (a CTA's TMA issues block
+            // behind earlier loads in flight; two issuing warps keep both rings fed)
+            const bool doA = warp == 0, doB = !a.split_prod || warp == 3;
             int as = 0, bs = 0;
             uint32_t ap = 0, bp = 0;
             // pair mode: both CTAs' loads complete on the LEADER's full barriers, which the leader
@@ -258,7 +262,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             // Weights are read-only for the whole stream (the weight DLT never triggers its dependents
             // early, ollie.h), so their smem loads go out BEFORE griddepcontrol.wait and overlap the
             // previous kernel's tail: the resident slice, or the first step's weight boxes.
-            if (a.resident && cid < a.num_items) {
+            if (doB && a.resident && cid < a.num_items) {
                 // the CTA's f-slice is fixed (pair count is a multiple of f_slices): load it once
                 const TileCoord tc0 = fc_work<kPair>(a, cid, rank);
                 if (leader) mbar_arrive_expect_tx(&b_full[0], xmul * (uint32_t)b_region);
@@ -278,7 +282,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                     }
             }
             int pre_b = 0;                   // weight boxes of the first step already issued
-            if (!a.resident && cid < a.num_items) {
+            if (doB && !a.resident && cid < a.num_items) {
                 const TileCoord tc = fc_work<kPair>(a, cid, rank);
                 const int q = ks > 1 ? q_lo : (cid / a.max_taps) % nq_all;
                 const int kc = q / a.nph;
@@ -297,8 +301,10 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                     ++pre_b;
                 }
             }
-            pdl_wait();
-            FC_TRACE(2);
+            if (doA) {                       // X may be written by the previous kernel (weights are not)
+                pdl_wait();
+                FC_TRACE(2);
+            }
             for (int item = cid; item < a.num_items; item += ncl) {
                 const TileCoord tc = fc_work<kPair>(a, item, rank);
                 // steps (kc, ph): channel chunk kc of input phase ph -- one patch, that phase's taps.
@@ -309,6 +315,7 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                     const int kc = q / a.nph;
                     const FusedClass &cl = a.cls[tc.cls * a.nph + (q - kc * a.nph)];
                     const int xin = a.ist * tc.x0 + cl.px, yin = a.ist * tc.y0 + cl.py;
+                    if (doA) {
                     mbar_wait(&a_empty[as], ap ^ 1);
                     if (leader) mbar_arrive_expect_tx(&a_full[as], xmul * (uint32_t)a.a_box_bytes);
                     uint8_t *dstA = sA + as * a.a_stage_bytes;
@@ -322,7 +329,8 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                             tma_load_5d(dstA, &tmX, &a_full[as], 0, xin, tc.img, yin, kc * (a.BK / CI));
                     }
                     if (++as == a.na) { as = 0; ap ^= 1; }
-                    if (!a.resident) {
+                    }
+                    if (doB && !a.resident) {
                         for (int g = (item == cid && qi == 0) ? pre_b : 0; g < cl.ngroups; ++g) {
                             mbar_wait(&b_empty[bs], bp ^ 1);
                             if (item == cid && qi == 1 && g == 0) FC_TRACE(27);   // step 1's weights issued (debug trace)
@@ -342,11 +350,11 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
             if constexpr (kPair) {
                 // producer tail: every stage's last release (a multicast commit from the leader)
                 // has landed before this CTA may exit
-                for (int i = 0; i < a.na; ++i) {
+                for (int i = 0; i < (doA ? a.na : 0); ++i) {
                     mbar_wait(&a_empty[as], ap ^ 1);
                     if (++as == a.na) { as = 0; ap ^= 1; }
                 }
-                if (!a.resident)
+                if (doB && !a.resident)
                     for (int i = 0; i < a.nb; ++i) {
                         mbar_wait(&b_empty[bs], bp ^ 1);
                         if (++bs == a.nb) { bs = 0; bp ^= 1; }

@@ -394,6 +394,14 @@ static int na_cap() {   // OLLIE_NA_MAX: deepest patch ring of streamed fused pl
     }
     return v;
 }
+static int split_prod_env() {   // OLLIE_FC_SPLIT_PROD=0/1 forces the producer split, else the plan's
+    static int v = -2;
+    if (v == -2) {
+        const char *e = getenv("OLLIE_FC_SPLIT_PROD");
+        v = e ? (atoi(e) ? 1 : 0) : -1;
+    }
+    return v;
+}
 static int grb_cap() {   // OLLIE_GRB_MAX caps the kernel rows per weight box (experiments: deeper rings)
     static int v = -1;
     if (v < 0) {
@@ -409,6 +417,9 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
     if ((s->c * es) % 16 != 0) return false;
     if (s->n > INT32_MAX || s->h > 32768 || s->w > 32768 || s->c > 65535 || s->f > 65535) return false;
     FusedArgs base{};
+    // patches from warp 0, weight boxes from warp 3: A/B on recorded plans (OLLIE_FC_SPLIT_PROD=0/1) --
+    // ResNet-18 78.5 -> 77.1, stride-2 44.7 -> 42.3, InfoGAN 15.2 -> 14.4, CSRNet 173.7 -> 171.6 us
+    base.split_prod = 1;
     int span_y, span_x, max_taps, nclass, taps_item;
     int64_t GH, GW;                               // class-grid (tile space) extent
     PhaseGeom pg{};
@@ -935,6 +946,7 @@ static ollie_status run_fused(const ollie_conv_shape *s, bool tf32, int transpos
         }
         a.dbg = dbg;
     }
+    if (split_prod_env() >= 0) a.split_prod = split_prod_env();
     PFN_encodeTiled enc = get_encode();
     if (!enc) return fail(OLLIE_E_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
     const int es = tf32 ? 4 : 2, CI = 16 / es;
