@@ -11,11 +11,21 @@
 
 using namespace ollie;
 
-__global__ void __launch_bounds__(128, 1) bench(int N, int chunks, int sbo, int xb, int mt, int bpertap, long long *out) {
+__device__ __forceinline__ void bulk1d_(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// stream > 0: warp 2 keeps 32 KB bulk copies (L2-resident source) landing in a 2-stage ring at smem
+// offset 128 KB while the MMAs run (the fused kernel's loads next to its MMAs)
+__global__ void __launch_bounds__(128, 1) bench(int N, int chunks, int sbo, int xb, int mt, int bpertap, long long *out,
+                                               const uint8_t *gsrc = nullptr, int stream = 0) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar, sfull[2];
     __shared__ uint32_t tslot;
+    __shared__ volatile int stop;
     for (int i = threadIdx.x; i < 190 * 1024 / 4; i += blockDim.x) {
         uint32_t h = (uint32_t)i * 2654435761u + blockIdx.x;
         h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
@@ -23,7 +33,7 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int chunks, int sbo, int 
         uint32_t hi = (((h >> 10) & 1) << 15) | ((126u + ((h >> 11) % 3)) << 7) | ((h >> 14) & 0x7F);
         reinterpret_cast<uint32_t *>(smem)[i] = lo | (hi << 16);
     }
-    if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&sfull[0], 1); mbar_init(&sfull[1], 1); stop = 0; fence_barrier_init(); }
     fence_proxy_async_smem();
     __syncthreads();
     if (threadIdx.x < 32) tmem_alloc<512>(&tslot);
@@ -36,7 +46,7 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int chunks, int sbo, int 
         const uint32_t idesc = make_idesc(false, 128, (uint32_t)N);
         const uint64_t tpl = ((uint64_t)1 << 16) | ((uint64_t)((uint32_t)sbo >> 4) << 32) | ((uint64_t)1 << 46) |
                              ((uint64_t)2 << 61);
-        const uint32_t a16 = smem_u32(smem) >> 4, b16 = smem_u32(smem + 100 * 1024) >> 4;
+        const uint32_t a16 = smem_u32(smem) >> 4, b16 = smem_u32(smem + 48 * 1024) >> 4;
         const uint64_t da0 = tpl | a16, db0 = tpl | b16;
         const uint64_t dbn = (((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
                               ((uint64_t)2 << 61)) | b16;
@@ -61,7 +71,16 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int chunks, int sbo, int 
         (void)db0;
         umma_commit_elect(&bar);
         mbar_wait(&bar, 0);
-        if ((threadIdx.x & 31) == 0) out[blockIdx.x] = clock64() - s0;
+        if ((threadIdx.x & 31) == 0) { out[blockIdx.x] = clock64() - s0; stop = 1; }
+    } else if (warp == 2 && stream && (threadIdx.x & 31) == 0) {
+        uint32_t ph[2] = {0, 0};
+        long long n = 0;
+        for (int s = 0; !stop; s ^= 1, ++n) {
+            if (n >= 2) { mbar_wait(&sfull[s], ph[s]); ph[s] ^= 1; }
+            mbar_arrive_expect_tx(&sfull[s], 32768);
+            bulk1d_(smem + 128 * 1024 + s * 32768, gsrc + (size_t)blockIdx.x * 262144 + (size_t)(n & 7) * 32768, 32768, &sfull[s]);
+        }
+        for (int s = 0; s < 2; ++s) if (n > s) mbar_wait(&sfull[s], ph[s]);
     }
     tc_fence_before();
     __syncthreads();
@@ -73,6 +92,22 @@ int main() {
     cudaMalloc(&d, 148 * sizeof(long long));
     cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     struct Cfg { int N, sbo, xb, mt, bpt; const char *what; };
+    uint8_t *gsrc;
+    cudaMalloc(&gsrc, (size_t)148 * 262144);
+    cudaMemset(gsrc, 1, (size_t)148 * 262144);
+    for (int stream : {0, 1})
+        for (int N : {64, 128, 256}) {
+            const int chunks = 64;
+            bench<<<148, 128, 200 * 1024>>>(N, chunks, 1024, 16, 1, N == 256 ? 0 : 1, d, gsrc, stream);
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+            long long h[148];
+            cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+            long long mx = 0;
+            for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+            printf("N=%3d %s %6.1f cyc/mma\n", N, stream ? "with a concurrent 32 KB bulk-copy stream:" : "alone:                                   ",
+                   mx / (chunks * 36.0));
+        }
     const Cfg cfgs[] = {
         {64, 1024, 16, 1, 1, "SBO 1024, patch width 16 (microbenchmark layout)"},
         {64, 1024, 10, 1, 1, "SBO 1024, patch width 10 (lanes over consecutive rows)"},
