@@ -106,7 +106,8 @@ struct FusedArgs {
     void *y;
     EpiArgs epi;                      // NEXT-3 element-wise epilogue (bias / residual / ReLU / PReLU)
     long long *trace;                 // debug only (nullptr in production): per-CTA timestamps
-    int32_t dbg;                      // debug only (0 in production): 1 skip MMAs, 2 tap offsets 0, 4 skip Y stores, 8 B tile 0
+    int32_t dbg;                      // debug only (0 in production): 1 skip MMAs, 2 tap offsets 0, 4 skip Y stores, 8 B tile 0,
+                                      // 128 no weight loads, 256 no patch loads
     int32_t split_prod;               // 1: patches issued by warp 0, weight boxes by warp 3
     FusedClass cls[FC_MAX_CLASSES];
 };
@@ -163,6 +164,22 @@ template <bool kPair>
 __device__ __forceinline__ TileCoord fc_work(const FusedArgs &a, int item, int rank) {
     if constexpr (kPair) return fc_tile_pair(a, item, rank);
     else return fc_tile(a, item);
+}
+
+// Producer-side barrier wait; debug builds with FusedArgs::dbg bit 512 poll with a nanosleep back-off
+// instead of spinning in try_wait (ablation: do spinning warps slow the MMA warp?)
+__device__ __forceinline__ void fc_pwait(uint64_t *bar, uint32_t parity, int dbg) {
+    if (OLLIE_FC_DEBUG && (dbg & 512)) {
+        uint32_t ok = 0;
+        while (true) {
+            asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                         "selp.u32 %0, 1, 0, P1;\n}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+            if (ok) break;
+            __nanosleep(200);
+        }
+    } else {
+        mbar_wait(bar, parity);
+    }
 }
 
 template <bool kTF32, bool kPair, bool kOneEntry, bool kSplit>
@@ -288,8 +305,14 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                 const int kc = q / a.nph;
                 const FusedClass &cl = a.cls[tc.cls * a.nph + (q - kc * a.nph)];
                 for (int g = 0; g < cl.ngroups && g < a.nb; ++g) {
-                    mbar_wait(&b_empty[bs], bp ^ 1);
+                    fc_pwait(&b_empty[bs], bp ^ 1, a.dbg);
                     if (g == 0) FC_TRACE(26);                        // step 0's weights issued (debug trace)
+                    if (OLLIE_FC_DEBUG && (a.dbg & 128)) {           // debug: no weight loads (stale smem)
+                        mbar_arrive(&b_full[bs]);
+                        if (++bs == a.nb) { bs = 0; bp ^= 1; }
+                        ++pre_b;
+                        continue;
+                    }
                     if (leader) mbar_arrive_expect_tx(&b_full[bs], xmul * (uint32_t)a.b_stage_bytes);
                     uint8_t *dstB = sB + bs * a.b_stage_bytes;
                     const int wi = cl.wi0 + g * a.grb * a.westr;
@@ -315,8 +338,12 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                     const int kc = q / a.nph;
                     const FusedClass &cl = a.cls[tc.cls * a.nph + (q - kc * a.nph)];
                     const int xin = a.ist * tc.x0 + cl.px, yin = a.ist * tc.y0 + cl.py;
-                    if (doA) {
-                    mbar_wait(&a_empty[as], ap ^ 1);
+                    if (doA && OLLIE_FC_DEBUG && (a.dbg & 256)) {   // debug: no patch loads (stale smem)
+                        fc_pwait(&a_empty[as], ap ^ 1, a.dbg);
+                        mbar_arrive(&a_full[as]);
+                        if (++as == a.na) { as = 0; ap ^= 1; }
+                    } else if (doA) {
+                    fc_pwait(&a_empty[as], ap ^ 1, a.dbg);
                     if (leader) mbar_arrive_expect_tx(&a_full[as], xmul * (uint32_t)a.a_box_bytes);
                     uint8_t *dstA = sA + as * a.a_stage_bytes;
                     if (a.sw128) {
@@ -332,8 +359,13 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                     }
                     if (doB && !a.resident) {
                         for (int g = (item == cid && qi == 0) ? pre_b : 0; g < cl.ngroups; ++g) {
-                            mbar_wait(&b_empty[bs], bp ^ 1);
+                            fc_pwait(&b_empty[bs], bp ^ 1, a.dbg);
                             if (item == cid && qi == 1 && g == 0) FC_TRACE(27);   // step 1's weights issued (debug trace)
+                            if (OLLIE_FC_DEBUG && (a.dbg & 128)) {   // debug: no weight loads (stale smem)
+                                mbar_arrive(&b_full[bs]);
+                                if (++bs == a.nb) { bs = 0; bp ^= 1; }
+                                continue;
+                            }
                             if (leader) mbar_arrive_expect_tx(&b_full[bs], xmul * (uint32_t)a.b_stage_bytes);
                             uint8_t *dstB = sB + bs * a.b_stage_bytes;
                             const int wi = cl.wi0 + g * a.grb * a.westr;
@@ -351,12 +383,12 @@ fused_conv_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant
                 // producer tail: every stage's last release (a multicast commit from the leader)
                 // has landed before this CTA may exit
                 for (int i = 0; i < (doA ? a.na : 0); ++i) {
-                    mbar_wait(&a_empty[as], ap ^ 1);
+                    fc_pwait(&a_empty[as], ap ^ 1, a.dbg);
                     if (++as == a.na) { as = 0; ap ^= 1; }
                 }
                 if (doB && !a.resident)
                     for (int i = 0; i < a.nb; ++i) {
-                        mbar_wait(&b_empty[bs], bp ^ 1);
+                        fc_pwait(&b_empty[bs], bp ^ 1, a.dbg);
                         if (++bs == a.nb) { bs = 0; bp ^= 1; }
                     }
             }

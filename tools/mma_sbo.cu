@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int chunks, int sbo, int 
             bulk1d_(smem + 128 * 1024 + s * 32768, gsrc + (size_t)blockIdx.x * 262144 + (size_t)(n & 7) * 32768, 32768, &sfull[s]);
         }
         for (int s = 0; s < 2; ++s) if (n > s) mbar_wait(&sfull[s], ph[s]);
+        out[gridDim.x + blockIdx.x] = n;        // copies issued while the MMAs ran
     }
     tc_fence_before();
     __syncthreads();
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int chunks, int sbo, int 
 
 int main() {
     long long *d;
-    cudaMalloc(&d, 148 * sizeof(long long));
+    cudaMalloc(&d, 2 * 148 * sizeof(long long));
     cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     struct Cfg { int N, sbo, xb, mt, bpt; const char *what; };
     uint8_t *gsrc;
@@ -105,8 +106,14 @@ int main() {
             cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
             long long mx = 0;
             for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
-            printf("N=%3d %s %6.1f cyc/mma\n", N, stream ? "with a concurrent 32 KB bulk-copy stream:" : "alone:                                   ",
+            long long nc[148];
+            cudaMemcpy(nc, d + 148, sizeof(nc), cudaMemcpyDeviceToHost);
+            double mean_n = 0;
+            for (int i = 0; i < 148; ++i) mean_n += nc[i] / 148.0;
+            printf("N=%3d %s %6.1f cyc/mma", N, stream ? "with a concurrent 32 KB bulk-copy stream:" : "alone:                                   ",
                    mx / (chunks * 36.0));
+            if (stream) printf("   copies meanwhile: %6.1f B/clk per SM", mean_n * 32768.0 / mx);
+            printf("\n");
         }
     const Cfg cfgs[] = {
         {64, 1024, 16, 1, 1, "SBO 1024, patch width 16 (microbenchmark layout)"},
