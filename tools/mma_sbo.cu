@@ -19,11 +19,11 @@ __device__ __forceinline__ void bulk1d_(void *dst, const void *src, uint32_t byt
 
 // stream > 0: warp 2 keeps 32 KB bulk copies (L2-resident source) landing in a 2-stage ring at smem
 // offset 128 KB while the MMAs run (the fused kernel's loads next to its MMAs)
-__global__ void __launch_bounds__(128, 1) bench(int N, int chunks, int sbo, int xb, int mt, int bpertap, long long *out,
-                                               const uint8_t *gsrc = nullptr, int stream = 0) {
+__global__ void __launch_bounds__(256, 1) bench(int N, int chunks, int sbo, int xb, int mt, int bpertap, long long *out,
+                                               const uint8_t *gsrc = nullptr, int stream = 0, int spin = 0) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar, sfull[2];
+    __shared__ uint64_t bar, sfull[2], done_bar;
     __shared__ uint32_t tslot;
     __shared__ volatile int stop;
     for (int i = threadIdx.x; i < 190 * 1024 / 4; i += blockDim.x) {
@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int chunks, int sbo, int 
         uint32_t hi = (((h >> 10) & 1) << 15) | ((126u + ((h >> 11) % 3)) << 7) | ((h >> 14) & 0x7F);
         reinterpret_cast<uint32_t *>(smem)[i] = lo | (hi << 16);
     }
-    if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&sfull[0], 1); mbar_init(&sfull[1], 1); stop = 0; fence_barrier_init(); }
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&sfull[0], 1); mbar_init(&sfull[1], 1); mbar_init(&done_bar, 1); stop = 0; fence_barrier_init(); }
     fence_proxy_async_smem();
     __syncthreads();
     if (threadIdx.x < 32) tmem_alloc<512>(&tslot);
@@ -71,7 +71,10 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int chunks, int sbo, int 
         (void)db0;
         umma_commit_elect(&bar);
         mbar_wait(&bar, 0);
-        if ((threadIdx.x & 31) == 0) { out[blockIdx.x] = clock64() - s0; stop = 1; }
+        if ((threadIdx.x & 31) == 0) { out[blockIdx.x] = clock64() - s0; stop = 1; mbar_arrive(&done_bar); }
+    } else if (spin && (warp == 0 || warp >= 4)) {
+        // the fused kernel's waiting warps: every lane of warps 0 and 4-7 spins in try_wait
+        mbar_wait(&done_bar, 0);
     } else if (warp == 2 && stream && (threadIdx.x & 31) == 0) {
         uint32_t ph[2] = {0, 0};
         long long n = 0;
@@ -96,6 +99,19 @@ int main() {
     uint8_t *gsrc;
     cudaMalloc(&gsrc, (size_t)148 * 262144);
     cudaMemset(gsrc, 1, (size_t)148 * 262144);
+    for (int spin : {0, 1})
+        for (int thr : {128, 256}) {
+            if (spin && thr == 128) continue;
+            bench<<<148, thr, 200 * 1024>>>(64, 64, 1280, 10, 1, 1, d, gsrc, 0, spin);
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+            long long h[148];
+            cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+            long long mx = 0;
+            for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+            printf("N= 64 grp8 Xb=10, %d threads, %s: %6.1f cyc/mma\n", thr, spin ? "warps 0 and 4-7 spinning in try_wait" : "idle warps at the barrier",
+                   mx / (64 * 36.0));
+        }
     for (int stream : {0, 1})
         for (int N : {64, 128, 256}) {
             const int chunks = 64;
