@@ -20,7 +20,8 @@ __device__ __forceinline__ void bulk1d_(void *dst, const void *src, uint32_t byt
 // stream > 0: warp 2 keeps 32 KB bulk copies (L2-resident source) landing in a 2-stage ring at smem
 // offset 128 KB while the MMAs run (the fused kernel's loads next to its MMAs)
 __global__ void __launch_bounds__(256, 1) bench(int N, int chunks, int sbo, int xb, int mt, int bpertap, long long *out,
-                                               const uint8_t *gsrc = nullptr, int stream = 0, int spin = 0) {
+                                               const uint8_t *gsrc = nullptr, int stream = 0, int spin = 0,
+                                               const int *voff = nullptr) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t bar, sfull[2], done_bar;
@@ -51,6 +52,11 @@ __global__ void __launch_bounds__(256, 1) bench(int N, int chunks, int sbo, int 
         const uint64_t dbn = (((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
                               ((uint64_t)2 << 61)) | b16;
         const uint32_t mstride16 = (uint32_t)(16 * xb) * 8u;    // stacked M-tiles: 16 rows of xb patch rows
+        // voff: per-tap descriptor offsets read from global memory (vector registers: the operands then
+        // reach the MMA through R2UR, as in the fused kernel's issue loop)
+        int vo[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) vo[t] = voff ? __ldg(voff + t) : ((t / 3) * xb + (t % 3)) * 8;
         __syncwarp();
         const long long s0 = clock64();
         for (int c = 0; c < chunks; ++c) {
@@ -59,7 +65,7 @@ __global__ void __launch_bounds__(256, 1) bench(int N, int chunks, int sbo, int 
                     const uint32_t dm = tmem + (uint32_t)(m * N);
 #pragma unroll
                     for (int t = 0; t < 9; ++t) {
-                        const uint64_t da = da0 + (uint64_t)(((t / 3) * xb + (t % 3)) * 8) + (uint64_t)(m * mstride16);
+                        const uint64_t da = da0 + (uint64_t)vo[t] + (uint64_t)(m * mstride16);
                         const uint64_t db = dbn + (uint64_t)(bpertap ? t * N * 8 : 0);
 #pragma unroll
                         for (int k = 0; k < 4; ++k) umma<false>(dm, da + 2 * k, db + 2 * k, idesc, (c | t | k) ? 1u : 0u);
@@ -99,6 +105,24 @@ int main() {
     uint8_t *gsrc;
     cudaMalloc(&gsrc, (size_t)148 * 262144);
     cudaMemset(gsrc, 1, (size_t)148 * 262144);
+    {
+        int hv[9];
+        for (int t = 0; t < 9; ++t) hv[t] = ((t / 3) * 10 + (t % 3)) * 8;
+        int *dv;
+        cudaMalloc(&dv, sizeof(hv));
+        cudaMemcpy(dv, hv, sizeof(hv), cudaMemcpyHostToDevice);
+        for (int vec : {0, 1}) {
+            bench<<<148, 128, 200 * 1024>>>(64, 64, 1280, 10, 1, 1, d, gsrc, 0, 0, vec ? dv : nullptr);
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+            long long h[148];
+            cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+            long long mx = 0;
+            for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+            printf("N= 64 grp8 Xb=10, tap offsets %s: %6.1f cyc/mma\n", vec ? "from global memory (vector regs, R2UR)" : "compile-time (uniform)                 ",
+                   mx / (64 * 36.0));
+        }
+    }
     for (int spin : {0, 1})
         for (int thr : {128, 256}) {
             if (spin && thr == 128) continue;
