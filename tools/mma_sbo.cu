@@ -21,10 +21,10 @@ __device__ __forceinline__ void bulk1d_(void *dst, const void *src, uint32_t byt
 // offset 128 KB while the MMAs run (the fused kernel's loads next to its MMAs)
 __global__ void __launch_bounds__(256, 1) bench(int N, int chunks, int sbo, int xb, int mt, int bpertap, long long *out,
                                                const uint8_t *gsrc = nullptr, int stream = 0, int spin = 0,
-                                               const int *voff = nullptr) {
+                                               const int *voff = nullptr, int sync = 0) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar, sfull[2], done_bar;
+    __shared__ uint64_t bar, sfull[2], done_bar, ready, sink[2];
     __shared__ uint32_t tslot;
     __shared__ volatile int stop;
     for (int i = threadIdx.x; i < 190 * 1024 / 4; i += blockDim.x) {
@@ -34,8 +34,11 @@ __global__ void __launch_bounds__(256, 1) bench(int N, int chunks, int sbo, int 
         uint32_t hi = (((h >> 10) & 1) << 15) | ((126u + ((h >> 11) % 3)) << 7) | ((h >> 14) & 0x7F);
         reinterpret_cast<uint32_t *>(smem)[i] = lo | (hi << 16);
     }
-    if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&sfull[0], 1); mbar_init(&sfull[1], 1); mbar_init(&done_bar, 1); stop = 0; fence_barrier_init(); }
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&sfull[0], 1); mbar_init(&sfull[1], 1); mbar_init(&done_bar, 1); mbar_init(&ready, 1);
+                            mbar_init(&sink[0], 1); mbar_init(&sink[1], 1); stop = 0; fence_barrier_init(); }
     fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) mbar_arrive(&ready);      // completes phase 0: waits on parity 0 pass at once
     __syncthreads();
     if (threadIdx.x < 32) tmem_alloc<512>(&tslot);
     tc_fence_before();
@@ -60,6 +63,12 @@ __global__ void __launch_bounds__(256, 1) bench(int N, int chunks, int sbo, int 
         __syncwarp();
         const long long s0 = clock64();
         for (int c = 0; c < chunks; ++c) {
+            if (sync) {   // the fused kernel's per-step protocol: wait A, fence, wait B, fence ... commit, commit
+                mbar_wait_warp(&ready, 0);
+                tc_fence_after();
+                mbar_wait_warp(&ready, 0);
+                tc_fence_after();
+            }
             if (elect_one()) {
                 for (int m = 0; m < mt; ++m) {
                     const uint32_t dm = tmem + (uint32_t)(m * N);
@@ -73,6 +82,11 @@ __global__ void __launch_bounds__(256, 1) bench(int N, int chunks, int sbo, int 
                 }
             }
             __syncwarp();
+            if (sync) {
+                umma_commit_elect(&sink[0]);
+                umma_commit_elect(&sink[1]);
+                __syncwarp();
+            }
         }
         (void)db0;
         umma_commit_elect(&bar);
@@ -111,6 +125,17 @@ int main() {
         int *dv;
         cudaMalloc(&dv, sizeof(hv));
         cudaMemcpy(dv, hv, sizeof(hv), cudaMemcpyHostToDevice);
+        for (int sync : {0, 1}) {
+            bench<<<148, 128, 200 * 1024>>>(64, 64, 1280, 10, 1, 1, d, gsrc, 0, 0, nullptr, sync);
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+            long long h[148];
+            cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+            long long mx = 0;
+            for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+            printf("N= 64 grp8 Xb=10, %s: %6.1f cyc/mma\n", sync ? "per-36-MMA waits + fences + 2 commits    " : "no per-step synchronisation              ",
+                   mx / (64 * 36.0));
+        }
         for (int vec : {0, 1}) {
             bench<<<148, 128, 200 * 1024>>>(64, 64, 1280, 10, 1, 1, d, gsrc, 0, 0, vec ? dv : nullptr);
             cudaError_t e = cudaDeviceSynchronize();
