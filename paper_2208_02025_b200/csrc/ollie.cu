@@ -523,7 +523,7 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
       if (Xb * ist > 256) continue;                // TMA box: <= 256 traversed elements
       // ipt > 1: several images share a tile, patch rows interleaved [y][image][x] (row pitch
       // Xr = ipt * Xb), so every tap is still one row offset -- small images fill the 128 lanes
-      for (int ipt = 1; ipt <= 4; ++ipt) {
+      for (int ipt = 1; ipt <= 16; ++ipt) {   // up to 16 images: 2x2 / 4x4 GAN inputs fill the lanes
         if (ipt > 1 && (GW > XB || base.n < ipt)) break;
         if (g_force_ipt > 0 && ipt != g_force_ipt) continue;
         if (g8 && 16 % ipt) continue;

@@ -67,6 +67,28 @@ def test_ipt_exact(O, force, lay, mode):
     assert np.array_equal(got, _round_like(_oracle_layer(lay, x, w), lay.dtype)), d
 
 
+# up to 16 images per tile (GAN inputs of 2x2 / 4x4 pixels): ragged batches, ConvT classes, both lane
+# layouts, bit-exact in integer mode
+BIG = [
+    syn.Layer("convt_2to4_b17", 17, 64, 2, 2, 48, 4, 4, pad=1, stride=2, transposed=True),
+    syn.Layer("convt_4to8_b9", 9, 64, 4, 4, 32, 4, 4, pad=1, stride=2, transposed=True),
+    syn.Layer("c3_2x2_b16", 16, 64, 2, 2, 64, 3, 3, pad=1),
+    syn.Layer("s2_4to2_b11", 11, 64, 4, 4, 64, 3, 3, pad=1, stride=2),
+]
+
+
+@pytest.mark.parametrize("ipt", [5, 8, 16])
+@pytest.mark.parametrize("lay", BIG, ids=lambda l: l.name)
+def test_ipt_many_images_exact(O, force, lay, ipt):
+    if lay.n < ipt:
+        pytest.skip("batch smaller than ipt")
+    force(ipt, -1, -1)
+    x, w = syn.layer_inputs(lay, 33, exact_int=True)
+    got, d = _run(O, lay, x, w)
+    assert f"ipt={ipt}" in d, d
+    assert np.array_equal(got, _round_like(_oracle_layer(lay, x, w), lay.dtype)), d
+
+
 @pytest.mark.parametrize("lay", LAYERS[:3] + LAYERS[-1:], ids=lambda l: l.name)
 def test_ipt_random(O, force, lay):
     force(2, -1, -1)
