@@ -21,7 +21,7 @@ __device__ __forceinline__ void bulk1d_(void *dst, const void *src, uint32_t byt
 // offset 128 KB while the MMAs run (the fused kernel's loads next to its MMAs)
 __global__ void __launch_bounds__(256, 1) bench(int N, int chunks, int sbo, int xb, int mt, int bpertap, long long *out,
                                                const uint8_t *gsrc = nullptr, int stream = 0, int spin = 0,
-                                               const int *voff = nullptr, int sync = 0) {
+                                               const int *voff = nullptr, int sync = 0, int rot = 1) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t bar, sfull[2], done_bar, ready, sink[2];
@@ -74,8 +74,11 @@ __global__ void __launch_bounds__(256, 1) bench(int N, int chunks, int sbo, int 
                     const uint32_t dm = tmem + (uint32_t)(m * N);
 #pragma unroll
                     for (int t = 0; t < 9; ++t) {
-                        const uint64_t da = da0 + (uint64_t)vo[t] + (uint64_t)(m * mstride16);
-                        const uint64_t db = dbn + (uint64_t)(bpertap ? t * N * 8 : 0);
+                        // rot > 1: the operands rotate over `rot` stage buffers chunk by chunk, as the fused
+                        // kernel's rings do (A stages 24 KB apart, B stages 72 KB apart)
+                        const uint32_t r = rot > 1 ? (uint32_t)(c % rot) : 0u;
+                        const uint64_t da = da0 + (uint64_t)vo[t] + (uint64_t)(m * mstride16) + (uint64_t)(r * (24u * 1024u / 16u));
+                        const uint64_t db = dbn + (uint64_t)(bpertap ? t * N * 8 : 0) + (uint64_t)(r * (72u * 1024u / 16u));
 #pragma unroll
                         for (int k = 0; k < 4; ++k) umma<false>(dm, da + 2 * k, db + 2 * k, idesc, (c | t | k) ? 1u : 0u);
                     }
@@ -125,6 +128,17 @@ int main() {
         int *dv;
         cudaMalloc(&dv, sizeof(hv));
         cudaMemcpy(dv, hv, sizeof(hv), cudaMemcpyHostToDevice);
+        for (int rot : {1, 2}) {
+            bench<<<148, 128, 200 * 1024>>>(64, 64, 1280, 10, 1, 1, d, gsrc, 0, 0, nullptr, 1, rot);
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+            long long h[148];
+            cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+            long long mx = 0;
+            for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+            printf("N= 64 grp8 Xb=10, per-step sync, operands rotating over %d stage buffer(s): %6.1f cyc/mma\n", rot,
+                   mx / (64 * 36.0));
+        }
         for (int sync : {0, 1}) {
             bench<<<148, 128, 200 * 1024>>>(64, 64, 1280, 10, 1, 1, d, gsrc, 0, 0, nullptr, sync);
             cudaError_t e = cudaDeviceSynchronize();
