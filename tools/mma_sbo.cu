@@ -21,10 +21,10 @@ __device__ __forceinline__ void bulk1d_(void *dst, const void *src, uint32_t byt
 // offset 128 KB while the MMAs run (the fused kernel's loads next to its MMAs)
 __global__ void __launch_bounds__(256, 1) bench(int N, int chunks, int sbo, int xb, int mt, int bpertap, long long *out,
                                                const uint8_t *gsrc = nullptr, int stream = 0, int spin = 0,
-                                               const int *voff = nullptr, int sync = 0, int rot = 1) {
+                                               const int *voff = nullptr, int sync = 0, int rot = 1, int gate = 0) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar, sfull[2], done_bar, ready, sink[2];
+    __shared__ uint64_t bar, sfull[2], done_bar, ready, sink[2], ring[8];
     __shared__ uint32_t tslot;
     __shared__ volatile int stop;
     for (int i = threadIdx.x; i < 190 * 1024 / 4; i += blockDim.x) {
@@ -35,7 +35,9 @@ __global__ void __launch_bounds__(256, 1) bench(int N, int chunks, int sbo, int 
         reinterpret_cast<uint32_t *>(smem)[i] = lo | (hi << 16);
     }
     if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&sfull[0], 1); mbar_init(&sfull[1], 1); mbar_init(&done_bar, 1); mbar_init(&ready, 1);
-                            mbar_init(&sink[0], 1); mbar_init(&sink[1], 1); stop = 0; fence_barrier_init(); }
+                            mbar_init(&sink[0], 1); mbar_init(&sink[1], 1);
+                            for (int i = 0; i < 8; ++i) mbar_init(&ring[i], 1);
+                            stop = 0; fence_barrier_init(); }
     fence_proxy_async_smem();
     __syncthreads();
     if (threadIdx.x == 0) mbar_arrive(&ready);      // completes phase 0: waits on parity 0 pass at once
@@ -63,6 +65,11 @@ __global__ void __launch_bounds__(256, 1) bench(int N, int chunks, int sbo, int 
         __syncwarp();
         const long long s0 = clock64();
         for (int c = 0; c < chunks; ++c) {
+            if (gate > 0 && c >= gate) {   // chunk c may start once chunk c - gate's MMAs completed (a gate-deep ring)
+                const int slot = c % gate;
+                mbar_wait_warp(&ring[slot], (uint32_t)(((c - gate) / gate) & 1));
+                tc_fence_after();
+            }
             if (sync) {   // the fused kernel's per-step protocol: wait A, fence, wait B, fence ... commit, commit
                 mbar_wait_warp(&ready, 0);
                 tc_fence_after();
@@ -88,6 +95,10 @@ __global__ void __launch_bounds__(256, 1) bench(int N, int chunks, int sbo, int 
             if (sync) {
                 umma_commit_elect(&sink[0]);
                 umma_commit_elect(&sink[1]);
+                __syncwarp();
+            }
+            if (gate > 0) {
+                umma_commit_elect(&ring[c % gate]);
                 __syncwarp();
             }
         }
@@ -128,6 +139,16 @@ int main() {
         int *dv;
         cudaMalloc(&dv, sizeof(hv));
         cudaMemcpy(dv, hv, sizeof(hv), cudaMemcpyHostToDevice);
+        for (int gate : {1, 2, 3, 4}) {
+            bench<<<148, 128, 200 * 1024>>>(64, 64, 1280, 10, 1, 1, d, gsrc, 0, 0, nullptr, 0, 1, gate);
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+            long long h[148];
+            cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+            long long mx = 0;
+            for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+            printf("N= 64, chunk c gated on the MMA completion (commit) of chunk c-%d: %6.1f cyc/mma\n", gate, mx / (64 * 36.0));
+        }
         for (int rot : {1, 2}) {
             bench<<<148, 128, 200 * 1024>>>(64, 64, 1280, 10, 1, 1, d, gsrc, 0, 0, nullptr, 1, rot);
             cudaError_t e = cudaDeviceSynchronize();
