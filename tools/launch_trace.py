@@ -22,6 +22,12 @@ if DATA == "zero":
 elif DATA == "big":
     x.uniform_(-2, 2); w.uniform_(-2, 2)
 PLAN = int(os.environ.get("PLAN", "0"))   # 0 auto, 1 fused (no autotune)
+FORCE = os.environ.get("FORCE", "")       # "mt,fs,resident,pair,ksplit": force the fused plan family (with PLAN=1)
+if FORCE:
+    mt, fs, res, pr, ks = (int(v) for v in FORCE.split(","))
+    O._lib.ollie_debug_force_plan(mt, fs, res)
+    O._lib.ollie_debug_force_pair(pr)
+    O._lib.ollie_debug_force_ksplit(ks)
 conv = DerivedConv.from_layer(lay, plan=PLAN).prepare(w.cuda())
 xd = x.cuda(); y = conv.new_output()
 conv(xd, y)
