@@ -291,6 +291,7 @@ extern "C" ollie_status ollie_merged_gemm(int64_t M, int64_t N, int64_t K, ollie
 // Tile geometry + f-slice choice for fused_conv_kernel; see fused_conv.cuh for the design.
 static int g_force_mt = 0, g_force_fs = 0, g_force_res = -1;   // debug plan overrides (0 / -1 = auto)
 static int g_force_pair = -1;                                   // debug: -1 auto, 0 single CTAs, 1 CTA pairs
+static int g_force_occ = 0;                                     // debug: 0 auto, else CTAs per SM (1 or 2)
 static int g_force_ks = -1;                                     // debug: -1 auto, else the split-K factor
 static int g_force_ipt = 0;                                     // debug: 0 auto, else images per tile
 static int g_force_g8 = -1;                                     // debug: -1 auto, else the lane layout (grp8)
@@ -565,6 +566,7 @@ static bool plan_fused_search(const ollie_conv_shape *s, bool tf32, int transpos
                 for (int resident = 0; resident <= 1; ++resident) {
                     if (g_force_res >= 0 && resident != g_force_res) continue;
                     if (g_force_pair >= 0 && pair != g_force_pair) continue;
+                    if (g_force_occ > 0 && occ != g_force_occ) continue;
                     if (g_force_ks >= 0 && ksp != g_force_ks) continue;
                     // split-K over a cluster of ksp CTAs (DSMEM reduction): single CTAs, streamed
                     // weights, one M-tile, at least one (chunk, phase) step per CTA
@@ -790,7 +792,7 @@ static std::map<PlanKey, PlanEntry> g_plan_cache;
 static PlanEntry *plan_entry_mut(const ollie_conv_shape *s, bool tf32, int transposed, int64_t OH, int64_t OW) {
     PlanKey k{{s->n, s->c, s->h, s->w, s->f, s->r * 65536 + s->s, s->pad, s->stride * 65536 + s->dilation,
                (int64_t)tf32 * 2 + transposed + 4 * (int64_t)s->output_padding, num_sms(),
-               g_force_mt * 1000 + g_force_fs + 1000000 * g_force_ipt,
+               g_force_mt * 1000 + g_force_fs + 1000000 * g_force_ipt + 100000000ll * g_force_occ,
                ((g_force_res * 16 + g_force_pair) * 16 + g_force_ks) * 16 + g_force_g8}};
     {
         std::lock_guard<std::mutex> g(g_plan_mu);
@@ -2189,6 +2191,8 @@ extern "C" void ollie_debug_force_plan(int mt, int fs, int resident) {
 }
 // Debug hook (not part of include/ollie.h): -1 auto, 0 single-CTA plans only, 1 CTA-pair plans only.
 extern "C" void ollie_debug_force_pair(int pair) { g_force_pair = pair; }
+// Debug hook (not part of include/ollie.h): 0 auto, else the fused plan's CTAs per SM.
+extern "C" void ollie_debug_force_occ(int occ) { g_force_occ = occ; }
 // Debug hook (not part of include/ollie.h): -1 auto, else only plans with this split-K factor.
 extern "C" void ollie_debug_force_ksplit(int ks) { g_force_ks = ks; }
 // Debug hook (not part of include/ollie.h): 0 auto, else only plans with this many images per tile.

@@ -39,8 +39,10 @@ auto(xd, y)
 print(f"{lay.name} auto {graph_time(lambda s: auto(xd, y, s.cuda_stream)):.2f} us  {auto.resolved_plan()}")
 res = []
 G8S = tuple(int(v) for v in os.environ.get("G8S", "-1").split(","))
-for mt, fs, rs, pr, ks, g8 in itertools.product((1, 2, 4), (32, 64, 128, 256), (0, 1), (0, 1), (1, 2, 4), G8S):
+OCCS = tuple(int(v) for v in os.environ.get("OCCS", "0").split(","))   # CTAs per SM (0 = planner's choice)
+for mt, fs, rs, pr, ks, g8, occ in itertools.product((1, 2, 4), (32, 64, 128, 256), (0, 1), (0, 1), (1, 2, 4), G8S, OCCS):
     O._lib.ollie_debug_force_grp8(g8)
+    O._lib.ollie_debug_force_occ(occ)
     O._lib.ollie_debug_force_plan(mt, fs, rs)
     O._lib.ollie_debug_force_pair(pr)
     O._lib.ollie_debug_force_ksplit(ks)
@@ -55,6 +57,7 @@ O._lib.ollie_debug_force_plan(0, 0, -1)
 O._lib.ollie_debug_force_pair(-1)
 O._lib.ollie_debug_force_ksplit(-1)
 O._lib.ollie_debug_force_grp8(-1)
+O._lib.ollie_debug_force_occ(0)
 res.sort()
 for t, d in res[:int(os.environ.get("TOP", "6"))]:
     print(f"   {t:7.2f} us  {d}")
